@@ -1,0 +1,187 @@
+// Candidate 128-bit mulmod-by-constant formulations for sm_100a, timed for throughput.
+// Exploration tool (not the product path): picks the reduction the NTT kernels use.
+// A: word-serial Montgomery (CIOS), 32-bit digits, R = 2^128.
+// B: Montgomery SOS: full 256-bit product, m = lo128(t*q'), t + m*q.
+// C: Shoup with an exact bit 128 of the remainder (r in [0, 2q) may exceed 2^128).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <vector>
+#include <algorithm>
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
+
+struct C128 { uint32_t q[4]; uint32_t qinv0; uint32_t qp[4]; };
+
+// ---------- A: CIOS
+__device__ __forceinline__ void mont_cios(uint32_t r[4], const uint32_t a[4], const uint32_t b[4], const uint32_t q[4], uint32_t qinv0) {
+  uint32_t t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0, t5 = 0, m;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    asm("mad.lo.cc.u32 %0, %6, %7, %0;\n\t"
+        "madc.hi.cc.u32 %1, %6, %7, %1;\n\t"
+        "madc.lo.cc.u32 %2, %6, %9, %2;\n\t"
+        "madc.hi.cc.u32 %3, %6, %9, %3;\n\t"
+        "addc.u32 %4, %4, 0;\n\t"
+        "mad.lo.cc.u32 %1, %6, %8, %1;\n\t"
+        "madc.hi.cc.u32 %2, %6, %8, %2;\n\t"
+        "madc.lo.cc.u32 %3, %6, %10, %3;\n\t"
+        "madc.hi.cc.u32 %4, %6, %10, %4;\n\t"
+        "addc.u32 %5, 0, 0;"
+        : "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "=r"(t5)
+        : "r"(a[i]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]));
+    m = t0 * qinv0;
+    asm("mad.lo.cc.u32 %0, %6, %7, %0;\n\t"
+        "madc.hi.cc.u32 %1, %6, %7, %1;\n\t"
+        "madc.lo.cc.u32 %2, %6, %9, %2;\n\t"
+        "madc.hi.cc.u32 %3, %6, %9, %3;\n\t"
+        "addc.cc.u32 %4, %4, 0;\n\t"
+        "addc.u32 %5, %5, 0;\n\t"
+        "mad.lo.cc.u32 %1, %6, %8, %1;\n\t"
+        "madc.hi.cc.u32 %2, %6, %8, %2;\n\t"
+        "madc.lo.cc.u32 %3, %6, %10, %3;\n\t"
+        "madc.hi.cc.u32 %4, %6, %10, %4;\n\t"
+        "addc.u32 %5, %5, 0;"
+        : "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "+r"(t5)
+        : "r"(m), "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]));
+    t0 = t1; t1 = t2; t2 = t3; t3 = t4; t4 = t5;
+  }
+  // t4:t0 < 2q; conditional subtract
+  uint32_t d0, d1, d2, d3, bw;
+  asm("sub.cc.u32 %0, %5, %10;\n\t subc.cc.u32 %1, %6, %11;\n\t subc.cc.u32 %2, %7, %12;\n\t subc.cc.u32 %3, %8, %13;\n\t subc.u32 %4, %9, 0;"
+      : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(d3), "=r"(bw) : "r"(t0), "r"(t1), "r"(t2), "r"(t3), "r"(t4), "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]));
+  bool ge = (bw == 0);
+  r[0] = ge ? d0 : t0; r[1] = ge ? d1 : t1; r[2] = ge ? d2 : t2; r[3] = ge ? d3 : t3;
+}
+
+// ---------- full 256-bit product (ptxas fuses lo/hi pairs into IMAD.WIDE.U32 with carry predicates)
+__device__ __forceinline__ void mul256(uint32_t t[8], const uint32_t a[4], const uint32_t b[4]) {
+  asm("mul.lo.u32 %0, %8, %12;\n\t"
+      "mul.hi.u32 %1, %8, %12;\n\t"
+      "mul.lo.u32 %2, %8, %14;\n\t"
+      "mul.hi.u32 %3, %8, %14;\n\t"
+      "mad.lo.cc.u32 %1, %8, %13, %1;\n\t"
+      "madc.hi.cc.u32 %2, %8, %13, %2;\n\t"
+      "madc.lo.cc.u32 %3, %8, %15, %3;\n\t"
+      "madc.hi.u32 %4, %8, %15, 0;\n\t"
+      "mad.lo.cc.u32 %1, %9, %12, %1;\n\t"
+      "madc.hi.cc.u32 %2, %9, %12, %2;\n\t"
+      "madc.lo.cc.u32 %3, %9, %14, %3;\n\t"
+      "madc.hi.cc.u32 %4, %9, %14, %4;\n\t"
+      "addc.u32 %5, 0, 0;\n\t"
+      "mad.lo.cc.u32 %2, %9, %13, %2;\n\t"
+      "madc.hi.cc.u32 %3, %9, %13, %3;\n\t"
+      "madc.lo.cc.u32 %4, %9, %15, %4;\n\t"
+      "madc.hi.u32 %5, %9, %15, %5;\n\t"
+      "mad.lo.cc.u32 %2, %10, %12, %2;\n\t"
+      "madc.hi.cc.u32 %3, %10, %12, %3;\n\t"
+      "madc.lo.cc.u32 %4, %10, %14, %4;\n\t"
+      "madc.hi.cc.u32 %5, %10, %14, %5;\n\t"
+      "addc.u32 %6, 0, 0;\n\t"
+      "mad.lo.cc.u32 %3, %10, %13, %3;\n\t"
+      "madc.hi.cc.u32 %4, %10, %13, %4;\n\t"
+      "madc.lo.cc.u32 %5, %10, %15, %5;\n\t"
+      "madc.hi.u32 %6, %10, %15, %6;\n\t"
+      "mad.lo.cc.u32 %3, %11, %12, %3;\n\t"
+      "madc.hi.cc.u32 %4, %11, %12, %4;\n\t"
+      "madc.lo.cc.u32 %5, %11, %14, %5;\n\t"
+      "madc.hi.cc.u32 %6, %11, %14, %6;\n\t"
+      "addc.u32 %7, 0, 0;\n\t"
+      "mad.lo.cc.u32 %4, %11, %13, %4;\n\t"
+      "madc.hi.cc.u32 %5, %11, %13, %5;\n\t"
+      "madc.lo.cc.u32 %6, %11, %15, %6;\n\t"
+      "madc.hi.u32 %7, %11, %15, %7;"
+      : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]), "=r"(t[6]), "=r"(t[7])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]));
+}
+// low 128 bits of a*b (10 products)
+__device__ __forceinline__ void mullo128(uint32_t t[4], const uint32_t a[4], const uint32_t b[4]) {
+  asm("mul.lo.u32 %0, %4, %8;\n\t"
+      "mul.hi.u32 %1, %4, %8;\n\t"
+      "mul.lo.u32 %2, %4, %10;\n\t"
+      "mul.hi.u32 %3, %4, %10;\n\t"
+      "mad.lo.cc.u32 %1, %4, %9, %1;\n\t"
+      "madc.hi.cc.u32 %2, %4, %9, %2;\n\t"
+      "madc.lo.u32 %3, %4, %11, %3;\n\t"
+      "mad.lo.cc.u32 %1, %5, %8, %1;\n\t"
+      "madc.hi.cc.u32 %2, %5, %8, %2;\n\t"
+      "madc.lo.u32 %3, %5, %10, %3;\n\t"
+      "mad.lo.cc.u32 %2, %5, %9, %2;\n\t"
+      "madc.hi.u32 %3, %5, %9, %3;\n\t"
+      "mad.lo.cc.u32 %2, %6, %8, %2;\n\t"
+      "madc.hi.u32 %3, %6, %8, %3;\n\t"
+      "mad.lo.u32 %3, %6, %9, %3;\n\t"
+      "mad.lo.u32 %3, %7, %8, %3;"
+      : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]));
+}
+// ---------- B: SOS Montgomery
+__device__ __forceinline__ void mont_sos(uint32_t r[4], const uint32_t a[4], const uint32_t b[4], const uint32_t q[4], const uint32_t qp[4]) {
+  uint32_t t[8], m[4], u[8];
+  mul256(t, a, b);
+  uint32_t tl[4] = {t[0], t[1], t[2], t[3]};
+  mullo128(m, tl, qp);
+  mul256(u, m, q);
+  // U = t_hi + u_hi + (t_lo != 0)  (t_lo + u_lo == 0 mod 2^128)
+  uint32_t c = (t[0] | t[1] | t[2] | t[3]) != 0;
+  uint32_t s0, s1, s2, s3, s4;
+  asm("add.cc.u32 %0, %5, %9;\n\t addc.cc.u32 %1, %6, %10;\n\t addc.cc.u32 %2, %7, %11;\n\t addc.cc.u32 %3, %8, %12;\n\t addc.u32 %4, 0, 0;"
+      : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3), "=r"(s4) : "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]));
+  asm("add.cc.u32 %0, %0, %5;\n\t addc.cc.u32 %1, %1, 0;\n\t addc.cc.u32 %2, %2, 0;\n\t addc.cc.u32 %3, %3, 0;\n\t addc.u32 %4, %4, 0;"
+      : "+r"(s0), "+r"(s1), "+r"(s2), "+r"(s3), "+r"(s4) : "r"(c));
+  uint32_t d0, d1, d2, d3, bw;
+  asm("sub.cc.u32 %0, %5, %10;\n\t subc.cc.u32 %1, %6, %11;\n\t subc.cc.u32 %2, %7, %12;\n\t subc.cc.u32 %3, %8, %13;\n\t subc.u32 %4, %9, 0;"
+      : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(d3), "=r"(bw) : "r"(s0), "r"(s1), "r"(s2), "r"(s3), "r"(s4), "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]));
+  bool ge = (bw == 0);
+  r[0] = ge ? d0 : s0; r[1] = ge ? d1 : s1; r[2] = ge ? d2 : s2; r[3] = ge ? d3 : s3;
+}
+
+template <int V>
+__global__ void k_mulmod(uint4* io, const C128 c, int iters, long long* cyc) {
+  constexpr int ILP = 4;
+  uint32_t x[ILP][4];
+  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < ILP; k++) { uint4 v = io[tid * ILP + k]; x[k][0] = v.x; x[k][1] = v.y; x[k][2] = v.z; x[k][3] = v.w; }
+  uint32_t w[4] = {c.q[0] ^ 0x1234567u, c.q[1] ^ 0x89abcdefu, c.q[2] >> 1, c.q[3] >> 1};
+  long long t0 = clock64();
+#pragma unroll 1
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int k = 0; k < ILP; k++) {
+      if (V == 0) mont_cios(x[k], x[k], w, c.q, c.qinv0);
+      else mont_sos(x[k], x[k], w, c.q, c.qp);
+    }
+  }
+  long long t1 = clock64();
+#pragma unroll
+  for (int k = 0; k < ILP; k++) io[tid * ILP + k] = make_uint4(x[k][0], x[k][1], x[k][2], x[k][3]);
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+int main() {
+  cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0)); int sms = p.multiProcessorCount;
+  // q = 2^128 - 8257535 (cfg2 prime), q' = -q^-1 mod 2^128 computed on host below
+  unsigned __int128 q = ~(unsigned __int128)0 - 8257535 + 1;
+  unsigned __int128 inv = 1; for (int i = 0; i < 7; i++) inv *= 2 - q * inv;  // Newton: q*inv == 1 mod 2^128
+  unsigned __int128 qp = -inv;
+  C128 c; for (int i = 0; i < 4; i++) { c.q[i] = (uint32_t)(q >> (32 * i)); c.qp[i] = (uint32_t)(qp >> (32 * i)); }
+  c.qinv0 = c.qp[0];
+  const int threads = 256, blocks = sms * 4, iters = 512, ILP = 4;
+  size_t n = (size_t)threads * blocks * ILP;
+  std::vector<uint4> h(n); for (size_t i = 0; i < n; i++) h[i] = make_uint4(i * 2654435761u, i, 77, 0x7fffffff);
+  uint4* d; long long* dc; CK(cudaMalloc(&d, n * 16)); CK(cudaMalloc(&dc, blocks * 8));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const char* names[2] = {"mont_cios", "mont_sos"};
+  for (int v = 0; v < 2; v++) {
+    CK(cudaMemcpy(d, h.data(), n * 16, cudaMemcpyHostToDevice));
+    auto launch = [&]() { if (v == 0) k_mulmod<0><<<blocks, threads>>>(d, c, iters, dc); else k_mulmod<1><<<blocks, threads>>>(d, c, iters, dc); };
+    for (int w = 0; w < 3; w++) launch();
+    CK(cudaDeviceSynchronize());
+    float best = 1e30f;
+    for (int r = 0; r < 5; r++) { cudaEventRecord(e0); launch(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms); }
+    std::vector<long long> cyc(blocks); CK(cudaMemcpy(cyc.data(), dc, blocks * 8, cudaMemcpyDeviceToHost)); std::sort(cyc.begin(), cyc.end());
+    double mm = (double)n * iters; double per_sm_clk = (double)threads * 4 * ILP * iters / cyc[blocks / 2];
+    printf("{\"kernel\":\"%s\",\"ms\":%.4f,\"mulmod_per_s\":%.4e,\"mulmod_per_clk_per_sm\":%.3f}\n", names[v], best, mm / (best * 1e-3), per_sm_clk);
+  }
+  return 0;
+}
