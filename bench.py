@@ -1,0 +1,485 @@
+#!/usr/bin/env python
+"""Benchmark of the 128-bit NTT hot path (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--rows|--no-rows]
+
+Workload (BASELINE.json configs[2], "cfg3"): batched forward + inverse cyclic NTT,
+N = 2^16, 64 polynomials, each with its own 124..128-bit prime q_i = 1 mod 2N (RNS
+limbs), coefficients uniform in [0, q_i) (seeded).  One step = forward + inverse of
+the whole batch through the C ABI (ntt128_forward / ntt128_inverse).  Metric: 128-bit
+NTT butterflies per second (N/2 log2 N per transform, forward and inverse counted).
+
+Multi-GPU (torchrun): every rank transforms its own 64-polynomial batch (independent
+RNS limbs; no data-path collective), value = butterflies of all ranks / max-over-ranks
+time ("scaling": "weak").  Timing: CUDA events on the launching stream, barrier +
+synchronize on both sides, max over ranks.  L2: inputs rotate over 4 disjoint buffer
+sets (each step's input was last touched >= 3 steps, >= 576 MiB of traffic, earlier).
+
+--impl reference runs the oracle (oracle/, the plain CPU implementation written from
+the paper) on this host's cores as the reference arm, on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+PARAMS_PATH = os.path.join(ROOT, "tests", "golden", "params.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+# Roofline constants.  P = algorithmic 32x32->64 products per unit
+# (SURVEY.md §8(d)): 36 per butterfly / constant mulmod, 42 per general mulmod.
+P_BUTTERFLY = 36
+P_GENERAL = 42
+SMS = 148
+IMAD_WIDE_PER_CLK_SM = 32          # measured: profiles/r01/int_rate.jsonl (IMAD.WIDE.U32 half the IMAD rate)
+FALLBACK_HBM_GBS = 6650.0
+
+
+def load_params():
+    with open(PARAMS_PATH) as f:
+        P = json.load(f)
+    return P
+
+
+def hexint(s):
+    return int(s, 16)
+
+
+def peaks():
+    d = {}
+    if os.path.exists(PEAKS_PATH):
+        with open(PEAKS_PATH) as f:
+            d = json.load(f)
+    hbm = d.get("hbm_gbs")
+    sm_max = d.get("sm_max_mhz", 1965.0)
+    return {
+        "hbm_gbs": hbm if hbm else FALLBACK_HBM_GBS,
+        "hbm_src": "measured" if hbm else "fallback",
+        "sm_max_mhz": sm_max,
+        # integer-multiply peak: 148 SMs x 32 IMAD.WIDE.U32 per clock x max SM clock
+        "tprod_s": SMS * IMAD_WIDE_PER_CLK_SM * sm_max * 1e6 / 1e12,
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML samples of SM clock and clock-event reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_setup(ngpus: int):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- workloads
+def cfg3_inputs(P, rank, nsets):
+    mods = P["cfg3"]["moduli"]
+    qs = [hexint(m["q"]) for m in mods]
+    ws = [hexint(m["omega"]) for m in mods]
+    psis = [hexint(m["psi"]) for m in mods]
+    from paper_2509_12494_b200 import synth
+    n = 1 << P["cfg3"]["logn"]
+    sets = []
+    for s in range(nsets):
+        x = np.stack([synth.uniform_residues(qs[i], n, synth.stream_seed(3, 0, (rank << 20) | (s << 8) | i))
+                      for i in range(len(qs))])
+        sets.append(x)
+    return qs, ws, psis, sets
+
+
+def to_dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
+
+
+def time_events(fn, iters, stream):
+    """average ms per call over iters calls, CUDA events on `stream`"""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(iters):
+        fn(i)
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def run_gpu(args):
+    import torch
+    from paper_2509_12494_b200 import ntt128 as N
+
+    rank, world, local = dist_setup(args.gpus)
+    P = load_params()
+    pk = peaks()
+    logn, B = P["cfg3"]["logn"], P["cfg3"]["batch"]
+    n = 1 << logn
+    NSETS = 4
+    qs, ws, psis, sets = cfg3_inputs(P, rank, NSETS)
+    plan = N.Plan(logn, qs, ws, batch=B)
+    X = [to_dev(x) for x in sets]
+    Y = [torch.empty_like(x) for x in X]
+    Z = [torch.empty_like(x) for x in X]
+    stream = torch.cuda.current_stream()
+    bfly_per_transform = (n // 2) * logn
+    bfly_per_step = 2 * B * bfly_per_transform
+
+    def step(i):
+        k = i % NSETS
+        plan.forward(X[k], out=Y[k])
+        plan.inverse(Y[k], out=Z[k])
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    # correctness guard on rank data (round trip) before timing
+    assert torch.equal(Z[(args.warmup - 1) % NSETS], X[(args.warmup - 1) % NSETS]) if args.warmup else True
+
+    # ---------------- timed region: K steps, per-call events for the kernel split
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches0 = N.launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            k = (args.warmup + i) % NSETS
+            ev[i][0].record(stream)
+            plan.forward(X[k], out=Y[k])
+            ev[i][1].record(stream)
+            plan.inverse(Y[k], out=Z[k])
+            ev[i][2].record(stream)
+        t_end.record(stream)
+        t_end.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = N.launch_count() - launches0
+    ms_local = t_start.elapsed_time(t_end)
+    ms = max_over_ranks(ms_local, world)
+    fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    inv_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    ms_per_step = ms / args.steps
+    value = bfly_per_step * world * args.steps / (ms / 1e3)
+
+    # dominant kernel: the NTT pass kernel (k_ntt_pass); one launch = one pass over the batch
+    npasses = plan.info()["num_passes"]
+    launch_ms = (fwd_ms + inv_ms) / (2 * npasses)
+    prod_per_launch = P_BUTTERFLY * B * (n // 2) * (logn / npasses)
+    achieved = prod_per_launch / (launch_ms * 1e-3) / 1e12
+    traffic = None
+    if os.path.exists(TRAFFIC_PATH):
+        try:
+            with open(TRAFFIC_PATH) as f:
+                traffic = json.load(f).get("k_ntt_pass_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": "k_ntt_pass", "achieved": round(achieved, 4), "peak": round(pk["tprod_s"], 4),
+                "unit": "Tprod/s", "frac": round(achieved / pk["tprod_s"], 4), "traffic": traffic,
+                "peak_src": "148 SM x 32 IMAD.WIDE.U32/clk x sm_max_mhz (DESIGN.md §6)",
+                "step_frac": round(value / world * P_BUTTERFLY / 1e12 / pk["tprod_s"], 4)}
+
+    # ---------------- end to end through the public API with host buffers
+    e2e = run_e2e(plan, sets[0], args, stream, bfly_per_step, world)
+
+    rows = run_rows(args, P, pk, stream) if (args.rows and rank == 0) else None
+    cpu = cpu_baseline(P) if (rank == 0 and world == 1 and args.cpu_baseline) else None
+    if rank == 0:
+        out = {
+            "metric": "128-bit NTT butterflies/sec (N=2^16, fwd+inv, 64 RNS primes)",
+            "value": value, "unit": "butterflies/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u128", "data": "synthetic (seeded uniform residues)",
+            "config": {"workload": "cfg3: batched forward+inverse cyclic NTT, N=2^16, batch 64 per GPU, 64 distinct "
+                                   "124-128-bit primes (BASELINE.json configs[2])",
+                       "N": n, "batch_per_gpu": B, "parallelism": f"batch-shard x{world} (no collective)",
+                       "l2": "inputs rotate over 4 disjoint buffer sets (768 MiB footprint > 126 MB L2)",
+                       "passes": npasses},
+            "ntt_per_s": value / bfly_per_transform,
+            "ns_per_butterfly": 1e9 / value,
+            "fwd_ms": fwd_ms, "inv_ms": inv_ms,
+            "roofline": roofline,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "cpu_baseline": cpu,
+        }
+        if rows is not None:
+            out["rows"] = rows
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_e2e(plan, x_host, args, stream, bfly_per_step, world):
+    """same metric end to end: pinned host input -> H2D -> forward -> inverse -> D2H, per step"""
+    import torch
+    hx = torch.from_numpy(np.ascontiguousarray(x_host).view(np.int64)).pin_memory()
+    hz = torch.empty_like(hx).pin_memory()
+    dx = torch.empty(hx.shape, dtype=hx.dtype, device="cuda")
+    dy, dz = torch.empty_like(dx), torch.empty_like(dx)
+
+    def one():
+        dx.copy_(hx, non_blocking=True)
+        plan.forward(dx, out=dy)
+        plan.inverse(dy, out=dz)
+        hz.copy_(dz, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    steps = max(1, args.steps)
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    e1.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    assert torch.equal(hz, hx), "e2e round trip mismatch"
+    nbytes = hx.numel() * 8
+    return {"value": bfly_per_step * world * steps / (ms / 1e3), "unit": "butterflies/s",
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": ms / steps}
+
+
+# ----------------------------------------------------------------------------- other §8 rows
+def run_rows(args, P, pk, stream):
+    """One measurement per other SURVEY §8(a) row: cfg1 latency, cfg2 BLAS, cfg3 negacyclic
+    polymul, cfg4 size sweep (2 sizes by default), cfg5 N = 2^26 on one GPU."""
+    import torch
+    from paper_2509_12494_b200 import ntt128 as N
+    from paper_2509_12494_b200 import synth
+    rows = {}
+    # cfg1: single N = 1024 forward + inverse (latency)
+    e = P["cfg1"]
+    q, w = hexint(e["q"]), hexint(e["omega"])
+    p1 = N.Plan(10, q, w)
+    x = to_dev(synth.uniform_residues(q, 1024, synth.stream_seed(1, 0, 0)).reshape(1, 1024, 2))
+    y, z = torch.empty_like(x), torch.empty_like(x)
+    for _ in range(10):
+        p1.forward(x, out=y); p1.inverse(y, out=z)
+    ms = time_events(lambda i: (p1.forward(x, out=y), p1.inverse(y, out=z)), 200, stream)
+    rows["cfg1_n1024_fwd_inv_us"] = ms * 1e3
+    rows["cfg1_ns_per_butterfly"] = ms * 1e6 / (2 * 5120)
+    # cfg2: BLAS n = 2^20 (HBM-bound; 48 B/element); rotate 8 buffer sets (8 x 48 MiB > L2)
+    q2, a2, n2 = hexint(P["cfg2"]["q"]), hexint(P["cfg2"]["a"]), P["cfg2"]["n"]
+    xs = [to_dev(synth.uniform_residues(q2, n2, synth.stream_seed(2, 0, s))) for s in range(8)]
+    ys = [to_dev(synth.uniform_residues(q2, n2, synth.stream_seed(2, 1, s))) for s in range(8)]
+    zs = [torch.empty_like(v) for v in xs]
+    ops = {"add": lambda i: N.vadd(xs[i % 8], ys[i % 8], q2, out=zs[i % 8]),
+           "sub": lambda i: N.vsub(xs[i % 8], ys[i % 8], q2, out=zs[i % 8]),
+           "mul": lambda i: N.vmul(xs[i % 8], ys[i % 8], q2, out=zs[i % 8]),
+           "axpy": lambda i: N.axpy(a2, xs[i % 8], ys[i % 8], q2)}
+    for name, fn in ops.items():
+        for i in range(8):
+            fn(i)
+        ms = time_events(fn, 200, stream)
+        gbs = 48 * n2 / (ms * 1e-3) / 1e9
+        rows[f"cfg2_{name}_elem_per_s"] = n2 / (ms * 1e-3)
+        rows[f"cfg2_{name}_hbm_frac"] = gbs / pk["hbm_gbs"]
+    # cfg3 negacyclic polymul (B = 64)
+    mods = P["cfg3"]["moduli"]
+    qs, psis = [hexint(m["q"]) for m in mods], [hexint(m["psi"]) for m in mods]
+    n3 = 1 << 16
+    pn = N.Plan(16, qs, psis, batch=64, negacyclic=True)
+    a = to_dev(np.stack([synth.uniform_residues(qs[i], n3, synth.stream_seed(3, 0, i)) for i in range(64)]))
+    b = to_dev(np.stack([synth.uniform_residues(qs[i], n3, synth.stream_seed(3, 1, i)) for i in range(64)]))
+    c = torch.empty_like(a)
+    for _ in range(3):
+        pn.polymul(a, b, out=c)
+    ms = time_events(lambda i: pn.polymul(a, b, out=c), 10, stream)
+    rows["cfg3_negacyclic_polymul_per_s"] = 64 / (ms * 1e-3)
+    rows["cfg3_negacyclic_polymul_ms"] = ms
+    del pn, a, b, c
+    # cfg4 sweep (1 GiB of coefficients per size) -- sizes given by --sweep
+    for logn in args.sweep:
+        e = P["cfg4"][str(logn)]
+        q, w = hexint(e["q"]), hexint(e["omega"])
+        nn = 1 << logn
+        Bn = (1 << 26) // nn
+        ps = N.Plan(logn, q, w, batch=Bn)
+        xx = to_dev(synth.uniform_residues(q, 1 << 26, synth.stream_seed(4, 0, logn)).reshape(Bn, nn, 2))
+        yy = torch.empty_like(xx)
+        for _ in range(2):
+            ps.forward(xx, out=yy); ps.inverse(yy, out=xx)
+        ms = time_events(lambda i: (ps.forward(xx, out=yy), ps.inverse(yy, out=xx)), 5, stream)
+        rows[f"cfg4_logn{logn}_butterflies_per_s"] = 2 * Bn * (nn // 2) * logn / (ms * 1e-3)
+        del ps, xx, yy
+        torch.cuda.empty_cache()
+    # cfg5: N = 2^26 single transform on one GPU (three passes)
+    if args.cfg5:
+        e = P["cfg5"]
+        q, w = hexint(e["q"]), hexint(e["omega"])
+        p5 = N.Plan(26, q, w)
+        xx = to_dev(synth.uniform_residues(q, 1 << 26, synth.stream_seed(5, 0, 0)).reshape(1, 1 << 26, 2))
+        yy = torch.empty_like(xx)
+        zz = torch.empty_like(xx)
+        p5.forward(xx, out=yy); p5.inverse(yy, out=zz)
+        torch.cuda.synchronize()
+        assert torch.equal(zz, xx)
+        ms = time_events(lambda i: (p5.forward(xx, out=yy), p5.inverse(yy, out=zz)), 5, stream)
+        rows["cfg5_n2^26_fwd_inv_ms"] = ms
+        rows["cfg5_butterflies_per_s"] = 2 * (1 << 25) * 26 / (ms * 1e-3)
+        del p5, xx, yy, zz
+        torch.cuda.empty_cache()
+    return rows
+
+
+# ----------------------------------------------------------------------------- oracle legs
+def cpu_baseline(P, npolys: int = 16):
+    """The oracle (radix-2 on unsigned __int128, shift-subtract remainders) timed on this
+    host's cores: forward + inverse of `npolys` of the cfg3 polynomials (bounded sample)."""
+    from oracle import oracle as O
+    mods = P["cfg3"]["moduli"][:npolys]
+    qs, ws = [hexint(m["q"]) for m in mods], [hexint(m["omega"]) for m in mods]
+    from paper_2509_12494_b200 import synth
+    n = 1 << P["cfg3"]["logn"]
+    x = np.stack([synth.uniform_residues(qs[i], n, synth.stream_seed(3, 0, i)) for i in range(npolys)])
+    t0 = time.perf_counter()
+    y = O.ntt(x, qs, ws)
+    z = O.intt(y, qs, ws)
+    dt = time.perf_counter() - t0
+    assert np.array_equal(z, x)
+    bfly = 2 * npolys * (n // 2) * P["cfg3"]["logn"]
+    return {"value": bfly / dt, "unit": "butterflies/s", "cores": O.num_threads(), "kind": "oracle",
+            "sample": f"forward+inverse of {npolys} of the 64 cfg3 polynomials (N=2^16), {dt:.2f} s wall"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    P = load_params()
+    vals = []
+    cb = None
+    for _ in range(args.warmup):
+        cpu_baseline(P, npolys=4)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cb = cpu_baseline(P, npolys=4)
+        vals.append(cb["value"])
+    wall = time.perf_counter() - t0
+    value = statistics.mean(vals)
+    n, B = 1 << 16, 64
+    out = {"impl": "reference", "metric": "128-bit NTT butterflies/sec (N=2^16, fwd+inv, 64 RNS primes)",
+           "value": value, "unit": "butterflies/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u128", "data": "synthetic (seeded uniform residues)",
+           "config": {"workload": "cfg3: batched forward+inverse cyclic NTT, N=2^16, 64 distinct 124-128-bit primes "
+                                  "(BASELINE.json configs[2]); each step a bounded sample of 4 of the 64 polynomials",
+                      "N": n, "batch_per_gpu": B},
+           "cpu_baseline": {"value": value, "unit": "butterflies/s", "cores": cb["cores"], "kind": "oracle",
+                            "sample": cb["sample"]},
+           "e2e": {"value": value, "unit": "butterflies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", dest="rows", action="store_true", default=True)
+    ap.add_argument("--no-rows", dest="rows", action="store_false")
+    ap.add_argument("--sweep", type=lambda s: [int(v) for v in s.split(",") if v], default=[10, 16])
+    ap.add_argument("--no-cfg5", dest="cfg5", action="store_false", default=True)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false", default=True)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,136 @@
+/*
+ * ntt128.h -- C ABI of the B200-native 128-bit modular NTT and modular BLAS
+ * library (libntt128.so), a from-scratch sm_100a implementation of the hot path
+ * of arxiv 2509.12494 ("Towards Closing the Performance Gap for Cryptographic
+ * Kernels Between CPUs and Specialized Hardware").
+ *
+ * Citations are PAPER.md / SPEC.md lines under the paper's text (§ / Eq. given).
+ *
+ * ---------------------------------------------------------------------------
+ * Data layout (all entry points).  A residue x in Z_q (0 <= x < q < 2^128) is
+ * 16 bytes: two little-endian uint64 limbs [lo, hi], x = hi * 2^64 + lo -- the
+ * double-word [x0, x1] of Eq. def_dw stored low limb first,
+ * i.e. the memory image of unsigned __int128.  A polynomial of length N is N
+ * consecutive residues in natural coefficient order; a batch is B consecutive
+ * polynomials, [B][N][2] uint64.  Device pointers must be 16-byte aligned.
+ *
+ * Ownership.  Every data pointer is caller-owned device memory; the library
+ * never retains it after the call returns.  A plan owns its device tables
+ * (allocated on `device` at create, freed by destroy).  Host pointers (q, root,
+ * scalars) are read during the call only.
+ *
+ * Asynchrony.  Calls validate arguments synchronously, then enqueue kernels on
+ * `stream` and return.  A kernel fault surfaces at the caller's next sync.
+ * NTT128_ERR_CUDA is returned when a launch or allocation fails at enqueue.
+ *
+ * Preconditions.  Inputs are residues (< q): "a,b,c in Z_q".
+ * They are not checked unless NTT128_FLAG_CHECK_INPUT is set on the plan (or
+ * passed to a vec128 call); unreduced input gives unspecified output.
+ *
+ * Aliasing.  In place (out == in, z == x or z == y) is allowed everywhere.
+ * Partial overlap is undefined.
+ *
+ * Errors.  No exception crosses the ABI.  Every function returns a status;
+ * on error nothing is enqueued and outputs are untouched.
+ * ------------------------------------------------------------------------- */
+#ifndef NTT128_H
+#define NTT128_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *ntt128_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    NTT128_OK = 0,
+    NTT128_ERR_INVALID_ARG = 1,  /* null pointer, log2n out of [1, 26], batch == 0, n_moduli not 1 or batch, unknown flag bits */
+    NTT128_ERR_MODULUS = 2,      /* q even or q < 3 */
+    NTT128_ERR_NOT_PRIME = 3,    /* q fails the plan's Miller-Rabin test */
+    NTT128_ERR_NO_ROOT = 4,      /* N does not divide q-1 (cyclic) / 2N does not divide q-1 (negacyclic) */
+    NTT128_ERR_BAD_ROOT = 5,     /* root does not have exact order N (cyclic) / 2N (negacyclic), or root >= q */
+    NTT128_ERR_ALIGNMENT = 6,    /* a device pointer is not 16-byte aligned */
+    NTT128_ERR_INPUT_RANGE = 7,  /* only with NTT128_FLAG_CHECK_INPUT: some input coefficient >= q */
+    NTT128_ERR_OOM = 8,          /* device allocation failed */
+    NTT128_ERR_CUDA = 9,         /* a CUDA call failed at enqueue */
+    NTT128_ERR_UNSUPPORTED = 10  /* valid request this build does not implement */
+} ntt128_status;
+
+/* plan flags */
+#define NTT128_CYCLIC 0u            /* root = omega of exact order N; y_k = sum_j x_j omega^{jk} (Eq. ntt) */
+#define NTT128_NEGACYCLIC 1u        /* root = psi of exact order 2N; y_k = sum_j x_j psi^{j(2k+1)}, the evaluation at psi^{2k+1} */
+#define NTT128_FLAG_CHECK_INPUT 0x100u /* validate inputs < q on every call (synchronises the stream) */
+
+typedef struct ntt128_plan_s *ntt128_plan_t; /* opaque; immutable after create; safe to share across streams */
+
+/* Create a plan for `batch` transforms of length N = 2^log2n (1 <= log2n <= 26).
+ *   q_host:    [n_moduli][2] uint64 {lo, hi}: odd primes 3 <= q < 2^128 (any width;
+ *              deliberately beyond the paper's 124-bit Barrett limit, PAPER.md:208,
+ *              because the BASELINE configs use 128-bit q -- DESIGN.md reading c1)
+ *   root_host: [n_moduli][2]: omega (cyclic) or psi (negacyclic) per modulus; the
+ *              root is a plan input (reading c8)
+ *   n_moduli:  1 (all polynomials share q) or batch (polynomial b uses modulus b, the
+ *              RNS case of BASELINE cfg 3)
+ *   flags:     NTT128_CYCLIC or NTT128_NEGACYCLIC, optionally | NTT128_FLAG_CHECK_INPUT
+ *   device:    CUDA device ordinal that owns the plan tables
+ * Validates primality (Miller-Rabin), divisibility and the root's exact order, then
+ * builds per-modulus Montgomery constants and twiddle tables on the device
+ * (untimed plan work; "twiddles are precomputed per stage"). */
+ntt128_status ntt128_plan_create(ntt128_plan_t *out, uint32_t log2n, uint32_t batch, const uint64_t *q_host,
+                                 const uint64_t *root_host, uint32_t n_moduli, uint32_t flags, int device);
+
+/* Forward transform of the whole batch, natural order in and out (
+ * DESIGN.md reading c6).  d_in/d_out: [batch][N][2] uint64 device arrays. */
+ntt128_status ntt128_forward(const ntt128_plan_t plan, const uint64_t *d_in, uint64_t *d_out, ntt128_stream_t stream);
+
+/* Inverse: x_j = N^{-1} sum_k y_k omega^{-jk} (cyclic, reading c7) or
+ * x_j = N^{-1} psi^{-j} sum_k y_k omega^{-jk} (negacyclic).  inverse(forward(x)) == x. */
+ntt128_status ntt128_inverse(const ntt128_plan_t plan, const uint64_t *d_in, uint64_t *d_out, ntt128_stream_t stream);
+
+/* Polynomial product through the transform: d_c = a * b mod (X^N + 1) for negacyclic
+ * plans, mod (X^N - 1) for cyclic plans (NTT, point-wise product,
+ * inverse NTT).  d_a, d_b, d_c: [batch][N][2]; d_c may alias d_a or d_b.
+ * Uses 2 x batch x N x 16 bytes of stream-ordered scratch. */
+ntt128_status ntt128_polymul(const ntt128_plan_t plan, const uint64_t *d_a, const uint64_t *d_b, uint64_t *d_c,
+                             ntt128_stream_t stream);
+
+/* Plan properties (host-side queries). */
+ntt128_status ntt128_plan_info(const ntt128_plan_t plan, uint32_t *log2n, uint32_t *batch, uint32_t *n_moduli,
+                               uint32_t *flags, uint32_t *num_passes);
+
+void ntt128_plan_destroy(ntt128_plan_t plan);
+
+/* ---------------------------------------------------------------------------
+ * Modular BLAS over one modulus q (§2.3; BLAS as "looping over
+ * ... modular arithmetic").  n elements (any n >= 0; n == 0 is a
+ * no-op returning OK; reading c14).  q: host {lo, hi}, odd, 3 <= q < 2^128
+ * (primality not required).  flags: 0 or NTT128_FLAG_CHECK_INPUT.
+ *   vec128_add : z = x + y mod q   (Eq. saddmod)
+ *   vec128_sub : z = x - y mod q   (Eq. ssubmod)
+ *   vec128_mul : z = x * y mod q   (point-wise product, "a special case of gemv")
+ *   vec128_axpy: y = a * x + y mod q, in place on y; a: host scalar {lo, hi} < q
+ * ------------------------------------------------------------------------- */
+ntt128_status vec128_add(uint64_t *d_z, const uint64_t *d_x, const uint64_t *d_y, size_t n, const uint64_t *q,
+                         uint32_t flags, ntt128_stream_t stream);
+ntt128_status vec128_sub(uint64_t *d_z, const uint64_t *d_x, const uint64_t *d_y, size_t n, const uint64_t *q,
+                         uint32_t flags, ntt128_stream_t stream);
+ntt128_status vec128_mul(uint64_t *d_z, const uint64_t *d_x, const uint64_t *d_y, size_t n, const uint64_t *q,
+                         uint32_t flags, ntt128_stream_t stream);
+ntt128_status vec128_axpy(uint64_t *d_y, const uint64_t *a, const uint64_t *d_x, size_t n, const uint64_t *q,
+                          uint32_t flags, ntt128_stream_t stream);
+
+/* Human-readable name of a status code (static storage). */
+const char *ntt128_status_string(ntt128_status s);
+
+/* Number of library kernels launched by this process so far (all entry points; a
+ * host-side counter used by the bench to report gpu_launches). */
+uint64_t ntt128_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NTT128_H */

@@ -1,0 +1,658 @@
+// ntt128.cu -- 128-bit modular NTT for sm_100a behind the C ABI of include/ntt128.h.
+//
+// Method: the radix-2 NTT of Eq. ntt, log N stages of N/2
+// butterflies, each "one modular addition, one modular subtraction, and one
+// modular multiplication" (§3.2).  The paper's x86 dataflow (Pease
+// with unpack/permute) is replaced by a GPU dataflow:
+//
+//  * Decimation in time (Cooley-Tukey): bit-reversed input order, natural output.
+//    Stage s pairs elements whose index differs in bit s, with twiddle
+//    omega^{(N/2^{s+1}) j}, j = index mod 2^s.  One table T[i] = omega^i, i < N/2,
+//    serves every stage (stage s reads T[j << (n-1-s)]); Montgomery form.
+//  * Stages are fused into passes of up to 9 (12 for a single pass) stages.  A CTA
+//    owns C "groups" (the elements closed under the pass's stages), stages them
+//    through shared memory, and runs them as register rounds of 4 stages on 16
+//    elements per thread (8 independent butterflies per stage per thread).
+//  * The bit reversal is folded into the first pass's gather (it reads strided
+//    columns of x, coalesced across the C groups) and every later pass runs in
+//    place, so no permutation pass exists.
+//  * Inverse = same pass with T[i] = omega^{-i}; N^{-1} is folded into the last
+//    stage (u N^{-1}, v (omega^{-j} N^{-1})), so the inverse costs N/2 log N mulmods.
+//  * Stage 0 has twiddle 1 for every butterfly and skips the multiply.
+//  * Negacyclic: twist x_j psi^j fused into the first pass's load, untwist
+//    N^{-1} psi^{-j} fused into the last pass's store (reading c9).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/ntt128.h"
+#include "arith128.cuh"
+#include "host128.h"
+
+using namespace ntt128;
+using ntt128h::u128;
+
+// ----------------------------------------------------------------------------- common
+static std::atomic<uint64_t> g_launches{0};
+extern "C" uint64_t ntt128_launch_count(void) { return g_launches.load(); }
+void ntt128_count_launch(uint64_t k) { g_launches += k; }
+
+extern "C" const char* ntt128_status_string(ntt128_status s) {
+    switch (s) {
+        case NTT128_OK: return "NTT128_OK";
+        case NTT128_ERR_INVALID_ARG: return "NTT128_ERR_INVALID_ARG";
+        case NTT128_ERR_MODULUS: return "NTT128_ERR_MODULUS";
+        case NTT128_ERR_NOT_PRIME: return "NTT128_ERR_NOT_PRIME";
+        case NTT128_ERR_NO_ROOT: return "NTT128_ERR_NO_ROOT";
+        case NTT128_ERR_BAD_ROOT: return "NTT128_ERR_BAD_ROOT";
+        case NTT128_ERR_ALIGNMENT: return "NTT128_ERR_ALIGNMENT";
+        case NTT128_ERR_INPUT_RANGE: return "NTT128_ERR_INPUT_RANGE";
+        case NTT128_ERR_OOM: return "NTT128_ERR_OOM";
+        case NTT128_ERR_CUDA: return "NTT128_ERR_CUDA";
+        case NTT128_ERR_UNSUPPORTED: return "NTT128_ERR_UNSUPPORTED";
+    }
+    return "NTT128_ERR_UNKNOWN";
+}
+
+static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static void to_words(u128 v, uint32_t w[4]) {
+    for (int i = 0; i < 4; i++) w[i] = (uint32_t)(v >> (32 * i));
+}
+
+__device__ __forceinline__ uint32_t brev_bits(uint32_t x, int bits) { return bits == 0 ? 0u : (__brev(x) >> (32 - bits)); }
+
+// ----------------------------------------------------------------------------- twiddle generation
+// out[m][i] = scale_m * base_m^i (Montgomery form), i < count; pow2[m][k] = base_m^{2^k}
+// (Montgomery form), scale[m] Montgomery form.  Product over the set bits of i.
+__global__ void k_gen_pow_table(uint4* out, uint64_t stride, uint64_t count, const uint4* pow2, int pow2_stride,
+                                const uint4* scale, const ModC* mods) {
+    const int m = blockIdx.y;
+    const ModC& M = mods[m];
+    uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+        U128 r = u128_from(scale[m]);
+        uint64_t e = i;
+        int k = 0;
+        while (e) {
+            if (e & 1) r = mont_mul(r, u128_from(pow2[m * pow2_stride + k]), q, M.qinv0);
+            e >>= 1;
+            k++;
+        }
+        out[m * stride + i] = u128_to(r);
+    }
+}
+
+// ----------------------------------------------------------------------------- pass kernel
+struct PassArgs {
+    const uint4* src;      // [batch][N]
+    uint4* dst;            // [batch][N]
+    const uint4* pmul;     // optional point-wise multiplicand, same layout as src (Montgomery product)
+    const uint4* tw;       // [nq][tw_stride]: T[i] = base^i, Montgomery form, i < N/2
+    const uint4* tw_last;  // optional [nq][tw_stride]: table for the final global stage (pre-scaled by N^{-1})
+    const uint4* fin;      // optional [nq][f_stride]: factor applied at load, by natural input index
+    const uint4* fout;     // optional [nq][f_stride]: factor applied at store, by natural output index
+    const ModC* mods;      // [nq]
+    int* err;              // input-range error flag (check_input)
+    uint64_t tw_stride, f_stride;
+    uint64_t total_groups; // batch << (n - B)
+    uint32_t n, lo, nq;
+    uint32_t brev_in;      // first pass: gather bit-reversed columns
+    uint32_t first_trivial;// global stage 0 twiddle is 1: skip the multiply
+    uint32_t scale_last;   // global stage n-1: u *= ninv, v *= tw_last[j]
+    uint32_t ninv_r;       // scale_last multiplier: 0 -> ninv_m, 1 -> ninv_rm (point-wise R^-1 compensation)
+    uint32_t check_input;
+};
+
+template <int B>
+struct PassShape {
+    static constexpr int G = 1 << B;                // elements per group
+    static constexpr int E = G >= 16 ? 16 : G;      // elements per thread
+    static constexpr int LE = G >= 16 ? 4 : B;      // log2 E: stages per register round
+    static constexpr int T = G / E;                 // threads per group
+    static constexpr int GS = G + 1;                // padded group stride in shared memory
+    static constexpr int ROUNDS = (B + LE - 1) / LE;
+};
+
+template <int B, int C>
+__global__ void __launch_bounds__(C * PassShape<B>::T)
+k_ntt_pass(const PassArgs a) {
+    using S = PassShape<B>;
+    constexpr int G = S::G, E = S::E, LE = S::LE, T = S::T, GS = S::GS;
+    constexpr int NT = C * T;
+    extern __shared__ uint4 sm[];
+
+    const uint32_t n = a.n, lo = a.lo, gbits = n - B;
+    const uint64_t N = 1ull << n;
+    const uint64_t gmask = (1ull << gbits) - 1;
+    const uint64_t gg0 = (uint64_t)blockIdx.x * C;
+    const int tid = threadIdx.x;
+
+    // ---------------- load phase: global -> shared, coalesced across the C groups
+    for (int e = tid; e < C * G; e += NT) {
+        const int c = e % C, r = e / C;
+        const uint64_t gg = gg0 + c;
+        if (gg >= a.total_groups) continue;
+        const uint64_t poly = gg >> gbits, g = gg & gmask;
+        uint64_t idx;  // natural index within the polynomial
+        int l;
+        if (a.brev_in) {
+            idx = ((uint64_t)r << gbits) | g;           // column g (= brev of the group id), row r
+            l = (int)brev_bits((uint32_t)r, B);
+        } else {
+            const uint64_t H = g >> lo, L = g & ((1ull << lo) - 1);
+            idx = (H << (lo + B)) | ((uint64_t)r << lo) | L;
+            l = r;
+        }
+        uint4 v = a.src[poly * N + idx];
+        if (a.fin || a.pmul || a.check_input) {
+            const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
+            const ModC& M = a.mods[m];
+            uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+            U128 x = u128_from(v);
+            if (a.check_input && !lt_q(x, q)) atomicOr(a.err, 1);
+            if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + m * a.f_stride + idx)), q, M.qinv0);
+            if (a.pmul) x = mont_mul(x, u128_from(__ldg(a.pmul + poly * N + idx)), q, M.qinv0);
+            v = u128_to(x);
+        }
+        sm[c * GS + l] = v;
+    }
+    __syncthreads();
+
+    // ---------------- register rounds
+    {
+        const int c = tid % C, t = tid / C;
+        const uint64_t gg = gg0 + c;
+        const uint64_t ggc = gg < a.total_groups ? gg : a.total_groups - 1;
+        const uint64_t poly = ggc >> gbits, g = ggc & gmask;
+        const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
+        const ModC& M = a.mods[m];
+        const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+        const uint32_t qinv0 = M.qinv0;
+        const uint4* tw = a.tw + m * a.tw_stride;
+        const uint4* twl = a.tw_last ? a.tw_last + m * a.tw_stride : nullptr;
+        const uint64_t L = a.brev_in ? 0 : (g & ((1ull << lo) - 1));
+        uint4* gsm = sm + c * GS;
+
+#pragma unroll
+        for (int rd = 0; rd < S::ROUNDS; rd++) {
+            const int slo = rd * LE;
+            const int shi = (slo + LE < B) ? slo + LE : B;
+            const int w = (slo + LE <= B) ? slo : B - LE;   // 16-element window [w, w + LE)
+            U128 x[E];
+#pragma unroll
+            for (int k = 0; k < E; k++) {
+                const int l = ((t >> w) << (w + LE)) | (k << w) | (t & ((1 << w) - 1));
+                x[k] = u128_from(gsm[l]);
+            }
+#pragma unroll
+            for (int sl = slo; sl < shi; sl++) {
+                const uint32_t s = lo + sl;          // global stage
+                const int bit = sl - w;              // pair bit inside the window
+                const bool trivial = a.first_trivial && s == 0 && !(a.scale_last && s == n - 1);
+                const bool last = a.scale_last && s == n - 1;
+#pragma unroll
+                for (int kk = 0; kk < E / 2; kk++) {
+                    const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                    const int k1 = k0 | (1 << bit);
+                    const U128 u = x[k0];
+                    U128 v = x[k1];
+                    if (!trivial) {
+                        const int l0 = ((t >> w) << (w + LE)) | (k0 << w) | (t & ((1 << w) - 1));
+                        const uint64_t j = ((uint64_t)(l0 & ((1 << sl) - 1)) << lo) | L;   // index mod 2^s
+                        const uint4 wv = last ? __ldg(twl + j) : __ldg(tw + (j << (n - 1 - s)));
+                        v = mont_mul(v, u128_from(wv), q, qinv0);
+                    }
+                    if (last) {
+                        // u * N^{-1} (Montgomery constant selected by ninv_r)
+                        const U128 nf = a.ninv_r ? U128{{M.ninv_rm[0], M.ninv_rm[1], M.ninv_rm[2], M.ninv_rm[3]}}
+                                                 : U128{{M.ninv_m[0], M.ninv_m[1], M.ninv_m[2], M.ninv_m[3]}};
+                        const U128 us = mont_mul(u, nf, q, qinv0);
+                        x[k0] = add_mod(us, v, q);
+                        x[k1] = sub_mod(us, v, q);
+                    } else {
+                        x[k0] = add_mod(u, v, q);
+                        x[k1] = sub_mod(u, v, q);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < E; k++) {
+                const int l = ((t >> w) << (w + LE)) | (k << w) | (t & ((1 << w) - 1));
+                gsm[l] = u128_to(x[k]);
+            }
+            __syncthreads();
+        }
+    }
+
+    // ---------------- store phase: shared -> global
+    for (int e = tid; e < C * G; e += NT) {
+        int c, l;
+        if (a.brev_in) { c = e / G; l = e % G; }    // groups are contiguous rows of the working order
+        else { c = e % C; l = e / C; }
+        const uint64_t gg = gg0 + c;
+        if (gg >= a.total_groups) continue;
+        const uint64_t poly = gg >> gbits, g = gg & gmask;
+        uint64_t idx;
+        if (a.brev_in) {
+            const uint64_t H = brev_bits((uint32_t)g, gbits);
+            idx = (H << B) | (uint64_t)l;
+        } else {
+            const uint64_t H = g >> lo, Lw = g & ((1ull << lo) - 1);
+            idx = (H << (lo + B)) | ((uint64_t)l << lo) | Lw;
+        }
+        uint4 v = sm[c * GS + l];
+        if (a.fout) {
+            const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
+            const ModC& M = a.mods[m];
+            uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+            v = u128_to(mont_mul(u128_from(v), u128_from(__ldg(a.fout + m * a.f_stride + idx)), q, M.qinv0));
+        }
+        a.dst[poly * N + idx] = v;
+    }
+}
+
+// ----------------------------------------------------------------------------- launch table
+typedef void (*PassKernel)(const PassArgs);
+
+struct PassCfg {
+    PassKernel fn;
+    int B, C, threads;
+    size_t smem;
+};
+
+template <int B, int C>
+static PassCfg make_cfg() {
+    using S = PassShape<B>;
+    PassCfg c;
+    c.fn = k_ntt_pass<B, C>;
+    c.B = B;
+    c.C = C;
+    c.threads = C * S::T;
+    c.smem = (size_t)C * S::GS * sizeof(uint4);
+    return c;
+}
+
+// single pass (n = B): C polynomials per CTA; multi-pass: C = 8 groups per CTA
+static PassCfg single_cfg(int B) {
+    switch (B) {
+        case 1: return make_cfg<1, 64>();
+        case 2: return make_cfg<2, 64>();
+        case 3: return make_cfg<3, 64>();
+        case 4: return make_cfg<4, 64>();
+        case 5: return make_cfg<5, 32>();
+        case 6: return make_cfg<6, 16>();
+        case 7: return make_cfg<7, 16>();
+        case 8: return make_cfg<8, 8>();
+        case 9: return make_cfg<9, 4>();
+        case 10: return make_cfg<10, 2>();
+        case 11: return make_cfg<11, 1>();
+        default: return make_cfg<12, 1>();
+    }
+}
+static PassCfg multi_cfg(int B) {
+    switch (B) {
+        case 5: return make_cfg<5, 8>();
+        case 6: return make_cfg<6, 8>();
+        case 7: return make_cfg<7, 8>();
+        case 8: return make_cfg<8, 8>();
+        default: return make_cfg<9, 8>();
+    }
+}
+
+// ----------------------------------------------------------------------------- plan
+struct ntt128_plan_s {
+    uint32_t log2n, batch, nq, flags, kind;  // kind: 0 cyclic, 1 negacyclic
+    int device;
+    uint64_t N;
+    std::vector<int> bits;                    // bits per pass, first pass first
+    ModC* d_mods = nullptr;
+    uint4* d_tw_fwd = nullptr;                // [nq][N/2]  omega^i
+    uint4* d_tw_inv = nullptr;                // [nq][N/2]  omega^-i
+    uint4* d_tw_inv_last = nullptr;           // [nq][N/2]  omega^-i N^-1          (cyclic)
+    uint4* d_tw_inv_last_r = nullptr;         // [nq][N/2]  omega^-i N^-1 R        (cyclic polymul)
+    uint4* d_f_twist = nullptr;               // [nq][N]    psi^j                  (negacyclic)
+    uint4* d_f_untwist = nullptr;             // [nq][N]    N^-1 psi^-j            (negacyclic)
+    uint4* d_f_untwist_r = nullptr;           // [nq][N]    N^-1 psi^-j R          (negacyclic polymul)
+    std::vector<u128> q_host;
+    int* d_err = nullptr;
+};
+
+static void plan_free(ntt128_plan_s* p) {
+    if (!p) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    cudaFree(p->d_mods);
+    cudaFree(p->d_tw_fwd);
+    cudaFree(p->d_tw_inv);
+    cudaFree(p->d_tw_inv_last);
+    cudaFree(p->d_tw_inv_last_r);
+    cudaFree(p->d_f_twist);
+    cudaFree(p->d_f_untwist);
+    cudaFree(p->d_f_untwist_r);
+    cudaFree(p->d_err);
+    cudaSetDevice(prev);
+    delete p;
+}
+
+static std::vector<int> pass_bits(int n) {
+    if (n <= 12) return {n};
+    if (n <= 18) return {(n + 1) / 2, n / 2};
+    int a = (n + 2) / 3, b = (n + 1) / 3, c = n / 3;
+    return {a, b, c};
+}
+
+static inline uint4 to_uint4(u128 v) {
+    uint32_t w[4];
+    to_words(v, w);
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Build one power table on the device: out[m][i] = scale_m * base_m^i, i < count.
+static cudaError_t gen_table(uint4* out, uint64_t stride, uint64_t count, const std::vector<ntt128h::Mont>& mont,
+                             const std::vector<u128>& base, const std::vector<u128>& scale, const ModC* d_mods) {
+    const int nq = (int)mont.size();
+    const int K = 40;
+    std::vector<uint4> pow2((size_t)nq * K), sc(nq);
+    for (int m = 0; m < nq; m++) {
+        u128 b = mont[m].to_m(base[m]);
+        for (int k = 0; k < K; k++) {
+            pow2[(size_t)m * K + k] = to_uint4(b);
+            b = mont[m].mul(b, b);
+        }
+        sc[m] = to_uint4(mont[m].to_m(scale[m]));
+    }
+    uint4 *d_pow2 = nullptr, *d_sc = nullptr;
+    cudaError_t e = cudaMalloc(&d_pow2, pow2.size() * sizeof(uint4));
+    if (e == cudaSuccess) e = cudaMalloc(&d_sc, sc.size() * sizeof(uint4));
+    if (e == cudaSuccess) e = cudaMemcpy(d_pow2, pow2.data(), pow2.size() * sizeof(uint4), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_sc, sc.data(), sc.size() * sizeof(uint4), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        unsigned gx = (unsigned)((count + 255) / 256);
+        if (gx > 4096) gx = 4096;
+        if (gx == 0) gx = 1;
+        k_gen_pow_table<<<dim3(gx, nq), 256>>>(out, stride, count, d_pow2, K, d_sc, d_mods);
+        ntt128_count_launch(1);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    cudaFree(d_pow2);
+    cudaFree(d_sc);
+    return e;
+}
+
+extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, uint32_t batch, const uint64_t* q_host,
+                                            const uint64_t* root_host, uint32_t n_moduli, uint32_t flags, int device) {
+    if (!out || !q_host || !root_host) return NTT128_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (log2n < 1 || log2n > 26 || batch == 0) return NTT128_ERR_INVALID_ARG;
+    if (n_moduli != 1 && n_moduli != batch) return NTT128_ERR_INVALID_ARG;
+    if (flags & ~(NTT128_NEGACYCLIC | NTT128_FLAG_CHECK_INPUT)) return NTT128_ERR_INVALID_ARG;
+    const uint32_t kind = flags & NTT128_NEGACYCLIC;
+    const uint64_t N = 1ull << log2n;
+
+    // ---- validate every modulus and root on the host
+    std::vector<ntt128h::Mont> mont;
+    std::vector<u128> qs, roots;
+    mont.reserve(n_moduli);
+    for (uint32_t m = 0; m < n_moduli; m++) {
+        u128 q = ntt128h::make(q_host[2 * m], q_host[2 * m + 1]);
+        u128 r = ntt128h::make(root_host[2 * m], root_host[2 * m + 1]);
+        if ((q & 1) == 0 || q < 3) return NTT128_ERR_MODULUS;
+        if (!ntt128h::is_probable_prime(q)) return NTT128_ERR_NOT_PRIME;
+        const u128 order = kind ? (u128)2 * N : (u128)N;
+        if ((q - 1) % order != 0) return NTT128_ERR_NO_ROOT;
+        if (r >= q) return NTT128_ERR_BAD_ROOT;
+        mont.emplace_back(q);
+        const ntt128h::Mont& M = mont.back();
+        // exact order `order` (a power of two): r^order == 1 and r^(order/2) == q-1
+        if (M.pow(r, order / 2) != q - 1) return NTT128_ERR_BAD_ROOT;
+        qs.push_back(q);
+        roots.push_back(r);
+    }
+
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(device) != cudaSuccess) return NTT128_ERR_INVALID_ARG;
+    ntt128_plan_s* p = new (std::nothrow) ntt128_plan_s();
+    if (!p) { cudaSetDevice(prev); return NTT128_ERR_OOM; }
+    p->log2n = log2n;
+    p->batch = batch;
+    p->nq = n_moduli;
+    p->flags = flags;
+    p->kind = kind;
+    p->device = device;
+    p->N = N;
+    p->bits = pass_bits((int)log2n);
+    p->q_host = qs;
+
+    // ---- per-modulus constants
+    std::vector<ModC> mc(n_moduli);
+    std::vector<u128> omega(n_moduli), omega_inv(n_moduli), ones(n_moduli), ninv(n_moduli), ninv_r(n_moduli);
+    std::vector<u128> psi(n_moduli), psi_inv(n_moduli);
+    for (uint32_t m = 0; m < n_moduli; m++) {
+        const ntt128h::Mont& M = mont[m];
+        const u128 q = qs[m];
+        ModC& c = mc[m];
+        memset(&c, 0, sizeof(c));
+        to_words(q, c.q);
+        c.qinv0 = (uint32_t)M.qp;
+        to_words(M.r1, c.one_m);
+        to_words(M.r2, c.r2);
+        const u128 ni = M.inv((u128)(N % q));
+        to_words(M.to_m(ni), c.ninv_m);
+        to_words(M.to_m(M.mulmod(ni, M.r1)), c.ninv_rm);
+        ones[m] = 1;
+        ninv[m] = ni;
+        ninv_r[m] = M.mulmod(ni, M.r1);
+        if (kind) {
+            psi[m] = roots[m];
+            psi_inv[m] = M.inv(roots[m]);
+            omega[m] = M.mulmod(roots[m], roots[m]);
+        } else {
+            omega[m] = roots[m];
+        }
+        omega_inv[m] = M.inv(omega[m]);
+    }
+
+    ntt128_status st = NTT128_OK;
+    const uint64_t half = N / 2;
+    auto alloc = [&](uint4** ptr, uint64_t per) -> bool {
+        if (cudaMalloc(ptr, (size_t)per * n_moduli * sizeof(uint4)) != cudaSuccess) { st = NTT128_ERR_OOM; return false; }
+        return true;
+    };
+    if (cudaMalloc(&p->d_mods, n_moduli * sizeof(ModC)) != cudaSuccess ||
+        cudaMalloc(&p->d_err, sizeof(int)) != cudaSuccess) st = NTT128_ERR_OOM;
+    if (st == NTT128_OK && cudaMemcpy(p->d_mods, mc.data(), n_moduli * sizeof(ModC), cudaMemcpyHostToDevice) != cudaSuccess)
+        st = NTT128_ERR_CUDA;
+    std::vector<u128> scale_ninv(ninv), scale_ninv_r(ninv_r);
+    if (st == NTT128_OK && alloc(&p->d_tw_fwd, half) && alloc(&p->d_tw_inv, half)) {
+        if (gen_table(p->d_tw_fwd, half, half, mont, omega, ones, p->d_mods) != cudaSuccess ||
+            gen_table(p->d_tw_inv, half, half, mont, omega_inv, ones, p->d_mods) != cudaSuccess)
+            st = NTT128_ERR_CUDA;
+    }
+    if (st == NTT128_OK && !kind && alloc(&p->d_tw_inv_last, half) && alloc(&p->d_tw_inv_last_r, half)) {
+        if (gen_table(p->d_tw_inv_last, half, half, mont, omega_inv, scale_ninv, p->d_mods) != cudaSuccess ||
+            gen_table(p->d_tw_inv_last_r, half, half, mont, omega_inv, scale_ninv_r, p->d_mods) != cudaSuccess)
+            st = NTT128_ERR_CUDA;
+    }
+    if (st == NTT128_OK && kind && alloc(&p->d_f_twist, N) && alloc(&p->d_f_untwist, N) && alloc(&p->d_f_untwist_r, N)) {
+        if (gen_table(p->d_f_twist, N, N, mont, psi, ones, p->d_mods) != cudaSuccess ||
+            gen_table(p->d_f_untwist, N, N, mont, psi_inv, scale_ninv, p->d_mods) != cudaSuccess ||
+            gen_table(p->d_f_untwist_r, N, N, mont, psi_inv, scale_ninv_r, p->d_mods) != cudaSuccess)
+            st = NTT128_ERR_CUDA;
+    }
+    // opt in to > 48 KB dynamic shared memory for every pass kernel this plan uses
+    if (st == NTT128_OK) {
+        for (size_t i = 0; i < p->bits.size(); i++) {
+            PassCfg c = p->bits.size() == 1 ? single_cfg(p->bits[i]) : multi_cfg(p->bits[i]);
+            if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
+                st = NTT128_ERR_CUDA;
+        }
+    }
+    cudaSetDevice(prev);
+    if (st != NTT128_OK) {
+        plan_free(p);
+        return st;
+    }
+    *out = p;
+    return NTT128_OK;
+}
+
+extern "C" void ntt128_plan_destroy(ntt128_plan_t plan) { plan_free(plan); }
+
+extern "C" ntt128_status ntt128_plan_info(const ntt128_plan_t p, uint32_t* log2n, uint32_t* batch, uint32_t* n_moduli,
+                                          uint32_t* flags, uint32_t* num_passes) {
+    if (!p) return NTT128_ERR_INVALID_ARG;
+    if (log2n) *log2n = p->log2n;
+    if (batch) *batch = p->batch;
+    if (n_moduli) *n_moduli = p->nq;
+    if (flags) *flags = p->flags;
+    if (num_passes) *num_passes = (uint32_t)p->bits.size();
+    return NTT128_OK;
+}
+
+// ----------------------------------------------------------------------------- execution
+struct RunOpts {
+    bool inverse;
+    const uint4* pmul;     // fused point-wise product (polymul inverse)
+    bool polymul;          // use the R-compensated inverse tables
+};
+
+static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaStream_t stream);
+
+static ntt128_status run_transform(const ntt128_plan_s* p, const uint4* src, uint4* dst, cudaStream_t stream,
+                                   const RunOpts& o) {
+    const int n = (int)p->log2n;
+    const size_t npass = p->bits.size();
+    int lo = 0;
+    for (size_t i = 0; i < npass; i++) {
+        const int B = p->bits[i];
+        PassCfg c = npass == 1 ? single_cfg(B) : multi_cfg(B);
+        PassArgs a;
+        memset(&a, 0, sizeof(a));
+        a.src = i == 0 ? src : dst;
+        a.dst = dst;
+        a.mods = p->d_mods;
+        a.err = p->d_err;
+        a.tw_stride = p->N / 2;
+        a.f_stride = p->N;
+        a.total_groups = (uint64_t)p->batch << (n - B);
+        a.n = (uint32_t)n;
+        a.lo = (uint32_t)lo;
+        a.nq = p->nq;
+        a.brev_in = i == 0;
+        a.first_trivial = 1;
+        a.tw = o.inverse ? p->d_tw_inv : p->d_tw_fwd;
+        const bool first = i == 0, last = i + 1 == npass;
+        if (first && o.pmul) a.pmul = o.pmul;
+        if (p->kind == 0) {
+            if (o.inverse && last) {
+                a.scale_last = 1;
+                a.tw_last = o.polymul ? p->d_tw_inv_last_r : p->d_tw_inv_last;
+                a.ninv_r = o.polymul ? 1 : 0;
+            }
+        } else {
+            if (!o.inverse && first) a.fin = p->d_f_twist;
+            if (o.inverse && last) a.fout = o.polymul ? p->d_f_untwist_r : p->d_f_untwist;
+        }
+        const uint64_t ctas = (a.total_groups + c.C - 1) / c.C;
+        c.fn<<<(unsigned)ctas, c.threads, c.smem, stream>>>(a);
+        ntt128_count_launch(1);
+        if (cudaGetLastError() != cudaSuccess) return NTT128_ERR_CUDA;
+        lo += B;
+    }
+    return NTT128_OK;
+}
+
+__global__ void k_check_range(const uint4* x, uint64_t per_poly, uint64_t total, const ModC* mods, uint32_t nq, int* err) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t m = nq == 1 ? 0 : (uint32_t)(i / per_poly);
+        const ModC& M = mods[m];
+        if (!lt_q(u128_from(x[i]), M.q)) atomicOr(err, 1);
+    }
+}
+
+static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaStream_t stream) {
+    if (cudaMemsetAsync(p->d_err, 0, sizeof(int), stream) != cudaSuccess) return NTT128_ERR_CUDA;
+    const uint64_t total = p->N * p->batch;
+    unsigned g = (unsigned)((total + 255) / 256);
+    if (g > 148 * 16) g = 148 * 16;
+    k_check_range<<<g, 256, 0, stream>>>(src, p->N, total, p->d_mods, p->nq, p->d_err);
+    ntt128_count_launch(1);
+    int h = 0;
+    if (cudaMemcpyAsync(&h, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, stream) != cudaSuccess) return NTT128_ERR_CUDA;
+    if (cudaStreamSynchronize(stream) != cudaSuccess) return NTT128_ERR_CUDA;
+    return h ? NTT128_ERR_INPUT_RANGE : NTT128_OK;
+}
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int d) { cudaGetDevice(&prev); cudaSetDevice(d); }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+static ntt128_status transform(const ntt128_plan_t p, const uint64_t* d_in, uint64_t* d_out, cudaStream_t stream,
+                               bool inverse) {
+    if (!p || !d_in || !d_out) return NTT128_ERR_INVALID_ARG;
+    if (!aligned16(d_in) || !aligned16(d_out)) return NTT128_ERR_ALIGNMENT;
+    DeviceGuard g(p->device);
+    const uint4* src = (const uint4*)d_in;
+    uint4* dst = (uint4*)d_out;
+    if (p->flags & NTT128_FLAG_CHECK_INPUT) {
+        ntt128_status s = check_range(p, src, stream);
+        if (s != NTT128_OK) return s;
+    }
+    RunOpts o{inverse, nullptr, false};
+    if (src == dst && p->bits.size() > 1) {
+        // the first pass gathers bit-reversed columns: it cannot run in place
+        const size_t bytes = (size_t)p->N * p->batch * sizeof(uint4);
+        uint4* tmp = nullptr;
+        if (cudaMallocAsync(&tmp, bytes, stream) != cudaSuccess) return NTT128_ERR_OOM;
+        if (cudaMemcpyAsync(tmp, src, bytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess) return NTT128_ERR_CUDA;
+        ntt128_status s = run_transform(p, tmp, dst, stream, o);
+        cudaFreeAsync(tmp, stream);
+        return s;
+    }
+    return run_transform(p, src, dst, stream, o);
+}
+
+extern "C" ntt128_status ntt128_forward(const ntt128_plan_t p, const uint64_t* d_in, uint64_t* d_out, ntt128_stream_t stream) {
+    return transform(p, d_in, d_out, (cudaStream_t)stream, false);
+}
+
+extern "C" ntt128_status ntt128_inverse(const ntt128_plan_t p, const uint64_t* d_in, uint64_t* d_out, ntt128_stream_t stream) {
+    return transform(p, d_in, d_out, (cudaStream_t)stream, true);
+}
+
+extern "C" ntt128_status ntt128_polymul(const ntt128_plan_t p, const uint64_t* d_a, const uint64_t* d_b, uint64_t* d_c,
+                                        ntt128_stream_t stream_) {
+    if (!p || !d_a || !d_b || !d_c) return NTT128_ERR_INVALID_ARG;
+    if (!aligned16(d_a) || !aligned16(d_b) || !aligned16(d_c)) return NTT128_ERR_ALIGNMENT;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    DeviceGuard g(p->device);
+    if (p->flags & NTT128_FLAG_CHECK_INPUT) {
+        ntt128_status s = check_range(p, (const uint4*)d_a, stream);
+        if (s == NTT128_OK) s = check_range(p, (const uint4*)d_b, stream);
+        if (s != NTT128_OK) return s;
+    }
+    const size_t bytes = (size_t)p->N * p->batch * sizeof(uint4);
+    uint4 *fa = nullptr, *fb = nullptr;
+    if (cudaMallocAsync(&fa, bytes, stream) != cudaSuccess) return NTT128_ERR_OOM;
+    if (cudaMallocAsync(&fb, bytes, stream) != cudaSuccess) { cudaFreeAsync(fa, stream); return NTT128_ERR_OOM; }
+    RunOpts fwd{false, nullptr, false};
+    ntt128_status s = run_transform(p, (const uint4*)d_a, fa, stream, fwd);
+    if (s == NTT128_OK) s = run_transform(p, (const uint4*)d_b, fb, stream, fwd);
+    // inverse with the point-wise Montgomery product fused into its first pass's load
+    RunOpts inv{true, fb, true};
+    if (s == NTT128_OK) s = run_transform(p, fa, (uint4*)d_c, stream, inv);
+    cudaFreeAsync(fa, stream);
+    cudaFreeAsync(fb, stream);
+    return s;
+}
