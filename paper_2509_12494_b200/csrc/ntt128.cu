@@ -67,6 +67,13 @@ static void to_words(u128 v, uint32_t w[4]) {
 
 __device__ __forceinline__ uint32_t brev_bits(uint32_t x, int bits) { return bits == 0 ? 0u : (__brev(x) >> (32 - bits)); }
 
+// 16-byte global -> shared copy without a register round trip (SASS LDGSTS)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ----------------------------------------------------------------------------- twiddle generation
 // out[m][i] = scale_m * base_m^i (Montgomery form), i < count; pow2[m][k] = base_m^{2^k}
 // (Montgomery form), scale[m] Montgomery form.  Product over the set bits of i.
@@ -94,38 +101,48 @@ struct PassArgs {
     uint4* dst;            // [batch][N]
     const uint4* pmul;     // optional point-wise multiplicand, same layout as src (Montgomery product)
     const uint4* tw;       // [nq][tw_stride]: T[i] = base^i, Montgomery form, i < N/2
-    const uint4* tw_last;  // optional [nq][tw_stride]: table for the final global stage (pre-scaled by N^{-1})
+    const uint4* tw_last;  // [nq][tw_stride]: final-stage table (pre-scaled by N^{-1}) when SCALE_LAST
     const uint4* fin;      // optional [nq][f_stride]: factor applied at load, by natural input index
     const uint4* fout;     // optional [nq][f_stride]: factor applied at store, by natural output index
     const ModC* mods;      // [nq]
-    int* err;              // input-range error flag (check_input)
     uint64_t tw_stride, f_stride;
     uint64_t total_groups; // batch << (n - B)
     uint32_t n, lo, nq;
-    uint32_t brev_in;      // first pass: gather bit-reversed columns
-    uint32_t first_trivial;// global stage 0 twiddle is 1: skip the multiply
-    uint32_t scale_last;   // global stage n-1: u *= ninv, v *= tw_last[j]
-    uint32_t ninv_r;       // scale_last multiplier: 0 -> ninv_m, 1 -> ninv_rm (point-wise R^-1 compensation)
-    uint32_t check_input;
+    uint32_t ninv_r;       // SCALE_LAST multiplier: 0 -> ninv_m, 1 -> ninv_rm (point-wise R^-1 compensation)
 };
 
+// Shape of one pass: groups of G = 2^B elements, E = 2^RB elements per thread
+// (register rounds of RB stages), T threads per group.
 template <int B>
 struct PassShape {
-    static constexpr int G = 1 << B;                // elements per group
-    static constexpr int E = G >= 16 ? 16 : G;      // elements per thread
-    static constexpr int LE = G >= 16 ? 4 : B;      // log2 E: stages per register round
-    static constexpr int T = G / E;                 // threads per group
-    static constexpr int GS = G + 1;                // padded group stride in shared memory
-    static constexpr int ROUNDS = (B + LE - 1) / LE;
+    static constexpr int G = 1 << B;
+    static constexpr int RB = B >= 3 ? 3 : B;       // radix-8 register rounds
+    static constexpr int E = 1 << RB;
+    static constexpr int T = G / E;
+    static constexpr int GS = G + 1;                // padded group stride (elements)
+    static constexpr int TS = G + 1;                // padded twiddle-set stride (entries)
+    static constexpr int ROUNDS = (B + RB - 1) / RB;
 };
 
-template <int B, int C>
+// XOR swizzle of the low 3 element-index bits (16-byte slots of a 128-byte bank
+// row): conflict-free for the register-round patterns and, when B >= 9, for the
+// bit-reversed gather of a single-group CTA.
+template <int B>
+__device__ __forceinline__ int swz(int l) {
+    int f = l >> 3;
+    if (B >= 9) f ^= l >> (B >= 9 ? B - 3 : 0);
+    return l ^ (f & 7);
+}
+
+template <int B, int C, bool FIRST, bool SCALE_LAST>
 __global__ void __launch_bounds__(C * PassShape<B>::T)
 k_ntt_pass(const PassArgs a) {
     using S = PassShape<B>;
-    constexpr int G = S::G, E = S::E, LE = S::LE, T = S::T, GS = S::GS;
+    constexpr int G = S::G, RB = S::RB, E = S::E, T = S::T, GS = S::GS, TS = S::TS;
     constexpr int NT = C * T;
+    constexpr int NTW = FIRST ? 1 : C;               // twiddle sets: pass 0 shares one (L = 0)
     extern __shared__ uint4 sm[];
+    uint4* tsm = sm + C * GS;                        // [NTW][TS] pass-local twiddles
 
     const uint32_t n = a.n, lo = a.lo, gbits = n - B;
     const uint64_t N = 1ull << n;
@@ -133,127 +150,193 @@ k_ntt_pass(const PassArgs a) {
     const uint64_t gg0 = (uint64_t)blockIdx.x * C;
     const int tid = threadIdx.x;
 
-    // ---------------- load phase: global -> shared, coalesced across the C groups
-    for (int e = tid; e < C * G; e += NT) {
+    // ---------------- load phase: twiddles and data -> shared memory, all copies in flight
+    // at once (cp.async 16-byte copies, LDGSTS), then one wait.
+    // Twiddles: set c, local stage sl, jj < 2^sl -> slot (2^sl - 1) + jj holds the twiddle
+    // of the butterflies whose index mod 2^s (s = lo + sl) is (jj << lo) | L_c.
+    constexpr int TW_PER = (NTW * (G - 1) + NT - 1) / NT;
+#pragma unroll
+    for (int i = 0; i < TW_PER; i++) {
+        const int e = tid + i * NT;
+        if (e < NTW * (G - 1)) {
+            const int c = e % NTW, k = e / NTW;
+            const int sl = 31 - __clz(k + 1);
+            const int jj = k + 1 - (1 << sl);
+            const uint64_t gg = gg0 + c;
+            const uint64_t ggc = gg < a.total_groups ? gg : a.total_groups - 1;
+            const uint32_t m = a.nq == 1 ? 0 : (uint32_t)(ggc >> gbits);
+            const uint64_t L = FIRST ? 0 : ((ggc & gmask) & ((1ull << lo) - 1));
+            const uint32_t s = lo + sl;
+            const uint64_t j = ((uint64_t)jj << lo) | L;
+            const uint4* gp = (SCALE_LAST && s == n - 1) ? a.tw_last + m * a.tw_stride + j
+                                                         : a.tw + m * a.tw_stride + (j << (n - 1 - s));
+            cp_async16(tsm + c * TS + k, gp);
+        }
+    }
+    constexpr int PER = (C * G) / NT;
+    const bool direct = !a.fin && !a.pmul;
+    uint4 stage[PER];
+#pragma unroll
+    for (int i = 0; i < PER; i++) {
+        const int e = tid + i * NT;
         const int c = e % C, r = e / C;
         const uint64_t gg = gg0 + c;
         if (gg >= a.total_groups) continue;
         const uint64_t poly = gg >> gbits, g = gg & gmask;
         uint64_t idx;  // natural index within the polynomial
         int l;
-        if (a.brev_in) {
-            idx = ((uint64_t)r << gbits) | g;           // column g (= brev of the group id), row r
+        if (FIRST) {   // gather: column g of the (2^B x 2^gbits) view, row r -> local brev(r)
+            idx = ((uint64_t)r << gbits) | g;
             l = (int)brev_bits((uint32_t)r, B);
         } else {
             const uint64_t H = g >> lo, L = g & ((1ull << lo) - 1);
             idx = (H << (lo + B)) | ((uint64_t)r << lo) | L;
             l = r;
         }
-        uint4 v = a.src[poly * N + idx];
-        if (a.fin || a.pmul || a.check_input) {
+        if (direct) cp_async16(sm + c * GS + swz<B>(l), a.src + poly * N + idx);
+        else stage[i] = a.src[poly * N + idx];
+    }
+    if (!direct) {
+#pragma unroll
+        for (int i = 0; i < PER; i++) {
+            const int e = tid + i * NT;
+            const int c = e % C, r = e / C;
+            const uint64_t gg = gg0 + c;
+            if (gg >= a.total_groups) continue;
+            const uint64_t poly = gg >> gbits, g = gg & gmask;
+            uint64_t idx;
+            int l;
+            if (FIRST) {
+                idx = ((uint64_t)r << gbits) | g;
+                l = (int)brev_bits((uint32_t)r, B);
+            } else {
+                const uint64_t H = g >> lo, L = g & ((1ull << lo) - 1);
+                idx = (H << (lo + B)) | ((uint64_t)r << lo) | L;
+                l = r;
+            }
             const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
             const ModC& M = a.mods[m];
-            uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
-            U128 x = u128_from(v);
-            if (a.check_input && !lt_q(x, q)) atomicOr(a.err, 1);
+            const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+            U128 x = u128_from(stage[i]);
             if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + m * a.f_stride + idx)), q, M.qinv0);
             if (a.pmul) x = mont_mul(x, u128_from(__ldg(a.pmul + poly * N + idx)), q, M.qinv0);
-            v = u128_to(x);
+            sm[c * GS + swz<B>(l)] = u128_to(x);
         }
-        sm[c * GS + l] = v;
     }
+    cp_async_wait_all();
     __syncthreads();
 
-    // ---------------- register rounds
+    // ---------------- register rounds: RB stages on E elements per thread
     {
         const int c = tid % C, t = tid / C;
         const uint64_t gg = gg0 + c;
         const uint64_t ggc = gg < a.total_groups ? gg : a.total_groups - 1;
-        const uint64_t poly = ggc >> gbits, g = ggc & gmask;
-        const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
-        const ModC& M = a.mods[m];
-        const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
-        const uint32_t qinv0 = M.qinv0;
-        const uint4* tw = a.tw + m * a.tw_stride;
-        const uint4* twl = a.tw_last ? a.tw_last + m * a.tw_stride : nullptr;
-        const uint64_t L = a.brev_in ? 0 : (g & ((1ull << lo) - 1));
+        const uint32_t m = a.nq == 1 ? 0 : (uint32_t)(ggc >> gbits);
+        uint32_t q[4], qinv0;
+        U128 nf;
+        {
+            const ModC& M = a.mods[m];
+            q[0] = M.q[0]; q[1] = M.q[1]; q[2] = M.q[2]; q[3] = M.q[3];
+            qinv0 = M.qinv0;
+            if (SCALE_LAST) {
+                const uint32_t* src = a.ninv_r ? M.ninv_rm : M.ninv_m;
+                nf = U128{{src[0], src[1], src[2], src[3]}};
+            }
+        }
         uint4* gsm = sm + c * GS;
+        const uint4* tws = tsm + (FIRST ? 0 : c) * TS;
 
-#pragma unroll
+#pragma unroll 1
         for (int rd = 0; rd < S::ROUNDS; rd++) {
-            const int slo = rd * LE;
-            const int shi = (slo + LE < B) ? slo + LE : B;
-            const int w = (slo + LE <= B) ? slo : B - LE;   // 16-element window [w, w + LE)
+            const int slo = rd * RB;
+            const int w = (slo + RB <= B) ? slo : B - RB;   // E-element window [w, w + RB)
+            const int tlo = t & ((1 << w) - 1), thi = (t >> w) << (w + RB);
             U128 x[E];
 #pragma unroll
-            for (int k = 0; k < E; k++) {
-                const int l = ((t >> w) << (w + LE)) | (k << w) | (t & ((1 << w) - 1));
-                x[k] = u128_from(gsm[l]);
-            }
+            for (int k = 0; k < E; k++) x[k] = u128_from(gsm[swz<B>(thi | (k << w) | tlo)]);
 #pragma unroll
-            for (int sl = slo; sl < shi; sl++) {
-                const uint32_t s = lo + sl;          // global stage
-                const int bit = sl - w;              // pair bit inside the window
-                const bool trivial = a.first_trivial && s == 0 && !(a.scale_last && s == n - 1);
-                const bool last = a.scale_last && s == n - 1;
+            for (int bit = 0; bit < RB; bit++) {
+                const int sl = w + bit;                      // local stage
+                if (sl < slo) continue;                      // overlap of the last window
+                const bool trivial = FIRST && sl == 0 && !(SCALE_LAST && n == 1);
+                const bool last = SCALE_LAST && lo + sl == n - 1;
+                if (trivial) {
 #pragma unroll
-                for (int kk = 0; kk < E / 2; kk++) {
-                    const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
-                    const int k1 = k0 | (1 << bit);
-                    const U128 u = x[k0];
-                    U128 v = x[k1];
-                    if (!trivial) {
-                        const int l0 = ((t >> w) << (w + LE)) | (k0 << w) | (t & ((1 << w) - 1));
-                        const uint64_t j = ((uint64_t)(l0 & ((1 << sl) - 1)) << lo) | L;   // index mod 2^s
-                        const uint4 wv = last ? __ldg(twl + j) : __ldg(tw + (j << (n - 1 - s)));
-                        v = mont_mul(v, u128_from(wv), q, qinv0);
+                    for (int kk = 0; kk < E / 2; kk++) {
+                        const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                        const int k1 = k0 | (1 << bit);
+                        const U128 u = x[k0], v = x[k1];
+                        x[k0] = add_mod(u, v, q);
+                        x[k1] = sub_mod(u, v, q);
                     }
-                    if (last) {
-                        // u * N^{-1} (Montgomery constant selected by ninv_r)
-                        const U128 nf = a.ninv_r ? U128{{M.ninv_rm[0], M.ninv_rm[1], M.ninv_rm[2], M.ninv_rm[3]}}
-                                                 : U128{{M.ninv_m[0], M.ninv_m[1], M.ninv_m[2], M.ninv_m[3]}};
-                        const U128 us = mont_mul(u, nf, q, qinv0);
+                } else if (last) {
+#pragma unroll
+                    for (int kk = 0; kk < E / 2; kk++) {
+                        const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                        const int k1 = k0 | (1 << bit);
+                        const int l0 = thi | (k0 << w) | tlo;
+                        const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
+                        const U128 us = mont_mul(x[k0], nf, q, qinv0);
+                        const U128 v = mont_mul(x[k1], wv, q, qinv0);
                         x[k0] = add_mod(us, v, q);
                         x[k1] = sub_mod(us, v, q);
-                    } else {
+                    }
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < E / 2; kk++) {
+                        const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                        const int k1 = k0 | (1 << bit);
+                        const int l0 = thi | (k0 << w) | tlo;
+                        const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
+                        const U128 u = x[k0];
+                        const U128 v = mont_mul(x[k1], wv, q, qinv0);
                         x[k0] = add_mod(u, v, q);
                         x[k1] = sub_mod(u, v, q);
                     }
                 }
             }
 #pragma unroll
-            for (int k = 0; k < E; k++) {
-                const int l = ((t >> w) << (w + LE)) | (k << w) | (t & ((1 << w) - 1));
-                gsm[l] = u128_to(x[k]);
-            }
+            for (int k = 0; k < E; k++) gsm[swz<B>(thi | (k << w) | tlo)] = u128_to(x[k]);
             __syncthreads();
         }
     }
 
-    // ---------------- store phase: shared -> global
-    for (int e = tid; e < C * G; e += NT) {
-        int c, l;
-        if (a.brev_in) { c = e / G; l = e % G; }    // groups are contiguous rows of the working order
-        else { c = e % C; l = e / C; }
-        const uint64_t gg = gg0 + c;
-        if (gg >= a.total_groups) continue;
-        const uint64_t poly = gg >> gbits, g = gg & gmask;
-        uint64_t idx;
-        if (a.brev_in) {
-            const uint64_t H = brev_bits((uint32_t)g, gbits);
-            idx = (H << B) | (uint64_t)l;
-        } else {
-            const uint64_t H = g >> lo, Lw = g & ((1ull << lo) - 1);
-            idx = (H << (lo + B)) | ((uint64_t)l << lo) | Lw;
+    // ---------------- store phase: shared -> global, coalesced; all smem reads first
+    {
+        uint4 outv[PER];
+#pragma unroll
+        for (int i = 0; i < PER; i++) {
+            const int e = tid + i * NT;
+            int c, l;
+            if (FIRST) { c = e / G; l = e % G; }     // groups are contiguous rows of the working order
+            else { c = e % C; l = e / C; }
+            outv[i] = sm[c * GS + swz<B>(l)];
         }
-        uint4 v = sm[c * GS + l];
-        if (a.fout) {
-            const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
-            const ModC& M = a.mods[m];
-            uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
-            v = u128_to(mont_mul(u128_from(v), u128_from(__ldg(a.fout + m * a.f_stride + idx)), q, M.qinv0));
+#pragma unroll
+        for (int i = 0; i < PER; i++) {
+            const int e = tid + i * NT;
+            int c, l;
+            if (FIRST) { c = e / G; l = e % G; }
+            else { c = e % C; l = e / C; }
+            const uint64_t gg = gg0 + c;
+            if (gg >= a.total_groups) continue;
+            const uint64_t poly = gg >> gbits, g = gg & gmask;
+            uint64_t idx;
+            if (FIRST) {
+                idx = ((uint64_t)brev_bits((uint32_t)g, gbits) << B) | (uint64_t)l;
+            } else {
+                const uint64_t H = g >> lo, Lw = g & ((1ull << lo) - 1);
+                idx = (H << (lo + B)) | ((uint64_t)l << lo) | Lw;
+            }
+            uint4 v = outv[i];
+            if (a.fout) {
+                const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
+                const ModC& M = a.mods[m];
+                const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+                v = u128_to(mont_mul(u128_from(v), u128_from(__ldg(a.fout + m * a.f_stride + idx)), q, M.qinv0));
+            }
+            a.dst[poly * N + idx] = v;
         }
-        a.dst[poly * N + idx] = v;
     }
 }
 
@@ -266,43 +349,52 @@ struct PassCfg {
     size_t smem;
 };
 
-template <int B, int C>
+template <int B, int C, bool FIRST, bool SCALE_LAST>
 static PassCfg make_cfg() {
     using S = PassShape<B>;
     PassCfg c;
-    c.fn = k_ntt_pass<B, C>;
+    c.fn = k_ntt_pass<B, C, FIRST, SCALE_LAST>;
     c.B = B;
     c.C = C;
     c.threads = C * S::T;
-    c.smem = (size_t)C * S::GS * sizeof(uint4);
+    c.smem = ((size_t)C * S::GS + (size_t)(FIRST ? 1 : C) * S::TS) * sizeof(uint4);
     return c;
 }
 
-// single pass (n = B): C polynomials per CTA; multi-pass: C = 8 groups per CTA
-static PassCfg single_cfg(int B) {
+// Single pass (n = B <= 12): C polynomials per CTA, the pass is both first and last.
+template <bool SL>
+static PassCfg single_cfg_t(int B) {
     switch (B) {
-        case 1: return make_cfg<1, 64>();
-        case 2: return make_cfg<2, 64>();
-        case 3: return make_cfg<3, 64>();
-        case 4: return make_cfg<4, 64>();
-        case 5: return make_cfg<5, 32>();
-        case 6: return make_cfg<6, 16>();
-        case 7: return make_cfg<7, 16>();
-        case 8: return make_cfg<8, 8>();
-        case 9: return make_cfg<9, 4>();
-        case 10: return make_cfg<10, 2>();
-        case 11: return make_cfg<11, 1>();
-        default: return make_cfg<12, 1>();
+        case 1: return make_cfg<1, 64, true, SL>();
+        case 2: return make_cfg<2, 64, true, SL>();
+        case 3: return make_cfg<3, 64, true, SL>();
+        case 4: return make_cfg<4, 32, true, SL>();
+        case 5: return make_cfg<5, 16, true, SL>();
+        case 6: return make_cfg<6, 16, true, SL>();
+        case 7: return make_cfg<7, 16, true, SL>();
+        case 8: return make_cfg<8, 8, true, SL>();
+        case 9: return make_cfg<9, 4, true, SL>();
+        case 10: return make_cfg<10, 2, true, SL>();
+        case 11: return make_cfg<11, 1, true, SL>();
+        default: return make_cfg<12, 1, true, SL>();
     }
 }
-static PassCfg multi_cfg(int B) {
+// Multi-pass: first pass (gather, stage 0), middle passes, last pass (optionally scaled).
+template <bool FIRST, bool SL>
+static PassCfg multi_cfg_t(int B) {
     switch (B) {
-        case 5: return make_cfg<5, 8>();
-        case 6: return make_cfg<6, 8>();
-        case 7: return make_cfg<7, 8>();
-        case 8: return make_cfg<8, 8>();
-        default: return make_cfg<9, 8>();
+        case 5: return make_cfg<5, 8, FIRST, SL>();
+        case 6: return make_cfg<6, 8, FIRST, SL>();
+        case 7: return make_cfg<7, 8, FIRST, SL>();
+        case 8: return make_cfg<8, 8, FIRST, SL>();
+        default: return make_cfg<9, 4, FIRST, SL>();
     }
+}
+static PassCfg pass_cfg(size_t npass, size_t i, int B, bool scale_last) {
+    if (npass == 1) return scale_last ? single_cfg_t<true>(B) : single_cfg_t<false>(B);
+    if (i == 0) return multi_cfg_t<true, false>(B);
+    if (i + 1 == npass && scale_last) return multi_cfg_t<false, true>(B);
+    return multi_cfg_t<false, false>(B);
 }
 
 // ----------------------------------------------------------------------------- plan
@@ -491,9 +583,11 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
     // opt in to > 48 KB dynamic shared memory for every pass kernel this plan uses
     if (st == NTT128_OK) {
         for (size_t i = 0; i < p->bits.size(); i++) {
-            PassCfg c = p->bits.size() == 1 ? single_cfg(p->bits[i]) : multi_cfg(p->bits[i]);
-            if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
-                st = NTT128_ERR_CUDA;
+            for (int sl = 0; sl < 2; sl++) {
+                PassCfg c = pass_cfg(p->bits.size(), i, p->bits[i], sl == 1);
+                if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
+                    st = NTT128_ERR_CUDA;
+            }
         }
     }
     cudaSetDevice(prev);
@@ -531,34 +625,30 @@ static ntt128_status run_transform(const ntt128_plan_s* p, const uint4* src, uin
                                    const RunOpts& o) {
     const int n = (int)p->log2n;
     const size_t npass = p->bits.size();
+    const bool scale_last = p->kind == 0 && o.inverse;
     int lo = 0;
     for (size_t i = 0; i < npass; i++) {
         const int B = p->bits[i];
-        PassCfg c = npass == 1 ? single_cfg(B) : multi_cfg(B);
+        PassCfg c = pass_cfg(npass, i, B, scale_last);
         PassArgs a;
         memset(&a, 0, sizeof(a));
         a.src = i == 0 ? src : dst;
         a.dst = dst;
         a.mods = p->d_mods;
-        a.err = p->d_err;
         a.tw_stride = p->N / 2;
         a.f_stride = p->N;
         a.total_groups = (uint64_t)p->batch << (n - B);
         a.n = (uint32_t)n;
         a.lo = (uint32_t)lo;
         a.nq = p->nq;
-        a.brev_in = i == 0;
-        a.first_trivial = 1;
         a.tw = o.inverse ? p->d_tw_inv : p->d_tw_fwd;
         const bool first = i == 0, last = i + 1 == npass;
         if (first && o.pmul) a.pmul = o.pmul;
-        if (p->kind == 0) {
-            if (o.inverse && last) {
-                a.scale_last = 1;
-                a.tw_last = o.polymul ? p->d_tw_inv_last_r : p->d_tw_inv_last;
-                a.ninv_r = o.polymul ? 1 : 0;
-            }
-        } else {
+        if (scale_last && last) {
+            a.tw_last = o.polymul ? p->d_tw_inv_last_r : p->d_tw_inv_last;
+            a.ninv_r = o.polymul ? 1 : 0;
+        }
+        if (p->kind == 1) {
             if (!o.inverse && first) a.fin = p->d_f_twist;
             if (o.inverse && last) a.fout = o.polymul ? p->d_f_untwist_r : p->d_f_untwist;
         }

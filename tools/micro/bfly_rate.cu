@@ -1,0 +1,118 @@
+// Register-only radix-2 butterfly throughput (no memory traffic): the compute
+// ceiling of the NTT pass kernel's arithmetic.  Variants of add/sub mod q:
+//   V0: product arith128.cuh (select by LOP3 masks)
+//   V1: 3-input IADD3 chain + predicated correction
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <algorithm>
+#include <cuda_runtime.h>
+#include "../../paper_2509_12494_b200/csrc/arith128.cuh"
+using namespace ntt128;
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
+
+// a + b mod q: d = a + b - q in one 3-input chain; if it borrowed (d < 0), add q back
+__device__ __forceinline__ U128 add_mod_p(const U128& a, const U128& b, const uint32_t q[4]) {
+    U128 r;
+    asm("{\n\t.reg .u32 t;\n\t.reg .pred p;\n\t"
+        "add.cc.u32  %0, %4, %8;\n\t"
+        "addc.cc.u32 %1, %5, %9;\n\t"
+        "addc.cc.u32 %2, %6, %10;\n\t"
+        "addc.cc.u32 %3, %7, %11;\n\t"
+        "addc.u32    t, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, %12;\n\t"
+        "subc.cc.u32 %1, %1, %13;\n\t"
+        "subc.cc.u32 %2, %2, %14;\n\t"
+        "subc.cc.u32 %3, %3, %15;\n\t"
+        "subc.u32    t, t, 0;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "@p add.cc.u32  %0, %0, %12;\n\t"
+        "@p addc.cc.u32 %1, %1, %13;\n\t"
+        "@p addc.cc.u32 %2, %2, %14;\n\t"
+        "@p addc.u32    %3, %3, %15;\n\t}"
+        : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+        : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]),
+          "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]));
+    return r;
+}
+// a - b mod q: borrow chain; if borrowed add q
+__device__ __forceinline__ U128 sub_mod_p(const U128& a, const U128& b, const uint32_t q[4]) {
+    U128 r;
+    asm("{\n\t.reg .u32 t;\n\t.reg .pred p;\n\t"
+        "sub.cc.u32  %0, %4, %8;\n\t"
+        "subc.cc.u32 %1, %5, %9;\n\t"
+        "subc.cc.u32 %2, %6, %10;\n\t"
+        "subc.cc.u32 %3, %7, %11;\n\t"
+        "subc.u32    t, 0, 0;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "@p add.cc.u32  %0, %0, %12;\n\t"
+        "@p addc.cc.u32 %1, %1, %13;\n\t"
+        "@p addc.cc.u32 %2, %2, %14;\n\t"
+        "@p addc.u32    %3, %3, %15;\n\t}"
+        : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+        : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]),
+          "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]));
+    return r;
+}
+
+template <int V, int E>
+__global__ void __launch_bounds__(256) k_bfly(uint4* io, const uint4* tw, const ModC* mods, int iters, int* bad) {
+    const ModC M = mods[0];
+    const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+    U128 x[E], w[E / 2];
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < E; k++) x[k] = u128_from(io[tid * E + k]);
+#pragma unroll
+    for (int k = 0; k < E / 2; k++) w[k] = u128_from(tw[k]);
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int bit = 0; bit < 3; bit++) {
+#pragma unroll
+            for (int kk = 0; kk < E / 2; kk++) {
+                const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                const int k1 = k0 | (1 << bit);
+                const U128 u = x[k0];
+                const U128 v = mont_mul(x[k1], w[(kk + bit) % (E / 2)], q, M.qinv0);
+                if (V == 0) { x[k0] = add_mod(u, v, q); x[k1] = sub_mod(u, v, q); }
+                else { x[k0] = add_mod_p(u, v, q); x[k1] = sub_mod_p(u, v, q); }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < E; k++) io[tid * E + k] = u128_to(x[k]);
+}
+
+int main() {
+    cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0)); int sms = p.multiProcessorCount;
+    unsigned __int128 q = ~(unsigned __int128)0 - 8257535 + 1;  // cfg2 prime
+    unsigned __int128 inv = 1; for (int i = 0; i < 7; i++) inv *= 2 - q * inv;
+    ModC mc = {}; for (int i = 0; i < 4; i++) mc.q[i] = (uint32_t)(q >> (32 * i)); mc.qinv0 = (uint32_t)(-inv);
+    constexpr int E = 8;
+    const int threads = 256, iters = 256;
+    ModC* dm; uint4* dtw; int* dbad; CK(cudaMalloc(&dm, sizeof(ModC))); CK(cudaMemcpy(dm, &mc, sizeof(ModC), cudaMemcpyHostToDevice));
+    std::vector<uint4> tw(E / 2); for (int k = 0; k < E / 2; k++) tw[k] = make_uint4(0x12345 + k, 0x6789 * k, 0xabcdef, 0x0fffffff);
+    CK(cudaMalloc(&dtw, 16 * E)); CK(cudaMemcpy(dtw, tw.data(), 16 * E / 2, cudaMemcpyHostToDevice)); CK(cudaMalloc(&dbad, 4));
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int bpsm : {2, 3, 4, 6, 8}) {
+        const int blocks = sms * bpsm;
+        size_t n = (size_t)threads * blocks * E;
+        std::vector<uint4> h(n); for (size_t i = 0; i < n; i++) h[i] = make_uint4(i * 2654435761u, i, 77, 0x7fffffff);
+        uint4* d; CK(cudaMalloc(&d, n * 16));
+        unsigned long long hsh[2];
+        for (int v = 0; v < 2; v++) {
+            CK(cudaMemcpy(d, h.data(), n * 16, cudaMemcpyHostToDevice));
+            auto launch = [&]() { if (v == 0) k_bfly<0, E><<<blocks, threads>>>(d, dtw, dm, iters, dbad); else k_bfly<1, E><<<blocks, threads>>>(d, dtw, dm, iters, dbad); };
+            launch(); CK(cudaDeviceSynchronize());
+            std::vector<uint4> res(n); CK(cudaMemcpy(res.data(), d, n * 16, cudaMemcpyDeviceToHost));
+            unsigned long long hs = 0; for (size_t i = 0; i < n; i++) hs = hs * 1000003ull + res[i].x + 7ull * res[i].w; hsh[v] = hs;
+            float best = 1e30f;
+            for (int r = 0; r < 3; r++) { cudaEventRecord(e0); launch(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms); }
+            double bf = (double)threads * blocks * iters * 3 * (E / 2);
+            printf("{\"variant\":%d,\"blocks_per_sm\":%d,\"ms\":%.4f,\"bfly_per_s\":%.4e,\"bfly_per_clk_sm_at1965\":%.3f}\n", v, bpsm, best, bf / (best * 1e-3), bf / (best * 1e-3) / (sms * 1.965e9));
+        }
+        printf("{\"blocks_per_sm\":%d,\"hash_equal\":%d}\n", bpsm, hsh[0] == hsh[1]);
+        cudaFree(d);
+    }
+    return 0;
+}
