@@ -34,6 +34,10 @@
 #include "arith128.cuh"
 #include "host128.h"
 
+#ifndef NTT_RB8
+#define NTT_RB8 3   // register-round radix (log2) of the 8-stage multi-pass kernel (4 measured slower)
+#endif
+
 using namespace ntt128;
 using ntt128h::u128;
 
@@ -95,17 +99,36 @@ __global__ void k_gen_pow_table(uint4* out, uint64_t stride, uint64_t count, con
     }
 }
 
+// Per-pass twiddle tables in consumption order: out[m][L][k], L < 2^lo, k < 2^b - 1,
+// k = (2^sl - 1) + jj for local stage sl (global s = lo + sl), holding the twiddle of
+// the butterflies whose index mod 2^s is (jj << lo) | L, i.e. T[((jj << lo) | L) << (n-1-s)]
+// (or T_last[(jj << lo) | L] for the final stage of a scaled inverse).
+__global__ void k_gather_pass_tw(uint4* out, uint64_t out_stride, const uint4* T, const uint4* T_last,
+                                 uint64_t tw_stride, uint32_t n, uint32_t lo, uint32_t b) {
+    const int m = blockIdx.y;
+    const uint32_t K = (1u << b) - 1;
+    const uint64_t count = ((uint64_t)1 << lo) * K;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t L = e / K;
+        const uint32_t k = (uint32_t)(e - L * K);
+        const int sl = 31 - __clz(k + 1);
+        const uint64_t jj = k + 1 - (1u << sl);
+        const uint32_t s = lo + sl;
+        const uint64_t j = (jj << lo) | L;
+        out[m * out_stride + e] = (T_last && s == n - 1) ? T_last[m * tw_stride + j] : T[m * tw_stride + (j << (n - 1 - s))];
+    }
+}
+
 // ----------------------------------------------------------------------------- pass kernel
 struct PassArgs {
     const uint4* src;      // [batch][N]
     uint4* dst;            // [batch][N]
     const uint4* pmul;     // optional point-wise multiplicand, same layout as src (Montgomery product)
-    const uint4* tw;       // [nq][tw_stride]: T[i] = base^i, Montgomery form, i < N/2
-    const uint4* tw_last;  // [nq][tw_stride]: final-stage table (pre-scaled by N^{-1}) when SCALE_LAST
+    const uint4* pt;       // [nq][pt_stride] pass twiddles in consumption order: [L][k], k < 2^B - 1
     const uint4* fin;      // optional [nq][f_stride]: factor applied at load, by natural input index
     const uint4* fout;     // optional [nq][f_stride]: factor applied at store, by natural output index
     const ModC* mods;      // [nq]
-    uint64_t tw_stride, f_stride;
+    uint64_t pt_stride, f_stride;
     uint64_t total_groups; // batch << (n - B)
     uint32_t n, lo, nq;
     uint32_t ninv_r;       // SCALE_LAST multiplier: 0 -> ninv_m, 1 -> ninv_rm (point-wise R^-1 compensation)
@@ -113,10 +136,10 @@ struct PassArgs {
 
 // Shape of one pass: groups of G = 2^B elements, E = 2^RB elements per thread
 // (register rounds of RB stages), T threads per group.
-template <int B>
+template <int B, int RBMAX = 3>
 struct PassShape {
     static constexpr int G = 1 << B;
-    static constexpr int RB = B >= 3 ? 3 : B;       // radix-8 register rounds
+    static constexpr int RB = B >= RBMAX ? RBMAX : B;  // radix-2^RB register rounds
     static constexpr int E = 1 << RB;
     static constexpr int T = G / E;
     static constexpr int GS = G + 1;                // padded group stride (elements)
@@ -134,13 +157,13 @@ __device__ __forceinline__ int swz(int l) {
     return l ^ (f & 7);
 }
 
-template <int B, int C, bool FIRST, bool SCALE_LAST>
-__global__ void __launch_bounds__(C * PassShape<B>::T)
+template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX>
+__global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (C * PassShape<B, RBMAX>::T) >= 256 ? 3 : 4)
 k_ntt_pass(const PassArgs a) {
-    using S = PassShape<B>;
+    using S = PassShape<B, RBMAX>;
     constexpr int G = S::G, RB = S::RB, E = S::E, T = S::T, GS = S::GS, TS = S::TS;
     constexpr int NT = C * T;
-    constexpr int NTW = FIRST ? 1 : C;               // twiddle sets: pass 0 shares one (L = 0)
+    constexpr int NTW = (FIRST && !SINGLE) ? 1 : C;  // twiddle sets: a multi-pass first pass shares one (L = 0)
     extern __shared__ uint4 sm[];
     uint4* tsm = sm + C * GS;                        // [NTW][TS] pass-local twiddles
 
@@ -152,25 +175,20 @@ k_ntt_pass(const PassArgs a) {
 
     // ---------------- load phase: twiddles and data -> shared memory, all copies in flight
     // at once (cp.async 16-byte copies, LDGSTS), then one wait.
-    // Twiddles: set c, local stage sl, jj < 2^sl -> slot (2^sl - 1) + jj holds the twiddle
-    // of the butterflies whose index mod 2^s (s = lo + sl) is (jj << lo) | L_c.
+    // Twiddles: set c holds the 2^B - 1 twiddles of its group in consumption order
+    // (slot (2^sl - 1) + jj for local stage sl), precomputed per pass at plan time:
+    // the copy is one contiguous run per CTA.
     constexpr int TW_PER = (NTW * (G - 1) + NT - 1) / NT;
 #pragma unroll
     for (int i = 0; i < TW_PER; i++) {
         const int e = tid + i * NT;
         if (e < NTW * (G - 1)) {
-            const int c = e % NTW, k = e / NTW;
-            const int sl = 31 - __clz(k + 1);
-            const int jj = k + 1 - (1 << sl);
+            const int c = e / (G - 1), k = e - c * (G - 1);
             const uint64_t gg = gg0 + c;
             const uint64_t ggc = gg < a.total_groups ? gg : a.total_groups - 1;
             const uint32_t m = a.nq == 1 ? 0 : (uint32_t)(ggc >> gbits);
             const uint64_t L = FIRST ? 0 : ((ggc & gmask) & ((1ull << lo) - 1));
-            const uint32_t s = lo + sl;
-            const uint64_t j = ((uint64_t)jj << lo) | L;
-            const uint4* gp = (SCALE_LAST && s == n - 1) ? a.tw_last + m * a.tw_stride + j
-                                                         : a.tw + m * a.tw_stride + (j << (n - 1 - s));
-            cp_async16(tsm + c * TS + k, gp);
+            cp_async16(tsm + c * TS + k, a.pt + m * a.pt_stride + L * (G - 1) + k);
         }
     }
     constexpr int PER = (C * G) / NT;
@@ -244,7 +262,7 @@ k_ntt_pass(const PassArgs a) {
             }
         }
         uint4* gsm = sm + c * GS;
-        const uint4* tws = tsm + (FIRST ? 0 : c) * TS;
+        const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
 #pragma unroll 1
         for (int rd = 0; rd < S::ROUNDS; rd++) {
@@ -349,15 +367,15 @@ struct PassCfg {
     size_t smem;
 };
 
-template <int B, int C, bool FIRST, bool SCALE_LAST>
+template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE = false, int RBMAX = 3>
 static PassCfg make_cfg() {
-    using S = PassShape<B>;
+    using S = PassShape<B, RBMAX>;
     PassCfg c;
-    c.fn = k_ntt_pass<B, C, FIRST, SCALE_LAST>;
+    c.fn = k_ntt_pass<B, C, FIRST, SCALE_LAST, SINGLE, RBMAX>;
     c.B = B;
     c.C = C;
     c.threads = C * S::T;
-    c.smem = ((size_t)C * S::GS + (size_t)(FIRST ? 1 : C) * S::TS) * sizeof(uint4);
+    c.smem = ((size_t)C * S::GS + (size_t)((FIRST && !SINGLE) ? 1 : C) * S::TS) * sizeof(uint4);
     return c;
 }
 
@@ -365,18 +383,18 @@ static PassCfg make_cfg() {
 template <bool SL>
 static PassCfg single_cfg_t(int B) {
     switch (B) {
-        case 1: return make_cfg<1, 64, true, SL>();
-        case 2: return make_cfg<2, 64, true, SL>();
-        case 3: return make_cfg<3, 64, true, SL>();
-        case 4: return make_cfg<4, 32, true, SL>();
-        case 5: return make_cfg<5, 16, true, SL>();
-        case 6: return make_cfg<6, 16, true, SL>();
-        case 7: return make_cfg<7, 16, true, SL>();
-        case 8: return make_cfg<8, 8, true, SL>();
-        case 9: return make_cfg<9, 4, true, SL>();
-        case 10: return make_cfg<10, 2, true, SL>();
-        case 11: return make_cfg<11, 1, true, SL>();
-        default: return make_cfg<12, 1, true, SL>();
+        case 1: return make_cfg<1, 64, true, SL, true>();
+        case 2: return make_cfg<2, 64, true, SL, true>();
+        case 3: return make_cfg<3, 64, true, SL, true>();
+        case 4: return make_cfg<4, 32, true, SL, true>();
+        case 5: return make_cfg<5, 16, true, SL, true>();
+        case 6: return make_cfg<6, 16, true, SL, true>();
+        case 7: return make_cfg<7, 16, true, SL, true>();
+        case 8: return make_cfg<8, 8, true, SL, true>();
+        case 9: return make_cfg<9, 4, true, SL, true>();
+        case 10: return make_cfg<10, 2, true, SL, true>();
+        case 11: return make_cfg<11, 1, true, SL, true>();
+        default: return make_cfg<12, 1, true, SL, true>();
     }
 }
 // Multi-pass: first pass (gather, stage 0), middle passes, last pass (optionally scaled).
@@ -386,7 +404,7 @@ static PassCfg multi_cfg_t(int B) {
         case 5: return make_cfg<5, 8, FIRST, SL>();
         case 6: return make_cfg<6, 8, FIRST, SL>();
         case 7: return make_cfg<7, 8, FIRST, SL>();
-        case 8: return make_cfg<8, 8, FIRST, SL>();
+        case 8: return make_cfg<8, 8, FIRST, SL, false, NTT_RB8>();
         default: return make_cfg<9, 4, FIRST, SL>();
     }
 }
@@ -413,6 +431,8 @@ struct ntt128_plan_s {
     uint4* d_f_untwist_r = nullptr;           // [nq][N]    N^-1 psi^-j R          (negacyclic polymul)
     std::vector<u128> q_host;
     int* d_err = nullptr;
+    std::vector<uint4*> d_pt_fwd, d_pt_inv, d_pt_inv_r;  // per pass, [nq][pt_stride]
+    std::vector<uint64_t> pt_stride;
 };
 
 static void plan_free(ntt128_plan_s* p) {
@@ -429,6 +449,11 @@ static void plan_free(ntt128_plan_s* p) {
     cudaFree(p->d_f_untwist);
     cudaFree(p->d_f_untwist_r);
     cudaFree(p->d_err);
+    for (size_t i = 0; i < p->d_pt_fwd.size(); i++) {
+        if (p->d_pt_inv_r[i] != p->d_pt_inv[i]) cudaFree(p->d_pt_inv_r[i]);
+        cudaFree(p->d_pt_fwd[i]);
+        cudaFree(p->d_pt_inv[i]);
+    }
     cudaSetDevice(prev);
     delete p;
 }
@@ -590,6 +615,41 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
             }
         }
     }
+    // per-pass twiddle tables in consumption order (gathered from the power tables)
+    if (st == NTT128_OK) {
+        int lo = 0;
+        const size_t np = p->bits.size();
+        for (size_t i = 0; i < np && st == NTT128_OK; i++) {
+            const int b = p->bits[i];
+            const uint64_t stride = ((uint64_t)1 << lo) * (((uint64_t)1 << b) - 1);
+            p->pt_stride.push_back(stride);
+            const bool last = i + 1 == np;
+            uint4 *f = nullptr, *v = nullptr, *vr = nullptr;
+            const size_t bytes = (size_t)stride * n_moduli * sizeof(uint4);
+            if (cudaMalloc(&f, bytes) != cudaSuccess || cudaMalloc(&v, bytes) != cudaSuccess) st = NTT128_ERR_OOM;
+            if (st == NTT128_OK && last && !kind && cudaMalloc(&vr, bytes) != cudaSuccess) st = NTT128_ERR_OOM;
+            if (!vr) vr = v;
+            p->d_pt_fwd.push_back(f);
+            p->d_pt_inv.push_back(v);
+            p->d_pt_inv_r.push_back(vr);
+            if (st != NTT128_OK) break;
+            unsigned gx = (unsigned)((stride + 255) / 256);
+            if (gx > 4096) gx = 4096;
+            const dim3 grid(gx, n_moduli);
+            k_gather_pass_tw<<<grid, 256>>>(f, stride, p->d_tw_fwd, nullptr, half, log2n, lo, b);
+            k_gather_pass_tw<<<grid, 256>>>(v, stride, p->d_tw_inv, (last && !kind) ? p->d_tw_inv_last : nullptr, half,
+                                            log2n, lo, b);
+            if (vr != v) k_gather_pass_tw<<<grid, 256>>>(vr, stride, p->d_tw_inv, p->d_tw_inv_last_r, half, log2n, lo, b);
+            ntt128_count_launch(vr != v ? 3 : 2);
+            if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = NTT128_ERR_CUDA;
+            lo += b;
+        }
+        // the power tables are only the source of the pass tables
+        cudaFree(p->d_tw_fwd); p->d_tw_fwd = nullptr;
+        cudaFree(p->d_tw_inv); p->d_tw_inv = nullptr;
+        cudaFree(p->d_tw_inv_last); p->d_tw_inv_last = nullptr;
+        cudaFree(p->d_tw_inv_last_r); p->d_tw_inv_last_r = nullptr;
+    }
     cudaSetDevice(prev);
     if (st != NTT128_OK) {
         plan_free(p);
@@ -635,19 +695,16 @@ static ntt128_status run_transform(const ntt128_plan_s* p, const uint4* src, uin
         a.src = i == 0 ? src : dst;
         a.dst = dst;
         a.mods = p->d_mods;
-        a.tw_stride = p->N / 2;
+        a.pt_stride = p->pt_stride[i];
         a.f_stride = p->N;
         a.total_groups = (uint64_t)p->batch << (n - B);
         a.n = (uint32_t)n;
         a.lo = (uint32_t)lo;
         a.nq = p->nq;
-        a.tw = o.inverse ? p->d_tw_inv : p->d_tw_fwd;
+        a.pt = !o.inverse ? p->d_pt_fwd[i] : (o.polymul ? p->d_pt_inv_r[i] : p->d_pt_inv[i]);
         const bool first = i == 0, last = i + 1 == npass;
         if (first && o.pmul) a.pmul = o.pmul;
-        if (scale_last && last) {
-            a.tw_last = o.polymul ? p->d_tw_inv_last_r : p->d_tw_inv_last;
-            a.ninv_r = o.polymul ? 1 : 0;
-        }
+        if (scale_last && last) a.ninv_r = o.polymul ? 1 : 0;
         if (p->kind == 1) {
             if (!o.inverse && first) a.fin = p->d_f_twist;
             if (o.inverse && last) a.fout = o.polymul ? p->d_f_untwist_r : p->d_f_untwist;

@@ -15,7 +15,7 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libntt128.so")
+LIB_PATH = os.environ.get("NTT128_LIB") or os.path.join(_PKG, "libntt128.so")  # override: experiments only
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2509_12494_b200.build` (no fallback path exists)")
 

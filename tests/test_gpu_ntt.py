@@ -210,3 +210,25 @@ def test_plan_errors(N, params):
     x[0, 7] = [0xFFFFFFFFFFFFFFFF, 0xFFFFFFFFFFFFFFFF]
     with pytest.raises(N.NTT128ArgError, match="INPUT_RANGE"):
         plan.forward(to_dev(x))
+
+
+@pytest.mark.parametrize("logn", [3, 6, 8, 10, 11, 14])
+def test_rns_many_primes_small_sizes(N, params, logn):
+    """one distinct prime per polynomial at sizes whose CTAs hold several polynomials
+    (single pass, C > 1) -- every polynomial must use its own modulus and twiddles"""
+    mods = params["cfg3"]["moduli"][:16]
+    qs = [m["q"] for m in mods]
+    ws = [sub_root(m, logn) for m in mods]
+    psis = [sub_root(m, logn, negacyclic=True) for m in mods]
+    n, B = 1 << logn, len(mods)
+    x = np.stack([synth.uniform_residues(qs[i], n, 1000 * logn + i) for i in range(B)])
+    plan = N.Plan(logn, qs, ws, batch=B)
+    y = to_host(plan.forward(to_dev(x)))
+    assert np.array_equal(y, O.ntt(x, qs, ws))
+    assert np.array_equal(to_host(plan.inverse(to_dev(y))), x)
+    pn = N.Plan(logn, qs, psis, batch=B, negacyclic=True)
+    yn = to_host(pn.forward(to_dev(x)))
+    assert np.array_equal(yn, O.negacyclic_ntt(x, qs, psis))
+    b = np.stack([synth.uniform_residues(qs[i], n, 2000 * logn + i) for i in range(B)])
+    c = to_host(pn.polymul(to_dev(x), to_dev(b)))
+    assert np.array_equal(c, O.negacyclic_polymul(x, b, qs, psis))
