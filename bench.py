@@ -188,6 +188,32 @@ def time_events(fn, iters, stream):
     return e0.elapsed_time(e1) / iters
 
 
+def time_graph(fn, ncalls, replays=20):
+    """average ms per call of `fn(i)`, i < ncalls, captured once into a CUDA graph and
+    replayed (removes host launch overhead from short kernels)"""
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(ncalls):
+            fn(i)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(ncalls):
+            fn(i)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(replays):
+        g.replay()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / (replays * ncalls)
+
+
 def run_gpu(args):
     import torch
     from paper_2509_12494_b200 import ntt128 as N
@@ -253,10 +279,10 @@ def run_gpu(args):
     prod_per_launch = P_BUTTERFLY * B * (n // 2) * (logn / npasses)
     achieved = prod_per_launch / (launch_ms * 1e-3) / 1e12
     traffic = None
-    if os.path.exists(TRAFFIC_PATH):
+    if os.path.exists(TRAFFIC_PATH):   # dram read+write bytes per launch from a committed ncu --set full capture
         try:
             with open(TRAFFIC_PATH) as f:
-                traffic = json.load(f).get("k_ntt_pass_bytes_per_launch")
+                traffic = json.load(f).get("bytes_per_launch_mean")
         except Exception:
             traffic = None
     roofline = {"bound": "alu", "kernel": "k_ntt_pass", "achieved": round(achieved, 4), "peak": round(pk["tprod_s"], 4),
@@ -343,10 +369,8 @@ def run_rows(args, P, pk, stream):
     p1 = N.Plan(10, q, w)
     x = to_dev(synth.uniform_residues(q, 1024, synth.stream_seed(1, 0, 0)).reshape(1, 1024, 2))
     y, z = torch.empty_like(x), torch.empty_like(x)
-    for _ in range(10):
-        p1.forward(x, out=y); p1.inverse(y, out=z)
-    ms = time_events(lambda i: (p1.forward(x, out=y), p1.inverse(y, out=z)), 200, stream)
-    rows["cfg1_n1024_fwd_inv_us"] = ms * 1e3
+    ms = time_graph(lambda i: (p1.forward(x, out=y), p1.inverse(y, out=z)), 50)
+    rows["cfg1_n1024_fwd_inv_us"] = ms * 1e3           # CUDA-graph replay (launch overhead excluded)
     rows["cfg1_ns_per_butterfly"] = ms * 1e6 / (2 * 5120)
     # cfg2: BLAS n = 2^20 (HBM-bound; 48 B/element); rotate 8 buffer sets (8 x 48 MiB > L2)
     q2, a2, n2 = hexint(P["cfg2"]["q"]), hexint(P["cfg2"]["a"]), P["cfg2"]["n"]
@@ -358,9 +382,7 @@ def run_rows(args, P, pk, stream):
            "mul": lambda i: N.vmul(xs[i % 8], ys[i % 8], q2, out=zs[i % 8]),
            "axpy": lambda i: N.axpy(a2, xs[i % 8], ys[i % 8], q2)}
     for name, fn in ops.items():
-        for i in range(8):
-            fn(i)
-        ms = time_events(fn, 200, stream)
+        ms = time_graph(fn, 64)
         gbs = 48 * n2 / (ms * 1e-3) / 1e9
         rows[f"cfg2_{name}_elem_per_s"] = n2 / (ms * 1e-3)
         rows[f"cfg2_{name}_hbm_frac"] = gbs / pk["hbm_gbs"]

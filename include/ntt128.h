@@ -122,6 +122,41 @@ ntt128_status vec128_mul(uint64_t *d_z, const uint64_t *d_x, const uint64_t *d_y
 ntt128_status vec128_axpy(uint64_t *d_y, const uint64_t *a, const uint64_t *d_x, size_t n, const uint64_t *q,
                           uint32_t flags, ntt128_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Distributed four-step NTT of one huge polynomial (BASELINE cfg 5, N = 2^26; SURVEY.md
+ * §8(a) row a13, §8(e)).  N = n1 n2, j = j1 + n1 j2, k = k2 + n2 k1:
+ *   z[j1][k2] = sum_{j2} x[j1 + n1 j2] w^{n1 j2 k2}       (n2-point NTTs, w = omega)
+ *   z[j1][k2] *= w^{j1 k2}                                 (twiddle)
+ *   y[k2 + n2 k1] = sum_{j1} z[j1][k2] w^{n2 j1 k1}        (n1-point NTTs)
+ * which equals Eq. ntt exactly.  G = world ranks (a power of two
+ * dividing n1 and n2), one process per GPU; the caller moves the packed blocks between
+ * ranks with an all-to-all of equal splits (NCCL over NVLink), e.g.
+ * torch.distributed.all_to_all_single.  Layouts (R1 = n1/G, R2 = n2/G, rank g):
+ *   "columns" X_g[R1][n2]: X_g[r][j2] = x[(g R1 + r) + n1 j2]       (forward input / inverse output)
+ *   "rows"    Y_g[R2][n1]: Y_g[r][k1] = y[(g R2 + r) + n2 k1]       (forward output / inverse input)
+ *   send/recv [G][R1][R2] (forward) and [G][R2][R1] (inverse): block h goes to / came from rank h.
+ * The inverse applies (n1 n2)^{-1} (each sub-transform scales by its own length).
+ * ------------------------------------------------------------------------- */
+typedef struct ntt128_fourstep_s *ntt128_fourstep_t;
+
+/* log2n1, log2n2 in [1, 13]; q, omega: host {lo, hi}, omega of exact order N = 2^(log2n1 + log2n2);
+ * world G a power of two dividing both n1 and n2; 0 <= rank < world. */
+ntt128_status ntt128_fourstep_create(ntt128_fourstep_t *out, uint32_t log2n1, uint32_t log2n2, const uint64_t *q,
+                                     const uint64_t *omega, uint32_t rank, uint32_t world, int device);
+/* forward, before the exchange: X_g (columns) -> send [G][R1][R2] */
+ntt128_status ntt128_fourstep_forward_a(const ntt128_fourstep_t fs, const uint64_t *d_cols, uint64_t *d_send,
+                                        ntt128_stream_t stream);
+/* forward, after the exchange: recv [G][R1][R2] -> Y_g (rows) */
+ntt128_status ntt128_fourstep_forward_c(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_rows,
+                                        ntt128_stream_t stream);
+/* inverse, before the exchange: Y_g (rows) -> send [G][R2][R1] */
+ntt128_status ntt128_fourstep_inverse_a(const ntt128_fourstep_t fs, const uint64_t *d_rows, uint64_t *d_send,
+                                        ntt128_stream_t stream);
+/* inverse, after the exchange: recv [G][R2][R1] -> X_g (columns) */
+ntt128_status ntt128_fourstep_inverse_c(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_cols,
+                                        ntt128_stream_t stream);
+void ntt128_fourstep_destroy(ntt128_fourstep_t fs);
+
 /* Human-readable name of a status code (static storage). */
 const char *ntt128_status_string(ntt128_status s);
 

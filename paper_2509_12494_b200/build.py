@@ -9,7 +9,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = ["ntt128.cu", "vec128.cu"]
+SOURCES = ["ntt128.cu", "vec128.cu", "fourstep.cu"]
 HEADERS = ["arith128.cuh", "host128.h", os.path.join("..", "..", "include", "ntt128.h")]
 LIB = os.path.join(PKG, "libntt128.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

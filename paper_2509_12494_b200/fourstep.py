@@ -1,0 +1,149 @@
+"""Distributed four-step NTT of one huge polynomial over G ranks (one process per GPU).
+
+Binding of the ntt128_fourstep_* C ABI (include/ntt128.h, "Distributed four-step") plus
+the host-side exchange: each rank runs its local pass A in the library, the packed
+blocks move with ONE all-to-all of equal splits (torch.distributed, NCCL over
+NVLink/NVSwitch on GPUs), then the local pass C.  No arithmetic happens here.
+
+Layouts (N = n1 n2, R1 = n1/G, R2 = n2/G, rank g):
+  columns  X_g[r][j2] = x[(g R1 + r) + n1 j2]     (forward input, inverse output)
+  rows     Y_g[r][k1] = y[(g R2 + r) + n2 k1]     (forward output, inverse input)
+`to_columns` / `from_columns` / `to_rows` / `from_rows` are the pure index maps between
+these and natural order (host logic; numpy, no arithmetic).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import ntt128 as _n
+
+_L = _n._L
+_vp = ctypes.c_void_p
+_L.ntt128_fourstep_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_uint32, ctypes.c_uint32, _n._u64p, _n._u64p,
+                                      ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int]
+_L.ntt128_fourstep_create.restype = ctypes.c_int
+for _name in ("ntt128_fourstep_forward_a", "ntt128_fourstep_forward_c", "ntt128_fourstep_inverse_a",
+              "ntt128_fourstep_inverse_c"):
+    getattr(_L, _name).argtypes = [_vp, _vp, _vp, _vp]
+    getattr(_L, _name).restype = ctypes.c_int
+_L.ntt128_fourstep_destroy.argtypes = [_vp]
+_L.ntt128_fourstep_destroy.restype = None
+
+
+# ----------------------------------------------------------------------------- layouts (host index maps)
+def split(log2n: int) -> tuple[int, int]:
+    """n1 = 2^ceil(log2n/2), n2 = 2^floor(log2n/2) exponents (2^13 x 2^13 for N = 2^26)"""
+    return (log2n + 1) // 2, log2n // 2
+
+
+def to_columns(x: np.ndarray, n1: int, n2: int, rank: int, world: int) -> np.ndarray:
+    """natural x[N, 2] -> X_rank[R1][n2][2]"""
+    R1 = n1 // world
+    v = x.reshape(n2, n1, 2)                     # v[j2][j1] = x[j1 + n1 j2]
+    return np.ascontiguousarray(v[:, rank * R1:(rank + 1) * R1].transpose(1, 0, 2))
+
+
+def from_columns(parts, n1: int, n2: int) -> np.ndarray:
+    """[X_0 .. X_{G-1}] -> natural x[N, 2]"""
+    cols = np.concatenate(parts, axis=0)         # [n1][n2]: cols[j1][j2] = x[j1 + n1 j2]
+    return np.ascontiguousarray(cols.transpose(1, 0, 2)).reshape(n1 * n2, 2)
+
+
+def to_rows(y: np.ndarray, n1: int, n2: int, rank: int, world: int) -> np.ndarray:
+    """natural y[N, 2] -> Y_rank[R2][n1][2]"""
+    R2 = n2 // world
+    v = y.reshape(n1, n2, 2)                     # v[k1][k2] = y[k2 + n2 k1]
+    return np.ascontiguousarray(v[:, rank * R2:(rank + 1) * R2].transpose(1, 0, 2))
+
+
+def from_rows(parts, n1: int, n2: int) -> np.ndarray:
+    """[Y_0 .. Y_{G-1}] -> natural y[N, 2]"""
+    rows = np.concatenate(parts, axis=0)         # [n2][n1]: rows[k2][k1] = y[k2 + n2 k1]
+    return np.ascontiguousarray(rows.transpose(1, 0, 2)).reshape(n1 * n2, 2)
+
+
+# ----------------------------------------------------------------------------- device object
+class FourStepLocal:
+    """One rank's share of a four-step transform (ntt128_fourstep_create)."""
+
+    def __init__(self, log2n: int, q: int, omega: int, rank: int = 0, world: int = 1, device: int | None = None):
+        import torch
+        self.log2n = int(log2n)
+        self.l1, self.l2 = split(self.log2n)
+        self.n1, self.n2 = 1 << self.l1, 1 << self.l2
+        self.rank, self.world = int(rank), int(world)
+        self.R1, self.R2 = self.n1 // self.world, self.n2 // self.world
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        h = _vp()
+        self._h = None
+        _n._check(_L.ntt128_fourstep_create(ctypes.byref(h), self.l1, self.l2, _n._pairs([q]), _n._pairs([omega]),
+                                            self.rank, self.world, self.device), "ntt128_fourstep_create")
+        self._h = h
+
+    def _call(self, name, a, b):
+        _n._check(getattr(_L, name)(self._h, _n._ptr(a, "in"), _n._ptr(b, "out"), _n._stream(a)), name)
+        return b
+
+    def forward_a(self, cols, send):
+        return self._call("ntt128_fourstep_forward_a", cols, send)
+
+    def forward_c(self, recv, rows):
+        return self._call("ntt128_fourstep_forward_c", recv, rows)
+
+    def inverse_a(self, rows, send):
+        return self._call("ntt128_fourstep_inverse_a", rows, send)
+
+    def inverse_c(self, recv, cols):
+        return self._call("ntt128_fourstep_inverse_c", recv, cols)
+
+    def close(self):
+        if self._h is not None:
+            _L.ntt128_fourstep_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def exchange(send, group=None, world: int = 1):
+    """all-to-all of equal blocks along dim 0 (block h -> rank h); world 1 is the identity"""
+    if world == 1:
+        return send
+    import torch
+    import torch.distributed as dist
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
+    return recv
+
+
+class FourStep:
+    """Distributed forward / inverse of one N-point transform; call on every rank."""
+
+    def __init__(self, log2n: int, q: int, omega: int, rank: int = 0, world: int = 1, group=None,
+                 device: int | None = None, local=None):
+        # `local` is injectable so the exchange schedule can be exercised by CPU tests (gloo)
+        self.local = local if local is not None else FourStepLocal(log2n, q, omega, rank, world, device)
+        self.group, self.world = group, world
+
+    def forward(self, cols, out=None):
+        import torch
+        L = self.local
+        send = torch.empty((self.world, L.R1, L.R2, 2), dtype=cols.dtype, device=cols.device)
+        L.forward_a(cols, send)
+        recv = exchange(send, self.group, self.world)
+        out = torch.empty((L.R2, L.n1, 2), dtype=cols.dtype, device=cols.device) if out is None else out
+        return L.forward_c(recv, out)
+
+    def inverse(self, rows, out=None):
+        import torch
+        L = self.local
+        send = torch.empty((self.world, L.R2, L.R1, 2), dtype=rows.dtype, device=rows.device)
+        L.inverse_a(rows, send)
+        recv = exchange(send, self.group, self.world)
+        out = torch.empty((L.R1, L.n2, 2), dtype=rows.dtype, device=rows.device) if out is None else out
+        return L.inverse_c(recv, out)

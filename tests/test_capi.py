@@ -25,7 +25,7 @@ def declared_functions():
 
 def test_exports_every_declared_symbol(N):
     names = declared_functions()
-    assert len(names) == 12, names
+    assert len(names) == 18, names
     lib = ctypes.CDLL(N.LIB_PATH)
     for name in names:
         assert hasattr(lib, name), name
@@ -67,6 +67,22 @@ def test_plan_create_validation_host_only(N, params):
 def test_known_small_roots(N):
     # Z_17: 2 has order 8 (2^4 = 16 = -1), 3 is a generator (order 16)
     assert pow(2, 4, 17) == 16 and pow(3, 8, 17) == 16
+
+
+def test_fourstep_validation_host_only(N, params):
+    import ctypes as C
+    from paper_2509_12494_b200 import fourstep  # noqa: F401  (declares argtypes)
+    e = params["cfg5"]
+    q, w = e["q"], e["omega"]
+    h = C.c_void_p()
+    f = N._L.ntt128_fourstep_create
+    assert f(C.byref(h), 0, 13, N._pairs([q]), N._pairs([w]), 0, 1, 0) == 1      # log2n1 out of range
+    assert f(C.byref(h), 13, 14, N._pairs([q]), N._pairs([w]), 0, 1, 0) == 1     # log2n2 out of range
+    assert f(C.byref(h), 13, 13, N._pairs([q]), N._pairs([w]), 0, 3, 0) == 1     # world not a power of two
+    assert f(C.byref(h), 13, 13, N._pairs([q]), N._pairs([w]), 2, 2, 0) == 1     # rank >= world
+    assert f(C.byref(h), 2, 2, N._pairs([q]), N._pairs([w]), 0, 8, 0) == 1      # world > n1
+    assert f(C.byref(h), 13, 13, N._pairs([q + 1]), N._pairs([w]), 0, 1, 0) == 2  # even modulus
+    assert f(C.byref(h), 13, 13, N._pairs([q]), N._pairs([w * w % q]), 0, 1, 0) == 5  # order N/2
 
 
 def test_vec_validation_host_only(N, params):

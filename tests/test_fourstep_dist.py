@@ -1,0 +1,108 @@
+"""CPU (gloo, world_size 2) test of the distributed four-step's host logic: layouts,
+packing order and the all-to-all schedule of paper_2509_12494_b200/fourstep.py, with
+an oracle-backed local backend standing in for the rank's kernels (test
+infrastructure only).  The composition must equal the oracle's N-point NTT."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2509_12494_b200 import synth
+from paper_2509_12494_b200.fourstep import FourStep, from_columns, from_rows, split, to_columns, to_rows
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64))
+
+
+def _n(t):
+    return t.numpy().view(np.uint64)
+
+
+class OracleLocal:
+    """the semantics of ntt128_fourstep_{forward,inverse}_{a,c} (include/ntt128.h), on the CPU oracle"""
+
+    def __init__(self, log2n, q, w, rank, world):
+        self.l1, self.l2 = split(log2n)
+        self.n1, self.n2 = 1 << self.l1, 1 << self.l2
+        self.N = self.n1 * self.n2
+        self.q, self.w, self.rank, self.world = q, w, rank, world
+        self.R1, self.R2 = self.n1 // world, self.n2 // world
+
+    def _pack(self, z, R, C, row0, w):
+        CG = C // self.world
+        tw = np.stack([synth.from_ints([pow(w, ((row0 + r) * c) % self.N, self.q) for c in range(C)]) for r in range(R)])
+        v = O.vmul(z.reshape(-1, 2), tw.reshape(-1, 2), self.q).reshape(R, C, 2)
+        return np.ascontiguousarray(v.reshape(R, self.world, CG, 2).transpose(1, 0, 2, 3))
+
+    def forward_a(self, cols, send):
+        z = O.ntt(_n(cols), self.q, pow(self.w, self.n1, self.q))
+        send.copy_(_t(self._pack(z, self.R1, self.n2, self.rank * self.R1, self.w)))
+
+    def forward_c(self, recv, rows):
+        m = _n(recv).reshape(self.n1, self.R2, 2).transpose(1, 0, 2)
+        rows.copy_(_t(O.ntt(np.ascontiguousarray(m), self.q, pow(self.w, self.n2, self.q))))
+        return rows
+
+    def inverse_a(self, rows, send):
+        z = O.intt(_n(rows), self.q, pow(self.w, self.n2, self.q))
+        send.copy_(_t(self._pack(z, self.R2, self.n1, self.rank * self.R2, pow(self.w, -1, self.q))))
+
+    def inverse_c(self, recv, cols):
+        m = _n(recv).reshape(self.n2, self.R1, 2).transpose(1, 0, 2)
+        cols.copy_(_t(O.intt(np.ascontiguousarray(m), self.q, pow(self.w, self.n1, self.q))))
+        return cols
+
+
+def _worker(rank, world, port, log2n, q, w, x, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    l1, l2 = split(log2n)
+    n1, n2 = 1 << l1, 1 << l2
+    fs = FourStep(log2n, q, w, rank, world, local=OracleLocal(log2n, q, w, rank, world))
+    rows = fs.forward(_t(to_columns(x, n1, n2, rank, world)))
+    cols = fs.inverse(rows)
+    out[rank] = (_n(rows).copy(), _n(cols).copy())
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("log2n,world", [(6, 2), (9, 2)])
+def test_fourstep_gloo_world2(params, log2n, world):
+    e = params["extra"]["rand128_0"]
+    q = e["q"]
+    w = pow(e["psi"], 1 << (e["logn"] + 1 - log2n), q)
+    n1, n2 = (1 << split(log2n)[0]), (1 << split(log2n)[1])
+    x = synth.uniform_residues(q, 1 << log2n, 77 + log2n)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), log2n, q, w, x, out), nprocs=world)
+    y = from_rows([out[r][0] for r in range(world)], n1, n2)
+    assert np.array_equal(y, O.ntt(x, q, w))
+    xr = from_columns([out[r][1] for r in range(world)], n1, n2)
+    assert np.array_equal(xr, x)
+
+
+def test_layout_maps_roundtrip():
+    x = synth.from_ints(range(64))
+    for world in (1, 2, 4):
+        parts = [to_columns(x, 8, 8, r, world) for r in range(world)]
+        assert np.array_equal(from_columns(parts, 8, 8), x)
+        parts = [to_rows(x, 8, 8, r, world) for r in range(world)]
+        assert np.array_equal(from_rows(parts, 8, 8), x)
+    # X_g[r][j2] = x[(g R1 + r) + n1 j2]
+    c = to_columns(x, 8, 8, 1, 2)
+    assert synth.to_ints(c[2, 3:4]) == [(1 * 4 + 2) + 8 * 3]
