@@ -34,6 +34,12 @@
 #include "arith128.cuh"
 #include "host128.h"
 
+#ifndef NTT_UNROLL_ROUNDS
+#define NTT_UNROLL_ROUNDS 0   // 1: unroll the register rounds (compile-time windows)
+#endif
+#ifndef NTT_C8
+#define NTT_C8 4              // groups per CTA of the 8-stage multi-pass kernel (8 measured 3% slower)
+#endif
 #ifndef NTT_RB8
 #define NTT_RB8 3   // register-round radix (log2) of the 8-stage multi-pass kernel (4 measured slower)
 #endif
@@ -143,7 +149,7 @@ struct PassShape {
     static constexpr int E = 1 << RB;
     static constexpr int T = G / E;
     static constexpr int GS = G + 1;                // padded group stride (elements)
-    static constexpr int TS = G + 1;                // padded twiddle-set stride (entries)
+    static constexpr int TS = G - 1;                // twiddle-set stride (odd: conflict-free across sets)
     static constexpr int ROUNDS = (B + RB - 1) / RB;
 };
 
@@ -158,7 +164,7 @@ __device__ __forceinline__ int swz(int l) {
 }
 
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX>
-__global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (C * PassShape<B, RBMAX>::T) >= 256 ? 3 : 4)
+__global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (768 / (C * PassShape<B, RBMAX>::T)) > 0 ? 768 / (C * PassShape<B, RBMAX>::T) : 1)
 k_ntt_pass(const PassArgs a) {
     using S = PassShape<B, RBMAX>;
     constexpr int G = S::G, RB = S::RB, E = S::E, T = S::T, GS = S::GS, TS = S::TS;
@@ -174,71 +180,82 @@ k_ntt_pass(const PassArgs a) {
     const int tid = threadIdx.x;
 
     // ---------------- load phase: twiddles and data -> shared memory, all copies in flight
-    // at once (cp.async 16-byte copies, LDGSTS), then one wait.
-    // Twiddles: set c holds the 2^B - 1 twiddles of its group in consumption order
-    // (slot (2^sl - 1) + jj for local stage sl), precomputed per pass at plan time:
-    // the copy is one contiguous run per CTA.
-    constexpr int TW_PER = (NTW * (G - 1) + NT - 1) / NT;
+    // at once (cp.async 16-byte copies, LDGSTS), then one wait.  NT is a multiple of C, so a
+    // thread keeps one group c = tid % C and visits rows t0 + i T (t0 = tid / C): every
+    // address below is a per-thread base plus a compile-time multiple of i.
+    const int c_me = tid % C, t0 = tid / C;
+    const uint64_t gg_me = gg0 + c_me;
+    const bool live = gg_me < a.total_groups;
+    const uint64_t ggc_me = live ? gg_me : a.total_groups - 1;
+    const uint64_t poly_me = ggc_me >> gbits, g_me = ggc_me & gmask;
+    const uint32_t m_me = a.nq == 1 ? 0 : (uint32_t)poly_me;
+    {
+        // Twiddles: set c holds its group's 2^B - 1 twiddles in consumption order (slot
+        // (2^sl - 1) + jj for local stage sl), precomputed per pass at plan time; the sets
+        // of one CTA (consecutive L, same polynomial) are one contiguous run of the table.
+        constexpr int TW_PER = (NTW * (G - 1) + NT - 1) / NT;
+        if (NTW == 1 || !(FIRST && SINGLE)) {
+            const uint64_t L0 = FIRST ? 0 : ((gg0 & gmask) & ((1ull << lo) - 1));
+            const uint32_t m0 = a.nq == 1 ? 0 : (uint32_t)((gg0 < a.total_groups ? gg0 : a.total_groups - 1) >> gbits);
+            const uint4* src = a.pt + m0 * a.pt_stride + L0 * (G - 1);
 #pragma unroll
-    for (int i = 0; i < TW_PER; i++) {
-        const int e = tid + i * NT;
-        if (e < NTW * (G - 1)) {
-            const int c = e / (G - 1), k = e - c * (G - 1);
-            const uint64_t gg = gg0 + c;
-            const uint64_t ggc = gg < a.total_groups ? gg : a.total_groups - 1;
-            const uint32_t m = a.nq == 1 ? 0 : (uint32_t)(ggc >> gbits);
-            const uint64_t L = FIRST ? 0 : ((ggc & gmask) & ((1ull << lo) - 1));
-            cp_async16(tsm + c * TS + k, a.pt + m * a.pt_stride + L * (G - 1) + k);
+            for (int i = 0; i < TW_PER; i++) {
+                const int e = tid + i * NT;
+                if (e < NTW * (G - 1)) cp_async16(tsm + e, src + e);
+            }
+        } else {   // single pass, C polynomials per CTA, each with its own modulus
+#pragma unroll
+            for (int i = 0; i < TW_PER; i++) {
+                const int e = tid + i * NT;
+                if (e < NTW * (G - 1)) {
+                    const int c = e / (G - 1), k = e - c * (G - 1);
+                    const uint64_t gg = gg0 + c;
+                    const uint32_t m = a.nq == 1 ? 0 : (uint32_t)((gg < a.total_groups ? gg : a.total_groups - 1) >> gbits);
+                    cp_async16(tsm + e, a.pt + m * a.pt_stride + k);
+                }
+            }
         }
     }
-    constexpr int PER = (C * G) / NT;
-    const bool direct = !a.fin && !a.pmul;
-    uint4 stage[PER];
-#pragma unroll
-    for (int i = 0; i < PER; i++) {
-        const int e = tid + i * NT;
-        const int c = e % C, r = e / C;
-        const uint64_t gg = gg0 + c;
-        if (gg >= a.total_groups) continue;
-        const uint64_t poly = gg >> gbits, g = gg & gmask;
-        uint64_t idx;  // natural index within the polynomial
-        int l;
-        if (FIRST) {   // gather: column g of the (2^B x 2^gbits) view, row r -> local brev(r)
-            idx = ((uint64_t)r << gbits) | g;
-            l = (int)brev_bits((uint32_t)r, B);
-        } else {
-            const uint64_t H = g >> lo, L = g & ((1ull << lo) - 1);
-            idx = (H << (lo + B)) | ((uint64_t)r << lo) | L;
-            l = r;
-        }
-        if (direct) cp_async16(sm + c * GS + swz<B>(l), a.src + poly * N + idx);
-        else stage[i] = a.src[poly * N + idx];
+    constexpr int PER = (C * G) / NT;            // == E
+    constexpr int LT = B - RB;                   // log2 T
+    // element i of this thread: row r = t0 + i T
+    uint64_t gbase;                              // natural index of row t0 of group c_me
+    uint64_t gstride;                            // natural-index step per i
+    int lbase;                                   // local index of row t0
+    if (FIRST) {   // gather column g of the (2^B x 2^gbits) view: row r -> local brev_B(r)
+        gbase = ((uint64_t)t0 << gbits) | g_me;
+        gstride = (uint64_t)T << gbits;
+        lbase = (int)brev_bits((uint32_t)t0, B);
+    } else {
+        const uint64_t H = g_me >> lo, L = g_me & ((1ull << lo) - 1);
+        gbase = (H << (lo + B)) | ((uint64_t)t0 << lo) | L;
+        gstride = (uint64_t)T << lo;
+        lbase = t0;
     }
-    if (!direct) {
+    const uint4* srcp = a.src + poly_me * N + gbase;
+    uint4* smc = sm + c_me * GS;
+    if (!a.fin && !a.pmul) {
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < PER; i++) {
+                const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
+                cp_async16(smc + swz<B>(l), srcp + i * gstride);
+            }
+        }
+    } else if (live) {
+        uint4 stage[PER];
+#pragma unroll
+        for (int i = 0; i < PER; i++) stage[i] = srcp[i * gstride];
+        const ModC& M = a.mods[m_me];
+        const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
 #pragma unroll
         for (int i = 0; i < PER; i++) {
-            const int e = tid + i * NT;
-            const int c = e % C, r = e / C;
-            const uint64_t gg = gg0 + c;
-            if (gg >= a.total_groups) continue;
-            const uint64_t poly = gg >> gbits, g = gg & gmask;
-            uint64_t idx;
-            int l;
-            if (FIRST) {
-                idx = ((uint64_t)r << gbits) | g;
-                l = (int)brev_bits((uint32_t)r, B);
-            } else {
-                const uint64_t H = g >> lo, L = g & ((1ull << lo) - 1);
-                idx = (H << (lo + B)) | ((uint64_t)r << lo) | L;
-                l = r;
-            }
-            const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
-            const ModC& M = a.mods[m];
-            const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+            const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
+            const uint64_t idx = gbase + i * gstride;
             U128 x = u128_from(stage[i]);
-            if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + m * a.f_stride + idx)), q, M.qinv0);
-            if (a.pmul) x = mont_mul(x, u128_from(__ldg(a.pmul + poly * N + idx)), q, M.qinv0);
-            sm[c * GS + swz<B>(l)] = u128_to(x);
+            if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + m_me * a.f_stride + idx)), q, M.qinv0);
+            if (a.pmul) x = mont_mul(x, u128_from(__ldg(a.pmul + poly_me * N + idx)), q, M.qinv0);
+            smc[swz<B>(l)] = u128_to(x);
         }
     }
     cp_async_wait_all();
@@ -264,7 +281,11 @@ k_ntt_pass(const PassArgs a) {
         uint4* gsm = sm + c * GS;
         const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
+#if NTT_UNROLL_ROUNDS
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
         for (int rd = 0; rd < S::ROUNDS; rd++) {
             const int slo = rd * RB;
             const int w = (slo + RB <= B) ? slo : B - RB;   // E-element window [w, w + RB)
@@ -322,38 +343,47 @@ k_ntt_pass(const PassArgs a) {
     // ---------------- store phase: shared -> global, coalesced; all smem reads first
     {
         uint4 outv[PER];
+        if (FIRST) {
+            // groups are contiguous rows of the working order: e = tid + i NT -> (c, l), l fastest
 #pragma unroll
-        for (int i = 0; i < PER; i++) {
-            const int e = tid + i * NT;
-            int c, l;
-            if (FIRST) { c = e / G; l = e % G; }     // groups are contiguous rows of the working order
-            else { c = e % C; l = e / C; }
-            outv[i] = sm[c * GS + swz<B>(l)];
-        }
+            for (int i = 0; i < PER; i++) {
+                const int e = tid + i * NT;
+                outv[i] = sm[(e / G) * GS + swz<B>(e % G)];
+            }
 #pragma unroll
-        for (int i = 0; i < PER; i++) {
-            const int e = tid + i * NT;
-            int c, l;
-            if (FIRST) { c = e / G; l = e % G; }
-            else { c = e % C; l = e / C; }
-            const uint64_t gg = gg0 + c;
-            if (gg >= a.total_groups) continue;
-            const uint64_t poly = gg >> gbits, g = gg & gmask;
-            uint64_t idx;
-            if (FIRST) {
-                idx = ((uint64_t)brev_bits((uint32_t)g, gbits) << B) | (uint64_t)l;
-            } else {
-                const uint64_t H = g >> lo, Lw = g & ((1ull << lo) - 1);
-                idx = (H << (lo + B)) | ((uint64_t)l << lo) | Lw;
+            for (int i = 0; i < PER; i++) {
+                const int e = tid + i * NT;
+                const int c = e / G, l = e % G;
+                const uint64_t gg = gg0 + c;
+                if (gg >= a.total_groups) continue;
+                const uint64_t poly = gg >> gbits, g = gg & gmask;
+                const uint64_t idx = ((uint64_t)brev_bits((uint32_t)g, gbits) << B) | (uint64_t)l;
+                uint4 v = outv[i];
+                if (a.fout) {
+                    const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
+                    const ModC& M = a.mods[m];
+                    const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+                    v = u128_to(mont_mul(u128_from(v), u128_from(__ldg(a.fout + m * a.f_stride + idx)), q, M.qinv0));
+                }
+                a.dst[poly * N + idx] = v;
             }
-            uint4 v = outv[i];
-            if (a.fout) {
-                const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
-                const ModC& M = a.mods[m];
-                const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
-                v = u128_to(mont_mul(u128_from(v), u128_from(__ldg(a.fout + m * a.f_stride + idx)), q, M.qinv0));
+        } else {
+            // same (c_me, rows t0 + i T) assignment as the load phase
+#pragma unroll
+            for (int i = 0; i < PER; i++) outv[i] = smc[swz<B>(lbase + (i << LT))];
+            if (live) {
+                uint4* dstp = a.dst + poly_me * N + gbase;
+                if (a.fout) {
+                    const ModC& M = a.mods[m_me];
+                    const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+#pragma unroll
+                    for (int i = 0; i < PER; i++)
+                        outv[i] = u128_to(mont_mul(u128_from(outv[i]),
+                                                   u128_from(__ldg(a.fout + m_me * a.f_stride + gbase + i * gstride)), q, M.qinv0));
+                }
+#pragma unroll
+                for (int i = 0; i < PER; i++) dstp[i * gstride] = outv[i];
             }
-            a.dst[poly * N + idx] = v;
         }
     }
 }
@@ -404,7 +434,7 @@ static PassCfg multi_cfg_t(int B) {
         case 5: return make_cfg<5, 8, FIRST, SL>();
         case 6: return make_cfg<6, 8, FIRST, SL>();
         case 7: return make_cfg<7, 8, FIRST, SL>();
-        case 8: return make_cfg<8, 8, FIRST, SL, false, NTT_RB8>();
+        case 8: return make_cfg<8, NTT_C8, FIRST, SL, false, NTT_RB8>();
         default: return make_cfg<9, 4, FIRST, SL>();
     }
 }

@@ -1,0 +1,10 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/t11
+for v in default unroll c4 c4u; do
+  if [ $v != default ]; then export NTT128_LIB=$PWD/paper_2509_12494_b200/libntt128_$v.so; else unset NTT128_LIB; fi
+  python bench.py --steps 20 --warmup 5 --no-rows --no-cpu-baseline > gpurun_out/t11/bench_$v.json 2>&1
+  python -c "import json;d=json.load(open('gpurun_out/t11/bench_$v.json'));print('$v', '%.4e'%d['value'], d['roofline']['frac'], '%.4f %.4f'%(d['fwd_ms'], d['inv_ms']))"
+done
+unset NTT128_LIB
+python bench.py --steps 5 --warmup 3 --no-cpu-baseline --sweep 10,12,13,14,16,17 > gpurun_out/t11/bench_rows.json 2>&1
+python -c "import json;d=json.load(open('gpurun_out/t11/bench_rows.json'));print(json.dumps(d['rows'], indent=0))"
