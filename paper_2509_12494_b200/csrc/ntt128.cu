@@ -142,14 +142,18 @@ struct PassArgs {
 
 // Shape of one pass: groups of G = 2^B elements, E = 2^RB elements per thread
 // (register rounds of RB stages), T threads per group.
-template <int B, int RBMAX = 3>
+template <int B, int RBMAX = 3, int C = 8>
 struct PassShape {
     static constexpr int G = 1 << B;
     static constexpr int RB = B >= RBMAX ? RBMAX : B;  // radix-2^RB register rounds
     static constexpr int E = 1 << RB;
     static constexpr int T = G / E;
-    static constexpr int GS = G + 1;                // padded group stride (elements)
-    static constexpr int TS = G - 1;                // twiddle-set stride (odd: conflict-free across sets)
+    // Strides between groups (data) and twiddle sets, in 16-byte slots: an 8-lane shared
+    // memory phase covers min(C, 8) groups x 8/min(C, 8) adjacent rows, so the group
+    // stride must be = 8/C (mod 8) for C in {2, 4} and odd for C >= 8.
+    static constexpr int PADG = (C >= 8 || C == 1) ? 1 : 8 / C;
+    static constexpr int GS = G + PADG;
+    static constexpr int TS = (C >= 8 || C == 1) ? G - 1 : G + 8 / C;
     static constexpr int ROUNDS = (B + RB - 1) / RB;
 };
 
@@ -166,7 +170,7 @@ __device__ __forceinline__ int swz(int l) {
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX>
 __global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (768 / (C * PassShape<B, RBMAX>::T)) > 0 ? 768 / (C * PassShape<B, RBMAX>::T) : 1)
 k_ntt_pass(const PassArgs a) {
-    using S = PassShape<B, RBMAX>;
+    using S = PassShape<B, RBMAX, C>;
     constexpr int G = S::G, RB = S::RB, E = S::E, T = S::T, GS = S::GS, TS = S::TS;
     constexpr int NT = C * T;
     constexpr int NTW = (FIRST && !SINGLE) ? 1 : C;  // twiddle sets: a multi-pass first pass shares one (L = 0)
@@ -201,7 +205,10 @@ k_ntt_pass(const PassArgs a) {
 #pragma unroll
             for (int i = 0; i < TW_PER; i++) {
                 const int e = tid + i * NT;
-                if (e < NTW * (G - 1)) cp_async16(tsm + e, src + e);
+                if (e < NTW * (G - 1)) {
+                    const int c = TS == G - 1 ? 0 : e / (G - 1);
+                    cp_async16(tsm + e + c * (TS - (G - 1)), src + e);
+                }
             }
         } else {   // single pass, C polynomials per CTA, each with its own modulus
 #pragma unroll
@@ -211,7 +218,7 @@ k_ntt_pass(const PassArgs a) {
                     const int c = e / (G - 1), k = e - c * (G - 1);
                     const uint64_t gg = gg0 + c;
                     const uint32_t m = a.nq == 1 ? 0 : (uint32_t)((gg < a.total_groups ? gg : a.total_groups - 1) >> gbits);
-                    cp_async16(tsm + e, a.pt + m * a.pt_stride + k);
+                    cp_async16(tsm + c * TS + k, a.pt + m * a.pt_stride + k);
                 }
             }
         }
@@ -399,7 +406,7 @@ struct PassCfg {
 
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE = false, int RBMAX = 3>
 static PassCfg make_cfg() {
-    using S = PassShape<B, RBMAX>;
+    using S = PassShape<B, RBMAX, C>;
     PassCfg c;
     c.fn = k_ntt_pass<B, C, FIRST, SCALE_LAST, SINGLE, RBMAX>;
     c.B = B;
