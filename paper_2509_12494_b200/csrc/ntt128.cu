@@ -27,6 +27,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 #include <vector>
 
@@ -83,6 +84,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 
 // ----------------------------------------------------------------------------- twiddle generation
 // out[m][i] = scale_m * base_m^i (Montgomery form), i < count; pow2[m][k] = base_m^{2^k}
@@ -167,11 +169,77 @@ __device__ __forceinline__ int swz(int l) {
     return l ^ (f & 7);
 }
 
+// Register rounds of one pass on a CTA's tile in shared memory: RB stages on E elements
+// per thread, 8-lane conflict-free addressing (swz + padded group strides).
+template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX>
+__device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
+                                            const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
+    using S = PassShape<B, RBMAX, C>;
+    constexpr int RB = S::RB, E = S::E;
+#if NTT_UNROLL_ROUNDS
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+    for (int rd = 0; rd < S::ROUNDS; rd++) {
+        const int slo = rd * RB;
+        const int w = (slo + RB <= B) ? slo : B - RB;   // E-element window [w, w + RB)
+        const int tlo = t & ((1 << w) - 1), thi = (t >> w) << (w + RB);
+        U128 x[E];
+#pragma unroll
+        for (int k = 0; k < E; k++) x[k] = u128_from(gsm[swz<B>(thi | (k << w) | tlo)]);
+#pragma unroll
+        for (int bit = 0; bit < RB; bit++) {
+            const int sl = w + bit;                      // local stage
+            if (sl < slo) continue;                      // overlap of the last window
+            const bool trivial = FIRST && sl == 0 && !(SCALE_LAST && n == 1);
+            const bool last = SCALE_LAST && lo + sl == n - 1;
+            if (trivial) {
+#pragma unroll
+                for (int kk = 0; kk < E / 2; kk++) {
+                    const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                    const int k1 = k0 | (1 << bit);
+                    const U128 u = x[k0], v = x[k1];
+                    x[k0] = add_mod(u, v, q);
+                    x[k1] = sub_mod(u, v, q);
+                }
+            } else if (last) {
+#pragma unroll
+                for (int kk = 0; kk < E / 2; kk++) {
+                    const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                    const int k1 = k0 | (1 << bit);
+                    const int l0 = thi | (k0 << w) | tlo;
+                    const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
+                    const U128 us = mont_mul(x[k0], nf, q, qinv0);
+                    const U128 v = mont_mul(x[k1], wv, q, qinv0);
+                    x[k0] = add_mod(us, v, q);
+                    x[k1] = sub_mod(us, v, q);
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < E / 2; kk++) {
+                    const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                    const int k1 = k0 | (1 << bit);
+                    const int l0 = thi | (k0 << w) | tlo;
+                    const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
+                    const U128 u = x[k0];
+                    const U128 v = mont_mul(x[k1], wv, q, qinv0);
+                    x[k0] = add_mod(u, v, q);
+                    x[k1] = sub_mod(u, v, q);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < E; k++) gsm[swz<B>(thi | (k << w) | tlo)] = u128_to(x[k]);
+        __syncthreads();
+    }
+}
+
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX>
 __global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (768 / (C * PassShape<B, RBMAX>::T)) > 0 ? 768 / (C * PassShape<B, RBMAX>::T) : 1)
 k_ntt_pass(const PassArgs a) {
     using S = PassShape<B, RBMAX, C>;
-    constexpr int G = S::G, RB = S::RB, E = S::E, T = S::T, GS = S::GS, TS = S::TS;
+    constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS, TS = S::TS;
     constexpr int NT = C * T;
     constexpr int NTW = (FIRST && !SINGLE) ? 1 : C;  // twiddle sets: a multi-pass first pass shares one (L = 0)
     extern __shared__ uint4 sm[];
@@ -288,63 +356,7 @@ k_ntt_pass(const PassArgs a) {
         uint4* gsm = sm + c * GS;
         const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
-#if NTT_UNROLL_ROUNDS
-#pragma unroll
-#else
-#pragma unroll 1
-#endif
-        for (int rd = 0; rd < S::ROUNDS; rd++) {
-            const int slo = rd * RB;
-            const int w = (slo + RB <= B) ? slo : B - RB;   // E-element window [w, w + RB)
-            const int tlo = t & ((1 << w) - 1), thi = (t >> w) << (w + RB);
-            U128 x[E];
-#pragma unroll
-            for (int k = 0; k < E; k++) x[k] = u128_from(gsm[swz<B>(thi | (k << w) | tlo)]);
-#pragma unroll
-            for (int bit = 0; bit < RB; bit++) {
-                const int sl = w + bit;                      // local stage
-                if (sl < slo) continue;                      // overlap of the last window
-                const bool trivial = FIRST && sl == 0 && !(SCALE_LAST && n == 1);
-                const bool last = SCALE_LAST && lo + sl == n - 1;
-                if (trivial) {
-#pragma unroll
-                    for (int kk = 0; kk < E / 2; kk++) {
-                        const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
-                        const int k1 = k0 | (1 << bit);
-                        const U128 u = x[k0], v = x[k1];
-                        x[k0] = add_mod(u, v, q);
-                        x[k1] = sub_mod(u, v, q);
-                    }
-                } else if (last) {
-#pragma unroll
-                    for (int kk = 0; kk < E / 2; kk++) {
-                        const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
-                        const int k1 = k0 | (1 << bit);
-                        const int l0 = thi | (k0 << w) | tlo;
-                        const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
-                        const U128 us = mont_mul(x[k0], nf, q, qinv0);
-                        const U128 v = mont_mul(x[k1], wv, q, qinv0);
-                        x[k0] = add_mod(us, v, q);
-                        x[k1] = sub_mod(us, v, q);
-                    }
-                } else {
-#pragma unroll
-                    for (int kk = 0; kk < E / 2; kk++) {
-                        const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
-                        const int k1 = k0 | (1 << bit);
-                        const int l0 = thi | (k0 << w) | tlo;
-                        const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
-                        const U128 u = x[k0];
-                        const U128 v = mont_mul(x[k1], wv, q, qinv0);
-                        x[k0] = add_mod(u, v, q);
-                        x[k1] = sub_mod(u, v, q);
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < E; k++) gsm[swz<B>(thi | (k << w) | tlo)] = u128_to(x[k]);
-            __syncthreads();
-        }
+pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX>(gsm, tws, t, lo, n, q, qinv0, nf);
     }
 
     // ---------------- store phase: shared -> global, coalesced; all smem reads first
