@@ -9,6 +9,9 @@
 #include <cuda_runtime.h>
 #include "../../paper_2509_12494_b200/csrc/arith128.cuh"
 using namespace ntt128;
+#ifndef EPT
+#define EPT 8
+#endif
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
 
 // a + b mod q: d = a + b - q in one 3-input chain; if it borrowed (d < 0), add q back
@@ -88,13 +91,13 @@ int main() {
     unsigned __int128 q = ~(unsigned __int128)0 - 8257535 + 1;  // cfg2 prime
     unsigned __int128 inv = 1; for (int i = 0; i < 7; i++) inv *= 2 - q * inv;
     ModC mc = {}; for (int i = 0; i < 4; i++) mc.q[i] = (uint32_t)(q >> (32 * i)); mc.qinv0 = (uint32_t)(-inv);
-    constexpr int E = 8;
+    constexpr int E = EPT;
     const int threads = 256, iters = 256;
     ModC* dm; uint4* dtw; int* dbad; CK(cudaMalloc(&dm, sizeof(ModC))); CK(cudaMemcpy(dm, &mc, sizeof(ModC), cudaMemcpyHostToDevice));
     std::vector<uint4> tw(E / 2); for (int k = 0; k < E / 2; k++) tw[k] = make_uint4(0x12345 + k, 0x6789 * k, 0xabcdef, 0x0fffffff);
     CK(cudaMalloc(&dtw, 16 * E)); CK(cudaMemcpy(dtw, tw.data(), 16 * E / 2, cudaMemcpyHostToDevice)); CK(cudaMalloc(&dbad, 4));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int bpsm : {3, 6}) {
+    for (int bpsm : {1, 2, 3, 4}) {
         const int blocks = sms * bpsm;
         size_t n = (size_t)threads * blocks * E;
         std::vector<uint4> h(n); for (size_t i = 0; i < n; i++) h[i] = make_uint4(i * 2654435761u, i, 77, 0x7fffffff);
