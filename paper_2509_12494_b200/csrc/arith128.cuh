@@ -159,6 +159,100 @@ __device__ __forceinline__ U128 mont_mul(const U128& a, const U128& b, const uin
     return r;
 }
 
+// ---------------------------------------------------------------------------------------
+// Lazy-reduction variants for moduli q < 2^126 (4q < 2^128: values kept in [0, 2q) fit four
+// words with room for one addition; Harvey-style butterflies).
+// mont_mul_lazy: a < 2q, b < q -> a b R^-1 mod q + {0, q}, i.e. a value in [0, 2q)
+// (T < (2q q + R q) / R < 1.5 q); no final subtraction and no fifth-word carry.
+__device__ __forceinline__ U128 mont_mul_lazy(const U128& a, const U128& b, const uint32_t q[4], uint32_t qinv0) {
+    uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0, e4 = 0, o1, o2, o3, o4, m;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
+            "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
+            "madc.lo.cc.u32 %2, %5, %7, %2;\n\t"
+            "madc.hi.cc.u32 %3, %5, %7, %3;\n\t"
+            "addc.u32       %4, %4, 0;"
+            : "+r"(e0), "+r"(e1), "+r"(e2), "+r"(e3), "+r"(e4)
+            : "r"(a.w[i]), "r"(b.w[0]), "r"(b.w[2]));
+        asm("mul.lo.u32 %0, %4, %5;\n\t"
+            "mul.hi.u32 %1, %4, %5;\n\t"
+            "mul.lo.u32 %2, %4, %6;\n\t"
+            "mul.hi.u32 %3, %4, %6;"
+            : "=r"(o1), "=r"(o2), "=r"(o3), "=r"(o4)
+            : "r"(a.w[i]), "r"(b.w[1]), "r"(b.w[3]));
+        m = e0 * qinv0;
+        asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
+            "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
+            "madc.lo.cc.u32 %2, %5, %7, %2;\n\t"
+            "madc.hi.cc.u32 %3, %5, %7, %3;\n\t"
+            "addc.u32       %4, %4, 0;"
+            : "+r"(e0), "+r"(e1), "+r"(e2), "+r"(e3), "+r"(e4)
+            : "r"(m), "r"(q[0]), "r"(q[2]));
+        // O + m (q1 2^32 + q3 2^96) < 2^160: no carry out of word 4
+        asm("mad.lo.cc.u32  %0, %4, %5, %0;\n\t"
+            "madc.hi.cc.u32 %1, %4, %5, %1;\n\t"
+            "madc.lo.cc.u32 %2, %4, %6, %2;\n\t"
+            "madc.hi.u32    %3, %4, %6, %3;"
+            : "+r"(o1), "+r"(o2), "+r"(o3), "+r"(o4)
+            : "r"(m), "r"(q[1]), "r"(q[3]));
+        // (E + O) / 2^32 < 2^129 / 2^32 ... the running value stays < 2q after the shift
+        asm("add.cc.u32  %0, %4, %8;\n\t"
+            "addc.cc.u32 %1, %5, %9;\n\t"
+            "addc.cc.u32 %2, %6, %10;\n\t"
+            "addc.u32    %3, %7, %11;"
+            : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
+            : "r"(e1), "r"(e2), "r"(e3), "r"(e4), "r"(o1), "r"(o2), "r"(o3), "r"(o4));
+        e4 = 0;
+    }
+    return U128{{e0, e1, e2, e3}};
+}
+
+// x - 2q if x >= 2q (x < 4q < 2^128); q2 = 2q
+__device__ __forceinline__ U128 reduce_2q(const U128& x, const uint32_t q2[4]) {
+    uint32_t d0, d1, d2, d3, bw;
+    asm("sub.cc.u32  %0, %5, %9;\n\t"
+        "subc.cc.u32 %1, %6, %10;\n\t"
+        "subc.cc.u32 %2, %7, %11;\n\t"
+        "subc.cc.u32 %3, %8, %12;\n\t"
+        "subc.u32    %4, 0, 0;"
+        : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(d3), "=r"(bw)
+        : "r"(x.w[0]), "r"(x.w[1]), "r"(x.w[2]), "r"(x.w[3]), "r"(q2[0]), "r"(q2[1]), "r"(q2[2]), "r"(q2[3]));
+    U128 r;
+    r.w[0] = (x.w[0] & bw) | (d0 & ~bw);
+    r.w[1] = (x.w[1] & bw) | (d1 & ~bw);
+    r.w[2] = (x.w[2] & bw) | (d2 & ~bw);
+    r.w[3] = (x.w[3] & bw) | (d3 & ~bw);
+    return r;
+}
+
+// lazy butterfly outputs: u + t and u - t + 2q, each brought back to [0, 2q)
+__device__ __forceinline__ U128 add_lazy(const U128& u, const U128& t, const uint32_t q2[4]) {
+    U128 s;
+    asm("add.cc.u32  %0, %4, %8;\n\t"
+        "addc.cc.u32 %1, %5, %9;\n\t"
+        "addc.cc.u32 %2, %6, %10;\n\t"
+        "addc.u32    %3, %7, %11;"
+        : "=r"(s.w[0]), "=r"(s.w[1]), "=r"(s.w[2]), "=r"(s.w[3])
+        : "r"(u.w[0]), "r"(u.w[1]), "r"(u.w[2]), "r"(u.w[3]), "r"(t.w[0]), "r"(t.w[1]), "r"(t.w[2]), "r"(t.w[3]));
+    return reduce_2q(s, q2);
+}
+__device__ __forceinline__ U128 sub_lazy(const U128& u, const U128& t, const uint32_t q2[4]) {
+    U128 s;
+    asm("sub.cc.u32  %0, %4, %8;\n\t"
+        "subc.cc.u32 %1, %5, %9;\n\t"
+        "subc.cc.u32 %2, %6, %10;\n\t"
+        "subc.u32    %3, %7, %11;\n\t"
+        "add.cc.u32  %0, %0, %12;\n\t"
+        "addc.cc.u32 %1, %1, %13;\n\t"
+        "addc.cc.u32 %2, %2, %14;\n\t"
+        "addc.u32    %3, %3, %15;"
+        : "=&r"(s.w[0]), "=&r"(s.w[1]), "=&r"(s.w[2]), "=&r"(s.w[3])
+        : "r"(u.w[0]), "r"(u.w[1]), "r"(u.w[2]), "r"(u.w[3]), "r"(t.w[0]), "r"(t.w[1]), "r"(t.w[2]), "r"(t.w[3]),
+          "r"(q2[0]), "r"(q2[1]), "r"(q2[2]), "r"(q2[3]));
+    return reduce_2q(s, q2);
+}
+
 // a < q check (for NTT128_FLAG_CHECK_INPUT): borrow out of a - q
 __device__ __forceinline__ bool lt_q(const U128& a, const uint32_t q[4]) {
     uint32_t bw;

@@ -136,6 +136,7 @@ struct PassArgs {
     const uint4* fin;      // optional [nq][f_stride]: factor applied at load, by natural input index
     const uint4* fout;     // optional [nq][f_stride]: factor applied at store, by natural output index
     const ModC* mods;      // [nq]
+    const uint32_t* order; // optional [batch]: polynomial processed by CTA slot (lazy-path polynomials first)
     uint64_t pt_stride, f_stride;
     uint64_t total_groups; // batch << (n - B)
     uint32_t n, lo, nq;
@@ -171,9 +172,18 @@ __device__ __forceinline__ int swz(int l) {
 
 // Register rounds of one pass on a CTA's tile in shared memory: RB stages on E elements
 // per thread, 8-lane conflict-free addressing (swz + padded group strides).
-template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX>
+template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, bool LAZY>
 __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
                                             const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
+    // LAZY (q < 2^126): operands and results in [0, 2q), Harvey butterflies, no final
+    // Montgomery subtraction; the last pass's store brings results back to [0, q).
+    uint32_t q2[4];
+    if (LAZY) {
+        q2[0] = q[0] << 1;
+        q2[1] = (q[1] << 1) | (q[0] >> 31);
+        q2[2] = (q[2] << 1) | (q[1] >> 31);
+        q2[3] = (q[3] << 1) | (q[2] >> 31);
+    }
     using S = PassShape<B, RBMAX, C>;
     constexpr int RB = S::RB, E = S::E;
 #if NTT_UNROLL_ROUNDS
@@ -200,8 +210,8 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
                     const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
                     const int k1 = k0 | (1 << bit);
                     const U128 u = x[k0], v = x[k1];
-                    x[k0] = add_mod(u, v, q);
-                    x[k1] = sub_mod(u, v, q);
+                    x[k0] = LAZY ? add_lazy(u, v, q2) : add_mod(u, v, q);
+                    x[k1] = LAZY ? sub_lazy(u, v, q2) : sub_mod(u, v, q);
                 }
             } else if (last) {
 #pragma unroll
@@ -210,10 +220,10 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
                     const int k1 = k0 | (1 << bit);
                     const int l0 = thi | (k0 << w) | tlo;
                     const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
-                    const U128 us = mont_mul(x[k0], nf, q, qinv0);
-                    const U128 v = mont_mul(x[k1], wv, q, qinv0);
-                    x[k0] = add_mod(us, v, q);
-                    x[k1] = sub_mod(us, v, q);
+                    const U128 us = LAZY ? mont_mul_lazy(x[k0], nf, q, qinv0) : mont_mul(x[k0], nf, q, qinv0);
+                    const U128 v = LAZY ? mont_mul_lazy(x[k1], wv, q, qinv0) : mont_mul(x[k1], wv, q, qinv0);
+                    x[k0] = LAZY ? add_lazy(us, v, q2) : add_mod(us, v, q);
+                    x[k1] = LAZY ? sub_lazy(us, v, q2) : sub_mod(us, v, q);
                 }
             } else {
 #pragma unroll
@@ -223,9 +233,9 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
                     const int l0 = thi | (k0 << w) | tlo;
                     const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
                     const U128 u = x[k0];
-                    const U128 v = mont_mul(x[k1], wv, q, qinv0);
-                    x[k0] = add_mod(u, v, q);
-                    x[k1] = sub_mod(u, v, q);
+                    const U128 v = LAZY ? mont_mul_lazy(x[k1], wv, q, qinv0) : mont_mul(x[k1], wv, q, qinv0);
+                    x[k0] = LAZY ? add_lazy(u, v, q2) : add_mod(u, v, q);
+                    x[k1] = LAZY ? sub_lazy(u, v, q2) : sub_mod(u, v, q);
                 }
             }
         }
@@ -248,7 +258,10 @@ k_ntt_pass(const PassArgs a) {
     const uint32_t n = a.n, lo = a.lo, gbits = n - B;
     const uint64_t N = 1ull << n;
     const uint64_t gmask = (1ull << gbits) - 1;
-    const uint64_t gg0 = (uint64_t)blockIdx.x * C;
+    uint64_t gg0 = (uint64_t)blockIdx.x * C;
+    // multi-pass CTAs hold groups of one polynomial: visit polynomials in the plan's order
+    // (all lazy-path moduli first) so one code path at a time is hot in the I-cache
+    if (!SINGLE && a.order) gg0 = ((uint64_t)a.order[gg0 >> gbits] << gbits) | (gg0 & gmask);
     const int tid = threadIdx.x;
 
     // ---------------- load phase: twiddles and data -> shared memory, all copies in flight
@@ -356,7 +369,10 @@ k_ntt_pass(const PassArgs a) {
         uint4* gsm = sm + c * GS;
         const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
-pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX>(gsm, tws, t, lo, n, q, qinv0, nf);
+if (!SINGLE && (q[3] >> 30) == 0)   // uniform per CTA: all C groups share the polynomial
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, true>(gsm, tws, t, lo, n, q, qinv0, nf);
+        else
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, false>(gsm, tws, t, lo, n, q, qinv0, nf);
     }
 
     // ---------------- store phase: shared -> global, coalesced; all smem reads first
@@ -390,6 +406,15 @@ pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX>(gsm, tws, t, lo, n, q, qinv0, nf);
             // same (c_me, rows t0 + i T) assignment as the load phase
 #pragma unroll
             for (int i = 0; i < PER; i++) outv[i] = smc[swz<B>(lbase + (i << LT))];
+            if (!SINGLE && lo + B == n && !a.fout) {
+                // lazy polynomials (q < 2^126) leave the last pass in [0, 2q): canonicalize
+                const ModC& M = a.mods[m_me];
+                const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+                if ((q[3] >> 30) == 0) {
+#pragma unroll
+                    for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q));
+                }
+            }
             if (live) {
                 uint4* dstp = a.dst + poly_me * N + gbase;
                 if (a.fout) {
@@ -481,6 +506,7 @@ struct ntt128_plan_s {
     std::vector<u128> q_host;
     int* d_err = nullptr;
     std::vector<uint4*> d_pt_fwd, d_pt_inv, d_pt_inv_r;  // per pass, [nq][pt_stride]
+    uint32_t* d_order = nullptr;                         // [batch] CTA-slot -> polynomial (nq == batch)
     std::vector<uint64_t> pt_stride;
 };
 
@@ -498,6 +524,7 @@ static void plan_free(ntt128_plan_s* p) {
     cudaFree(p->d_f_untwist);
     cudaFree(p->d_f_untwist_r);
     cudaFree(p->d_err);
+    cudaFree(p->d_order);
     for (size_t i = 0; i < p->d_pt_fwd.size(); i++) {
         if (p->d_pt_inv_r[i] != p->d_pt_inv[i]) cudaFree(p->d_pt_inv_r[i]);
         cudaFree(p->d_pt_fwd[i]);
@@ -664,6 +691,17 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
             }
         }
     }
+    // polynomial order for multi-pass launches: moduli < 2^126 (lazy path) first
+    if (st == NTT128_OK && n_moduli > 1 && p->bits.size() > 1) {
+        std::vector<uint32_t> order;
+        for (uint32_t m = 0; m < n_moduli; m++)
+            if ((qs[m] >> 126) == 0) order.push_back(m);
+        for (uint32_t m = 0; m < n_moduli; m++)
+            if ((qs[m] >> 126) != 0) order.push_back(m);
+        if (cudaMalloc(&p->d_order, order.size() * sizeof(uint32_t)) != cudaSuccess) st = NTT128_ERR_OOM;
+        else if (cudaMemcpy(p->d_order, order.data(), order.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess)
+            st = NTT128_ERR_CUDA;
+    }
     // per-pass twiddle tables in consumption order (gathered from the power tables)
     if (st == NTT128_OK) {
         int lo = 0;
@@ -744,6 +782,7 @@ static ntt128_status run_transform(const ntt128_plan_s* p, const uint4* src, uin
         a.src = i == 0 ? src : dst;
         a.dst = dst;
         a.mods = p->d_mods;
+        a.order = p->d_order;
         a.pt_stride = p->pt_stride[i];
         a.f_stride = p->N;
         a.total_groups = (uint64_t)p->batch << (n - B);

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/t20
+timeout 900 python -m pytest tests/test_gpu_ntt.py -x -q -p no:cacheprovider > gpurun_out/t20/pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/t20/pytest.log
+tail -2 gpurun_out/t20/pytest.log
+python tools/exp_lazy.py
+python bench.py --steps 20 --warmup 5 --no-rows --no-cpu-baseline > gpurun_out/t20/bench.json 2>&1
+python -c "import json;d=json.load(open('gpurun_out/t20/bench.json'));print('%.4e'%d['value'], d['roofline']['frac'], '%.4f %.4f'%(d['fwd_ms'], d['inv_ms']))"

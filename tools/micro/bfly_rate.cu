@@ -76,6 +76,12 @@ __global__ void __launch_bounds__(256) k_bfly(uint4* io, const uint4* tw, const 
                 const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
                 const int k1 = k0 | (1 << bit);
                 const U128 u = x[k0];
+                if (V == 3) {
+                    const uint32_t q2[4] = {M.r2[0], M.r2[1], M.r2[2], M.r2[3]};   // r2 slot holds 2q here
+                    const U128 v = mont_mul_lazy(x[k1], w[(kk + bit) % (E / 2)], q, M.qinv0);
+                    x[k0] = add_lazy(u, v, q2); x[k1] = sub_lazy(u, v, q2);
+                    continue;
+                }
                 const U128 v = mont_mul(x[k1], w[(kk + bit) % (E / 2)], q, M.qinv0);
                 if (V != 1) { x[k0] = add_mod(u, v, q); x[k1] = sub_mod(u, v, q); }
                 else { x[k0] = add_mod_p(u, v, q); x[k1] = sub_mod_p(u, v, q); }
@@ -97,7 +103,26 @@ int main() {
     std::vector<uint4> tw(E / 2); for (int k = 0; k < E / 2; k++) tw[k] = make_uint4(0x12345 + k, 0x6789 * k, 0xabcdef, 0x0fffffff);
     CK(cudaMalloc(&dtw, 16 * E)); CK(cudaMemcpy(dtw, tw.data(), 16 * E / 2, cudaMemcpyHostToDevice)); CK(cudaMalloc(&dbad, 4));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int bpsm : {1, 2, 3, 4}) {
+    {   // lazy variant on a 125-bit prime (q = 2^125 - 2^18... any odd q < 2^126 for timing)
+        unsigned __int128 q5 = ((unsigned __int128)1 << 125) - 262143;  // 2^125 - 2^18 + 1
+        unsigned __int128 inv5 = 1; for (int i = 0; i < 7; i++) inv5 *= 2 - q5 * inv5;
+        ModC m5 = {}; for (int i = 0; i < 4; i++) { m5.q[i] = (uint32_t)(q5 >> (32 * i)); m5.r2[i] = (uint32_t)((2 * q5) >> (32 * i)); }
+        m5.qinv0 = (uint32_t)(-inv5);
+        ModC* dm5; CK(cudaMalloc(&dm5, sizeof(ModC))); CK(cudaMemcpy(dm5, &m5, sizeof(ModC), cudaMemcpyHostToDevice));
+        const int blocks = sms * 3; size_t n = (size_t)threads * blocks * E;
+        std::vector<uint4> h(n); for (size_t i = 0; i < n; i++) h[i] = make_uint4(i * 2654435761u, i, 77, 0x0fffffff);
+        uint4* d; CK(cudaMalloc(&d, n * 16)); CK(cudaMemcpy(d, h.data(), n * 16, cudaMemcpyHostToDevice));
+        for (int v : {0, 3}) {
+            auto launch = [&]() { if (v == 0) k_bfly<0, E><<<blocks, threads>>>(d, dtw, dm5, iters, dbad); else k_bfly<3, E><<<blocks, threads>>>(d, dtw, dm5, iters, dbad); };
+            launch(); CK(cudaDeviceSynchronize());
+            float best = 1e30f;
+            for (int r = 0; r < 3; r++) { cudaEventRecord(e0); launch(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms); }
+            double bf = (double)threads * blocks * iters * 3 * (E / 2);
+            printf("{\"q125_variant\":%d,\"bfly_per_clk_sm_at1965\":%.3f}\n", v, bf / (best * 1e-3) / (sms * 1.965e9));
+        }
+        cudaFree(d);
+    }
+    for (int bpsm : {3}) {
         const int blocks = sms * bpsm;
         size_t n = (size_t)threads * blocks * E;
         std::vector<uint4> h(n); for (size_t i = 0; i < n; i++) h[i] = make_uint4(i * 2654435761u, i, 77, 0x7fffffff);
