@@ -172,7 +172,7 @@ __device__ __forceinline__ int swz(int l) {
 
 // Register rounds of one pass on a CTA's tile in shared memory: RB stages on E elements
 // per thread, 8-lane conflict-free addressing (swz + padded group strides).
-template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, bool LAZY>
+template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, bool LAZY, bool WARPSYNC>
 __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
                                             const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
     // LAZY (q < 2^126): operands and results in [0, 2q), Harvey butterflies, no final
@@ -241,7 +241,7 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
         }
 #pragma unroll
         for (int k = 0; k < E; k++) gsm[swz<B>(thi | (k << w) | tlo)] = u128_to(x[k]);
-        __syncthreads();
+        if (WARPSYNC) __syncwarp(); else __syncthreads();
     }
 }
 
@@ -350,8 +350,12 @@ k_ntt_pass(const PassArgs a) {
     __syncthreads();
 
     // ---------------- register rounds: RB stages on E elements per thread
+    // Groups of at most 32 threads are owned by whole warps (c = tid / T), so the exchanges
+    // between rounds never leave a warp and need only __syncwarp (pass_rounds); larger
+    // groups keep the interleaved mapping and block barriers.
     {
-        const int c = tid % C, t = tid / C;
+        constexpr bool WARPMAP = T <= 32 && (32 % T) == 0;
+        const int c = WARPMAP ? tid / T : tid % C, t = WARPMAP ? tid % T : tid / C;
         const uint64_t gg = gg0 + c;
         const uint64_t ggc = gg < a.total_groups ? gg : a.total_groups - 1;
         const uint32_t m = a.nq == 1 ? 0 : (uint32_t)(ggc >> gbits);
@@ -370,9 +374,10 @@ k_ntt_pass(const PassArgs a) {
         const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
 if (!SINGLE && (q[3] >> 30) == 0)   // uniform per CTA: all C groups share the polynomial
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, true>(gsm, tws, t, lo, n, q, qinv0, nf);
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, true, WARPMAP>(gsm, tws, t, lo, n, q, qinv0, nf);
         else
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, false>(gsm, tws, t, lo, n, q, qinv0, nf);
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, false, WARPMAP>(gsm, tws, t, lo, n, q, qinv0, nf);
+        if (WARPMAP) __syncthreads();   // the store phase reads every group
     }
 
     // ---------------- store phase: shared -> global, coalesced; all smem reads first
