@@ -87,22 +87,129 @@ __device__ __forceinline__ U128 sub_mod(const U128& a, const U128& b, const uint
     return r;
 }
 
-// Montgomery product a * b * 2^-128 mod q, word-serial CIOS with 32-bit digits.
-// Preconditions: b < q, a < 2^128 (then a b < q R and the value before the final
-// subtraction is T < 2q, which may exceed 2^128: its bit 128 is kept in e4).
+// Montgomery product core, even/odd alternating CIOS (R = 2^128, 32-bit digits b_i of b).
+// Preconditions: b < q and either a < 2^128 (any odd q < 2^128) or, for the lazy
+// callers, a < 4q with q < 2^126 / a < 2q with q < 2^127.  Output: T = a b R^-1 + {0, q},
+// T < 2q, as five words t[0..4] (t[4] <= 1; t[4] == 0 when 2q <= 2^128).
 //
-// The running value is split into an even-aligned part E (words 0..4) and an
-// odd-aligned part O (words 1..5), so every IMAD.WIDE.U32 writes an aligned
-// register pair and no register is shared by two pair layouts (the plain CIOS
-// chain needs ~30 moves per call for that).  Per digit a_i:
-//   E += a_i (b0 + b2 2^64)            2 IMAD.WIDE, carry chain
-//   O  = a_i (b1 2^32 + b3 2^96)       2 IMAD.WIDE, no carries (disjoint words)
-//   m  = E_0 q' mod 2^32               1 IMAD
-//   E += m (q0 + q2 2^64), O += m (q1 2^32 + q3 2^96)   4 IMAD.WIDE
-//   E  = (E + O) / 2^32                5-word add (E_0 == 0 mod 2^32 here)
-// = 32 IMAD.WIDE + 4 IMAD per call (the 36 algorithmic products of §8(d)).
-// Measured alone: 2.36e11 mulmod/s on B200 = 91 % of the IMAD.WIDE issue peak.
+// The running value is held as 2^32 T_i = X + 2^32 Y with two multiword accumulators
+// whose 64-bit partial products are all register-pair aligned: X collects the
+// a_even b_i = (a0 + a2 2^64) b_i and m (q0 + q2 2^64) products, Y the odd ones
+// (a1 + a3 2^64) b_i and m (q1 + q3 2^64).  After a digit X_0 = 0 and the division by
+// 2^32 is a change of roles instead of a 5-word add: the next X is Y with X_1 added to
+// its word 0 (the carry of that add has weight 2^32 and enters the next Y chain as
+// its carry-in), the next Y is X / 2^64 (words X_2, X_3, X_4 used as the addends of
+// the next a_odd b_i products, so the shift costs nothing).  Per digit: 8 IMAD.WIDE,
+// 1 IMAD (m = X_0 q'), 4 carry ops; one 5-word add at the end.  Every dropped carry
+// is proven absent in tools/model/mont_eo_model.c (which asserts it on 10^6 cases
+// including q = 2^128 - 1 and a = 2^128 - 1).
+template <bool TOP>
+__device__ __forceinline__ void mont_core(const U128& a, const U128& b, const uint32_t q[4], uint32_t qinv0,
+                                          uint32_t t[5]) {
+    uint32_t x0, x1, x2, x3, x4, y0, y1, y2, y3, y4, m;
+    // digit 0: X = a_even b0, Y = a_odd b0 (fresh 64-bit products, no carries)
+    asm("{\n\t.reg .u64 p;\n\t"
+        "mul.wide.u32 p, %8, %12;\n\tmov.b64 {%0, %1}, p;\n\t"
+        "mul.wide.u32 p, %10, %12;\n\tmov.b64 {%2, %3}, p;\n\t"
+        "mul.wide.u32 p, %9, %12;\n\tmov.b64 {%4, %5}, p;\n\t"
+        "mul.wide.u32 p, %11, %12;\n\tmov.b64 {%6, %7}, p;\n\t}"
+        : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3), "=r"(y0), "=r"(y1), "=r"(y2), "=r"(y3)
+        : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(b.w[0]));
+    m = x0 * qinv0;
+    asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
+        "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
+        "madc.lo.cc.u32 %2, %5, %7, %2;\n\t"
+        "madc.hi.cc.u32 %3, %5, %7, %3;\n\t"
+        "addc.u32       %4, 0, 0;"
+        : "+r"(x0), "+r"(x1), "+r"(x2), "+r"(x3), "=r"(x4)
+        : "r"(m), "r"(q[0]), "r"(q[2]));
+    asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
+        "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
+        "madc.lo.cc.u32 %2, %5, %7, %2;\n\t"
+        "madc.hi.cc.u32 %3, %5, %7, %3;\n\t"
+        "addc.u32       %4, 0, 0;"
+        : "+r"(y0), "+r"(y1), "+r"(y2), "+r"(y3), "=r"(y4)
+        : "r"(m), "r"(q[1]), "r"(q[3]));
+#pragma unroll
+    for (int i = 1; i < 4; i++) {
+        uint32_t n0, n1, n2, n3, n4;
+        // X' = Y + X_1 (+ a_even b_i below); Y' = X / 2^64 + carry + a_odd b_i (no carry out)
+        asm("add.cc.u32     %0, %0, %9;\n\t"
+            "madc.lo.cc.u32 %5, %12, %13, %10;\n\t"
+            "madc.hi.cc.u32 %6, %12, %13, %11;\n\t"
+            "madc.lo.cc.u32 %7, %14, %13, %15;\n\t"
+            "madc.hi.u32    %8, %14, %13, 0;\n\t"
+            "mad.lo.cc.u32  %0, %16, %13, %0;\n\t"
+            "madc.hi.cc.u32 %1, %16, %13, %1;\n\t"
+            "madc.lo.cc.u32 %2, %17, %13, %2;\n\t"
+            "madc.hi.cc.u32 %3, %17, %13, %3;\n\t"
+            "addc.u32       %4, %4, 0;"
+            : "+r"(y0), "+r"(y1), "+r"(y2), "+r"(y3), "+r"(y4), "=&r"(n0), "=&r"(n1), "=&r"(n2), "=&r"(n3)
+            : "r"(x1), "r"(x2), "r"(x3), "r"(a.w[1]), "r"(b.w[i]), "r"(a.w[3]), "r"(x4), "r"(a.w[0]), "r"(a.w[2]));
+        m = y0 * qinv0;
+        asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
+            "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
+            "madc.lo.cc.u32 %2, %5, %7, %2;\n\t"
+            "madc.hi.cc.u32 %3, %5, %7, %3;\n\t"
+            "addc.u32       %4, %4, 0;"
+            : "+r"(y0), "+r"(y1), "+r"(y2), "+r"(y3), "+r"(y4)
+            : "r"(m), "r"(q[0]), "r"(q[2]));
+        asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
+            "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
+            "madc.lo.cc.u32 %2, %5, %7, %2;\n\t"
+            "madc.hi.cc.u32 %3, %5, %7, %3;\n\t"
+            "addc.u32       %4, 0, 0;"
+            : "+r"(n0), "+r"(n1), "+r"(n2), "+r"(n3), "=r"(n4)
+            : "r"(m), "r"(q[1]), "r"(q[3]));
+        // roles: X <- X' (held in y), Y <- Y' (held in n)
+        x0 = y0; x1 = y1; x2 = y2; x3 = y3; x4 = y4;
+        y0 = n0; y1 = n1; y2 = n2; y3 = n3; y4 = n4;
+    }
+    // T = Y + X / 2^32 (X_0 == 0)
+    if (TOP) {
+        asm("add.cc.u32  %0, %5, %10;\n\t"
+            "addc.cc.u32 %1, %6, %11;\n\t"
+            "addc.cc.u32 %2, %7, %12;\n\t"
+            "addc.cc.u32 %3, %8, %13;\n\t"
+            "addc.u32    %4, %9, 0;"
+            : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4])
+            : "r"(y0), "r"(y1), "r"(y2), "r"(y3), "r"(y4), "r"(x1), "r"(x2), "r"(x3), "r"(x4));
+    } else {   // T < 2q <= 2^128: word 4 is zero
+        asm("add.cc.u32  %0, %4, %8;\n\t"
+            "addc.cc.u32 %1, %5, %9;\n\t"
+            "addc.cc.u32 %2, %6, %10;\n\t"
+            "addc.u32    %3, %7, %11;"
+            : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3])
+            : "r"(y0), "r"(y1), "r"(y2), "r"(y3), "r"(x1), "r"(x2), "r"(x3), "r"(x4));
+        t[4] = 0;
+    }
+}
+
+// Montgomery product a * b * 2^-128 mod q, canonical result.  Preconditions: b < q,
+// a < 2^128, q odd.  32 IMAD.WIDE + 4 IMAD per call (the 36 algorithmic products of
+// §8(d)); T < 2q keeps its bit 128 in t[4]; one conditional subtraction.
 __device__ __forceinline__ U128 mont_mul(const U128& a, const U128& b, const uint32_t q[4], uint32_t qinv0) {
+    uint32_t t[5];
+    mont_core<true>(a, b, q, qinv0, t);
+    uint32_t d0, d1, d2, d3, bw;
+    asm("sub.cc.u32  %0, %5, %10;\n\t"
+        "subc.cc.u32 %1, %6, %11;\n\t"
+        "subc.cc.u32 %2, %7, %12;\n\t"
+        "subc.cc.u32 %3, %8, %13;\n\t"
+        "subc.u32    %4, %9, 0;"
+        : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(d3), "=r"(bw)
+        : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]));
+    U128 r;
+    r.w[0] = (t[0] & bw) | (d0 & ~bw);
+    r.w[1] = (t[1] & bw) | (d1 & ~bw);
+    r.w[2] = (t[2] & bw) | (d2 & ~bw);
+    r.w[3] = (t[3] & bw) | (d3 & ~bw);
+    return r;
+}
+
+// Previous formulation (one accumulator pair merged every digit), kept for the
+// microbenchmark comparison in tools/micro/bfly_rate.cu.
+__device__ __forceinline__ U128 mont_mul_v1(const U128& a, const U128& b, const uint32_t q[4], uint32_t qinv0) {
     uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0, e4 = 0, o1, o2, o3, o4, o5, m;
 #pragma unroll
     for (int i = 0; i < 4; i++) {
@@ -160,55 +267,20 @@ __device__ __forceinline__ U128 mont_mul(const U128& a, const U128& b, const uin
 }
 
 // ---------------------------------------------------------------------------------------
-// Lazy-reduction variants for moduli q < 2^126 (4q < 2^128: values kept in [0, 2q) fit four
-// words with room for one addition; Harvey-style butterflies).
-// mont_mul_lazy: a < 2q, b < q -> a b R^-1 mod q + {0, q}, i.e. a value in [0, 2q)
-// (T < (2q q + R q) / R < 1.5 q); no final subtraction and no fifth-word carry.
+// Lazy reduction, by modulus class:
+//   q < 2^126 ("lazy"): butterfly values in [0, 4q) (4q < 2^128), Harvey butterflies;
+//   2^126 <= q < 2^127 ("half"): values in [0, 2q) (2q < 2^128), add/sub modulo 2q;
+//   q >= 2^127: canonical values (mont_mul, add_mod, sub_mod).
+// mont_mul_lazy: b < q and a < 4q (q < 2^126) or a < 2q (q < 2^127) -> T = a b R^-1 + {0, q}
+// in [0, 2q) (T < q (1 + a / R) < 2q); no final subtraction, no fifth word.
 __device__ __forceinline__ U128 mont_mul_lazy(const U128& a, const U128& b, const uint32_t q[4], uint32_t qinv0) {
-    uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0, e4 = 0, o1, o2, o3, o4, m;
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-        asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
-            "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
-            "madc.lo.cc.u32 %2, %5, %7, %2;\n\t"
-            "madc.hi.cc.u32 %3, %5, %7, %3;\n\t"
-            "addc.u32       %4, %4, 0;"
-            : "+r"(e0), "+r"(e1), "+r"(e2), "+r"(e3), "+r"(e4)
-            : "r"(a.w[i]), "r"(b.w[0]), "r"(b.w[2]));
-        asm("mul.lo.u32 %0, %4, %5;\n\t"
-            "mul.hi.u32 %1, %4, %5;\n\t"
-            "mul.lo.u32 %2, %4, %6;\n\t"
-            "mul.hi.u32 %3, %4, %6;"
-            : "=r"(o1), "=r"(o2), "=r"(o3), "=r"(o4)
-            : "r"(a.w[i]), "r"(b.w[1]), "r"(b.w[3]));
-        m = e0 * qinv0;
-        asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
-            "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
-            "madc.lo.cc.u32 %2, %5, %7, %2;\n\t"
-            "madc.hi.cc.u32 %3, %5, %7, %3;\n\t"
-            "addc.u32       %4, %4, 0;"
-            : "+r"(e0), "+r"(e1), "+r"(e2), "+r"(e3), "+r"(e4)
-            : "r"(m), "r"(q[0]), "r"(q[2]));
-        // O + m (q1 2^32 + q3 2^96) < 2^160: no carry out of word 4
-        asm("mad.lo.cc.u32  %0, %4, %5, %0;\n\t"
-            "madc.hi.cc.u32 %1, %4, %5, %1;\n\t"
-            "madc.lo.cc.u32 %2, %4, %6, %2;\n\t"
-            "madc.hi.u32    %3, %4, %6, %3;"
-            : "+r"(o1), "+r"(o2), "+r"(o3), "+r"(o4)
-            : "r"(m), "r"(q[1]), "r"(q[3]));
-        // (E + O) / 2^32 < 2^129 / 2^32 ... the running value stays < 2q after the shift
-        asm("add.cc.u32  %0, %4, %8;\n\t"
-            "addc.cc.u32 %1, %5, %9;\n\t"
-            "addc.cc.u32 %2, %6, %10;\n\t"
-            "addc.u32    %3, %7, %11;"
-            : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
-            : "r"(e1), "r"(e2), "r"(e3), "r"(e4), "r"(o1), "r"(o2), "r"(o3), "r"(o4));
-        e4 = 0;
-    }
-    return U128{{e0, e1, e2, e3}};
+    uint32_t t[5];
+    mont_core<false>(a, b, q, qinv0, t);
+    return U128{{t[0], t[1], t[2], t[3]}};
 }
 
-// x - 2q if x >= 2q (x < 4q < 2^128); q2 = 2q
+// x - m if x >= m else x (x < 2^128, m < 2^128): one borrow chain and a select.  With
+// m = 2q it maps [0, 4q) to [0, 2q); with m = q, [0, 2q) to [0, q).
 __device__ __forceinline__ U128 reduce_2q(const U128& x, const uint32_t q2[4]) {
     uint32_t d0, d1, d2, d3, bw;
     asm("sub.cc.u32  %0, %5, %9;\n\t"
@@ -226,8 +298,8 @@ __device__ __forceinline__ U128 reduce_2q(const U128& x, const uint32_t q2[4]) {
     return r;
 }
 
-// lazy butterfly outputs: u + t and u - t + 2q, each brought back to [0, 2q)
-__device__ __forceinline__ U128 add_lazy(const U128& u, const U128& t, const uint32_t q2[4]) {
+// u + t (no reduction; caller guarantees u + t < 2^128)
+__device__ __forceinline__ U128 add_nored(const U128& u, const U128& t) {
     U128 s;
     asm("add.cc.u32  %0, %4, %8;\n\t"
         "addc.cc.u32 %1, %5, %9;\n\t"
@@ -235,9 +307,10 @@ __device__ __forceinline__ U128 add_lazy(const U128& u, const U128& t, const uin
         "addc.u32    %3, %7, %11;"
         : "=r"(s.w[0]), "=r"(s.w[1]), "=r"(s.w[2]), "=r"(s.w[3])
         : "r"(u.w[0]), "r"(u.w[1]), "r"(u.w[2]), "r"(u.w[3]), "r"(t.w[0]), "r"(t.w[1]), "r"(t.w[2]), "r"(t.w[3]));
-    return reduce_2q(s, q2);
+    return s;
 }
-__device__ __forceinline__ U128 sub_lazy(const U128& u, const U128& t, const uint32_t q2[4]) {
+// u - t + c (no reduction; caller guarantees 0 <= u - t + c < 2^128)
+__device__ __forceinline__ U128 sub_add_nored(const U128& u, const U128& t, const uint32_t c[4]) {
     U128 s;
     asm("sub.cc.u32  %0, %4, %8;\n\t"
         "subc.cc.u32 %1, %5, %9;\n\t"
@@ -249,8 +322,8 @@ __device__ __forceinline__ U128 sub_lazy(const U128& u, const U128& t, const uin
         "addc.u32    %3, %3, %15;"
         : "=&r"(s.w[0]), "=&r"(s.w[1]), "=&r"(s.w[2]), "=&r"(s.w[3])
         : "r"(u.w[0]), "r"(u.w[1]), "r"(u.w[2]), "r"(u.w[3]), "r"(t.w[0]), "r"(t.w[1]), "r"(t.w[2]), "r"(t.w[3]),
-          "r"(q2[0]), "r"(q2[1]), "r"(q2[2]), "r"(q2[3]));
-    return reduce_2q(s, q2);
+          "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]));
+    return s;
 }
 
 // a < q check (for NTT128_FLAG_CHECK_INPUT): borrow out of a - q

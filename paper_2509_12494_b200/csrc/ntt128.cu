@@ -170,15 +170,60 @@ __device__ __forceinline__ int swz(int l) {
     return l ^ (f & 7);
 }
 
+// Arithmetic mode of a multi-pass CTA, by modulus class (uniform per CTA):
+//   MODE_FULL (q >= 2^127): canonical values in [0, q);
+//   MODE_HALF (2^126 <= q < 2^127): values in [0, 2q), add/sub modulo 2q, lazy Montgomery;
+//   MODE_LAZY (q < 2^126): values in [0, 4q), Harvey butterflies, lazy Montgomery.
+// Single-pass CTAs (one CTA may hold several moduli) and the last pass's store keep the
+// interface canonical.
+enum { MODE_FULL = 0, MODE_HALF = 1, MODE_LAZY = 2 };
+__device__ __forceinline__ int mode_of(const uint32_t q[4]) {
+    return (q[3] >> 30) == 0 ? MODE_LAZY : ((q[3] >> 31) == 0 ? MODE_HALF : MODE_FULL);
+}
+
+// One radix-2 CT butterfly (u, v) -> (u + w v, u - w v) in the given mode.  In the last
+// stage of a scaled inverse u is multiplied by nf = N^-1 (Montgomery form) too.
+template <int MODE, bool SCALE_U>
+__device__ __forceinline__ void bfly(U128& u, U128& v, const U128& w, const uint32_t q[4], const uint32_t q2[4],
+                                     uint32_t qinv0, const U128& nf) {
+    if (MODE == MODE_FULL) {
+        const U128 us = SCALE_U ? mont_mul(u, nf, q, qinv0) : u;
+        const U128 t = mont_mul(v, w, q, qinv0);
+        u = add_mod(us, t, q);
+        v = sub_mod(us, t, q);
+    } else if (MODE == MODE_HALF) {   // u, v in [0, 2q): t in [0, 2q); results mod 2q
+        const U128 us = SCALE_U ? mont_mul_lazy(u, nf, q, qinv0) : u;
+        const U128 t = mont_mul_lazy(v, w, q, qinv0);
+        u = add_mod(us, t, q2);
+        v = sub_mod(us, t, q2);
+    } else {                          // Harvey: u, v in [0, 4q); u' = u mod 2q; u' + t, u' - t + 2q
+        const U128 us = SCALE_U ? mont_mul_lazy(u, nf, q, qinv0) : reduce_2q(u, q2);
+        const U128 t = mont_mul_lazy(v, w, q, qinv0);
+        u = add_nored(us, t);
+        v = sub_add_nored(us, t, q2);
+    }
+}
+// Stage with twiddle 1 (first stage of a first pass): inputs canonical (< q).
+template <int MODE>
+__device__ __forceinline__ void bfly1(U128& u, U128& v, const uint32_t q[4]) {
+    if (MODE == MODE_FULL) {
+        const U128 a = add_mod(u, v, q);
+        v = sub_mod(u, v, q);
+        u = a;
+    } else {                          // u + v < 2q, u - v + q in (0, 2q): no reduction needed
+        const U128 a = add_nored(u, v);
+        v = sub_add_nored(u, v, q);
+        u = a;
+    }
+}
+
 // Register rounds of one pass on a CTA's tile in shared memory: RB stages on E elements
 // per thread, 8-lane conflict-free addressing (swz + padded group strides).
-template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, bool LAZY, bool WARPSYNC>
+template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC>
 __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
                                             const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
-    // LAZY (q < 2^126): operands and results in [0, 2q), Harvey butterflies, no final
-    // Montgomery subtraction; the last pass's store brings results back to [0, q).
-    uint32_t q2[4];
-    if (LAZY) {
+    uint32_t q2[4] = {0, 0, 0, 0};
+    if (MODE != MODE_FULL) {
         q2[0] = q[0] << 1;
         q2[1] = (q[1] << 1) | (q[0] >> 31);
         q2[2] = (q[2] << 1) | (q[1] >> 31);
@@ -209,9 +254,7 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
                 for (int kk = 0; kk < E / 2; kk++) {
                     const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
                     const int k1 = k0 | (1 << bit);
-                    const U128 u = x[k0], v = x[k1];
-                    x[k0] = LAZY ? add_lazy(u, v, q2) : add_mod(u, v, q);
-                    x[k1] = LAZY ? sub_lazy(u, v, q2) : sub_mod(u, v, q);
+                    bfly1<MODE>(x[k0], x[k1], q);
                 }
             } else if (last) {
 #pragma unroll
@@ -220,10 +263,7 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
                     const int k1 = k0 | (1 << bit);
                     const int l0 = thi | (k0 << w) | tlo;
                     const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
-                    const U128 us = LAZY ? mont_mul_lazy(x[k0], nf, q, qinv0) : mont_mul(x[k0], nf, q, qinv0);
-                    const U128 v = LAZY ? mont_mul_lazy(x[k1], wv, q, qinv0) : mont_mul(x[k1], wv, q, qinv0);
-                    x[k0] = LAZY ? add_lazy(us, v, q2) : add_mod(us, v, q);
-                    x[k1] = LAZY ? sub_lazy(us, v, q2) : sub_mod(us, v, q);
+                    bfly<MODE, true>(x[k0], x[k1], wv, q, q2, qinv0, nf);
                 }
             } else {
 #pragma unroll
@@ -232,10 +272,7 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
                     const int k1 = k0 | (1 << bit);
                     const int l0 = thi | (k0 << w) | tlo;
                     const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
-                    const U128 u = x[k0];
-                    const U128 v = LAZY ? mont_mul_lazy(x[k1], wv, q, qinv0) : mont_mul(x[k1], wv, q, qinv0);
-                    x[k0] = LAZY ? add_lazy(u, v, q2) : add_mod(u, v, q);
-                    x[k1] = LAZY ? sub_lazy(u, v, q2) : sub_mod(u, v, q);
+                    bfly<MODE, false>(x[k0], x[k1], wv, q, q2, qinv0, nf);
                 }
             }
         }
@@ -373,10 +410,13 @@ k_ntt_pass(const PassArgs a) {
         uint4* gsm = sm + c * GS;
         const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
-if (!SINGLE && (q[3] >> 30) == 0)   // uniform per CTA: all C groups share the polynomial
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, true, WARPMAP>(gsm, tws, t, lo, n, q, qinv0, nf);
+        const int mode = SINGLE ? MODE_FULL : mode_of(q);   // uniform per CTA: its groups share the polynomial
+        if (mode == MODE_LAZY)
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP>(gsm, tws, t, lo, n, q, qinv0, nf);
+        else if (mode == MODE_HALF)
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_HALF, WARPMAP>(gsm, tws, t, lo, n, q, qinv0, nf);
         else
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, false, WARPMAP>(gsm, tws, t, lo, n, q, qinv0, nf);
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_FULL, WARPMAP>(gsm, tws, t, lo, n, q, qinv0, nf);
         if (WARPMAP) __syncthreads();   // the store phase reads every group
     }
 
@@ -412,10 +452,17 @@ if (!SINGLE && (q[3] >> 30) == 0)   // uniform per CTA: all C groups share the p
 #pragma unroll
             for (int i = 0; i < PER; i++) outv[i] = smc[swz<B>(lbase + (i << LT))];
             if (!SINGLE && lo + B == n && !a.fout) {
-                // lazy polynomials (q < 2^126) leave the last pass in [0, 2q): canonicalize
+                // lazy classes leave the last pass in [0, 4q) / [0, 2q): canonicalize
                 const ModC& M = a.mods[m_me];
                 const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
-                if ((q[3] >> 30) == 0) {
+                const int mode = mode_of(q);
+                if (mode == MODE_LAZY) {
+                    const uint32_t q2[4] = {q[0] << 1, (q[1] << 1) | (q[0] >> 31), (q[2] << 1) | (q[1] >> 31),
+                                            (q[3] << 1) | (q[2] >> 31)};
+#pragma unroll
+                    for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q2));
+                }
+                if (mode != MODE_FULL) {
 #pragma unroll
                     for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q));
                 }
@@ -699,13 +746,15 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
             }
         }
     }
-    // polynomial order for multi-pass launches: moduli < 2^126 (lazy path) first
+    // polynomial order for multi-pass launches, grouped by arithmetic mode (q < 2^126,
+    // q < 2^127, the rest) so one code path at a time is hot in the instruction cache
     if (st == NTT128_OK && n_moduli > 1 && p->bits.size() > 1) {
         std::vector<uint32_t> order;
-        for (uint32_t m = 0; m < n_moduli; m++)
-            if ((qs[m] >> 126) == 0) order.push_back(m);
-        for (uint32_t m = 0; m < n_moduli; m++)
-            if ((qs[m] >> 126) != 0) order.push_back(m);
+        for (int cls = 0; cls < 3; cls++)
+            for (uint32_t m = 0; m < n_moduli; m++) {
+                const int c = (qs[m] >> 126) == 0 ? 0 : ((qs[m] >> 127) == 0 ? 1 : 2);
+                if (c == cls) order.push_back(m);
+            }
         if (cudaMalloc(&p->d_order, order.size() * sizeof(uint32_t)) != cudaSuccess) st = NTT128_ERR_OOM;
         else if (cudaMemcpy(p->d_order, order.data(), order.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess)
             st = NTT128_ERR_CUDA;

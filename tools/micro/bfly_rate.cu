@@ -76,13 +76,20 @@ __global__ void __launch_bounds__(256) k_bfly(uint4* io, const uint4* tw, const 
                 const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
                 const int k1 = k0 | (1 << bit);
                 const U128 u = x[k0];
-                if (V == 3) {
-                    const uint32_t q2[4] = {M.r2[0], M.r2[1], M.r2[2], M.r2[3]};   // r2 slot holds 2q here
+                const uint32_t q2[4] = {M.r2[0], M.r2[1], M.r2[2], M.r2[3]};   // r2 slot holds 2q here
+                if (V == 3) {          // Harvey (q < 2^126), values in [0, 4q)
+                    const U128 us = reduce_2q(u, q2);
                     const U128 v = mont_mul_lazy(x[k1], w[(kk + bit) % (E / 2)], q, M.qinv0);
-                    x[k0] = add_lazy(u, v, q2); x[k1] = sub_lazy(u, v, q2);
+                    x[k0] = add_nored(us, v); x[k1] = sub_add_nored(us, v, q2);
                     continue;
                 }
-                const U128 v = mont_mul(x[k1], w[(kk + bit) % (E / 2)], q, M.qinv0);
+                if (V == 5) {          // half-lazy (q < 2^127), values in [0, 2q)
+                    const U128 v = mont_mul_lazy(x[k1], w[(kk + bit) % (E / 2)], q, M.qinv0);
+                    x[k0] = add_mod(u, v, q2); x[k1] = sub_mod(u, v, q2);
+                    continue;
+                }
+                const U128 v = V == 4 ? mont_mul_v1(x[k1], w[(kk + bit) % (E / 2)], q, M.qinv0)
+                                      : mont_mul(x[k1], w[(kk + bit) % (E / 2)], q, M.qinv0);
                 if (V != 1) { x[k0] = add_mod(u, v, q); x[k1] = sub_mod(u, v, q); }
                 else { x[k0] = add_mod_p(u, v, q); x[k1] = sub_mod_p(u, v, q); }
             }
@@ -112,8 +119,8 @@ int main() {
         const int blocks = sms * 3; size_t n = (size_t)threads * blocks * E;
         std::vector<uint4> h(n); for (size_t i = 0; i < n; i++) h[i] = make_uint4(i * 2654435761u, i, 77, 0x0fffffff);
         uint4* d; CK(cudaMalloc(&d, n * 16)); CK(cudaMemcpy(d, h.data(), n * 16, cudaMemcpyHostToDevice));
-        for (int v : {0, 3}) {
-            auto launch = [&]() { if (v == 0) k_bfly<0, E><<<blocks, threads>>>(d, dtw, dm5, iters, dbad); else k_bfly<3, E><<<blocks, threads>>>(d, dtw, dm5, iters, dbad); };
+        for (int v : {0, 3, 5}) {
+            auto launch = [&]() { if (v == 0) k_bfly<0, E><<<blocks, threads>>>(d, dtw, dm5, iters, dbad); else if (v == 3) k_bfly<3, E><<<blocks, threads>>>(d, dtw, dm5, iters, dbad); else k_bfly<5, E><<<blocks, threads>>>(d, dtw, dm5, iters, dbad); };
             launch(); CK(cudaDeviceSynchronize());
             float best = 1e30f;
             for (int r = 0; r < 3; r++) { cudaEventRecord(e0); launch(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms); }
@@ -127,10 +134,10 @@ int main() {
         size_t n = (size_t)threads * blocks * E;
         std::vector<uint4> h(n); for (size_t i = 0; i < n; i++) h[i] = make_uint4(i * 2654435761u, i, 77, 0x7fffffff);
         uint4* d; CK(cudaMalloc(&d, n * 16));
-        unsigned long long hsh[3];
-        for (int v = 0; v < 3; v++) {
+        unsigned long long hsh[5];
+        for (int v = 0; v < 5; v++) {
             CK(cudaMemcpy(d, h.data(), n * 16, cudaMemcpyHostToDevice));
-            auto launch = [&]() { if (v == 0) k_bfly<0, E><<<blocks, threads>>>(d, dtw, dm, iters, dbad); else if (v == 1) k_bfly<1, E><<<blocks, threads>>>(d, dtw, dm, iters, dbad); else k_bfly<2, E><<<blocks, threads>>>(d, dtw, dm, iters, dbad); };
+            auto launch = [&]() { if (v == 0) k_bfly<0, E><<<blocks, threads>>>(d, dtw, dm, iters, dbad); else if (v == 1) k_bfly<1, E><<<blocks, threads>>>(d, dtw, dm, iters, dbad); else if (v == 2) k_bfly<2, E><<<blocks, threads>>>(d, dtw, dm, iters, dbad); else if (v == 3) k_bfly<4, E><<<blocks, threads>>>(d, dtw, dm, iters, dbad); else k_bfly<0, E><<<blocks, threads>>>(d, dtw, dm, iters, dbad); };
             launch(); CK(cudaDeviceSynchronize());
             std::vector<uint4> res(n); CK(cudaMemcpy(res.data(), d, n * 16, cudaMemcpyDeviceToHost));
             unsigned long long hs = 0; for (size_t i = 0; i < n; i++) hs = hs * 1000003ull + res[i].x + 7ull * res[i].w; hsh[v] = hs;
@@ -139,7 +146,7 @@ int main() {
             double bf = (double)threads * blocks * iters * 3 * (E / 2);
             printf("{\"variant\":%d,\"blocks_per_sm\":%d,\"ms\":%.4f,\"bfly_per_s\":%.4e,\"bfly_per_clk_sm_at1965\":%.3f}\n", v, bpsm, best, bf / (best * 1e-3), bf / (best * 1e-3) / (sms * 1.965e9));
         }
-        printf("{\"blocks_per_sm\":%d,\"hash_equal\":%d}\n", bpsm, hsh[0] == hsh[1] && hsh[0] == hsh[2]);
+        printf("{\"blocks_per_sm\":%d,\"hash_equal\":%d}\n", bpsm, hsh[0] == hsh[1] && hsh[0] == hsh[2] && hsh[0] == hsh[3]);
         cudaFree(d);
     }
     return 0;
