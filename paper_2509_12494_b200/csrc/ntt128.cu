@@ -144,8 +144,11 @@ struct PassArgs {
 };
 
 // Shape of one pass: groups of G = 2^B elements, E = 2^RB elements per thread
-// (register rounds of RB stages), T threads per group.
-template <int B, int RBMAX = 3, int C = 8>
+// (register rounds of RB stages), T threads per group.  PADL selects the shared-memory
+// layout of a group: padded (slot(l) = l + l/8, one empty 16-byte slot after every 8
+// elements; multi-pass kernels) or XOR-swizzled (single-pass kernels, whose one-group
+// CTAs gather bit-reversed rows).
+template <int B, int RBMAX = 3, int C = 8, bool PADL = false>
 struct PassShape {
     static constexpr int G = 1 << B;
     static constexpr int RB = B >= RBMAX ? RBMAX : B;  // radix-2^RB register rounds
@@ -154,10 +157,14 @@ struct PassShape {
     // Strides between groups (data) and twiddle sets, in 16-byte slots: an 8-lane shared
     // memory phase covers min(C, 8) groups x 8/min(C, 8) adjacent rows, so the group
     // stride must be = 8/C (mod 8) for C in {2, 4} and odd for C >= 8.
-    static constexpr int PADG = (C >= 8 || C == 1) ? 1 : 8 / C;
-    static constexpr int GS = G + PADG;
+    static constexpr int CM = C < 8 ? C : 8;
+    static constexpr int GP = PADL ? G + G / 8 : G;     // slots a group's elements span
+    static constexpr int PADG = PADL ? ((8 / CM) % 8 - GP % 8 + 8) % 8 : ((C >= 8 || C == 1) ? 1 : 8 / C);
+    static constexpr int GS = GP + PADG;
     static constexpr int TS = (C >= 8 || C == 1) ? G - 1 : G + 8 / C;
     static constexpr int ROUNDS = (B + RB - 1) / RB;
+    // every register-round window w is 0 or >= 3, so slot(l0 + k 2^w) is linear in k
+    static constexpr bool LINEAR = PADL && !(B - RB == 1 || B - RB == 2);
 };
 
 // XOR swizzle of the low 3 element-index bits (16-byte slots of a 128-byte bank
@@ -169,6 +176,8 @@ __device__ __forceinline__ int swz(int l) {
     if (B >= 9) f ^= l >> (B >= 9 ? B - 3 : 0);
     return l ^ (f & 7);
 }
+template <int B, bool PADL>
+__device__ __forceinline__ int slot(int l) { return PADL ? l + (l >> 3) : swz<B>(l); }
 
 // Arithmetic mode of a multi-pass CTA, by modulus class (uniform per CTA):
 //   MODE_FULL (q >= 2^127): canonical values in [0, q);
@@ -218,8 +227,11 @@ __device__ __forceinline__ void bfly1(U128& u, U128& v, const uint32_t q[4]) {
 }
 
 // Register rounds of one pass on a CTA's tile in shared memory: RB stages on E elements
-// per thread, 8-lane conflict-free addressing (swz + padded group strides).
-template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC>
+// per thread (window [w, w + RB) of the group's index bits), 8-lane conflict-free
+// addressing.  With the padded layout the E slots of a round are s0 + k st (one base,
+// one stride per round), and a stage's distinct twiddles are loaded once: stage w + bit
+// needs 2^bit of them (index (2^sl - 1) + tlo + (j << w), j < 2^bit).
+template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL>
 __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
                                             const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
     uint32_t q2[4] = {0, 0, 0, 0};
@@ -229,7 +241,7 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
         q2[2] = (q[2] << 1) | (q[1] >> 31);
         q2[3] = (q[3] << 1) | (q[2] >> 31);
     }
-    using S = PassShape<B, RBMAX, C>;
+    using S = PassShape<B, RBMAX, C, PADL>;
     constexpr int RB = S::RB, E = S::E;
 #if NTT_UNROLL_ROUNDS
 #pragma unroll
@@ -239,10 +251,14 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
     for (int rd = 0; rd < S::ROUNDS; rd++) {
         const int slo = rd * RB;
         const int w = (slo + RB <= B) ? slo : B - RB;   // E-element window [w, w + RB)
-        const int tlo = t & ((1 << w) - 1), thi = (t >> w) << (w + RB);
+        const int tlo = t & ((1 << w) - 1);
+        const int l0 = ((t >> w) << (w + RB)) | tlo;    // element k of this thread: l0 + (k << w)
+        const int s0 = S::LINEAR ? slot<B, PADL>(l0) : 0;
+        const int st = S::LINEAR ? (w >= 3 ? (9 << (w - 3)) : (1 << w)) : 0;
         U128 x[E];
 #pragma unroll
-        for (int k = 0; k < E; k++) x[k] = u128_from(gsm[swz<B>(thi | (k << w) | tlo)]);
+        for (int k = 0; k < E; k++)
+            x[k] = u128_from(gsm[S::LINEAR ? s0 + k * st : slot<B, PADL>(l0 | (k << w))]);
 #pragma unroll
         for (int bit = 0; bit < RB; bit++) {
             const int sl = w + bit;                      // local stage
@@ -256,28 +272,24 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
                     const int k1 = k0 | (1 << bit);
                     bfly1<MODE>(x[k0], x[k1], q);
                 }
-            } else if (last) {
-#pragma unroll
-                for (int kk = 0; kk < E / 2; kk++) {
-                    const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
-                    const int k1 = k0 | (1 << bit);
-                    const int l0 = thi | (k0 << w) | tlo;
-                    const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
-                    bfly<MODE, true>(x[k0], x[k1], wv, q, q2, qinv0, nf);
-                }
             } else {
+                const uint4* tp = tws + tlo + ((1 << sl) - 1);
+                U128 tw[E / 2];                          // the first 2^bit are used
+#pragma unroll
+                for (int j = 0; j < (1 << bit); j++) tw[j] = u128_from(tp[j << w]);
 #pragma unroll
                 for (int kk = 0; kk < E / 2; kk++) {
                     const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
                     const int k1 = k0 | (1 << bit);
-                    const int l0 = thi | (k0 << w) | tlo;
-                    const U128 wv = u128_from(tws[(1 << sl) - 1 + (l0 & ((1 << sl) - 1))]);
-                    bfly<MODE, false>(x[k0], x[k1], wv, q, q2, qinv0, nf);
+                    const U128& wv = tw[kk & ((1 << bit) - 1)];
+                    if (last) bfly<MODE, true>(x[k0], x[k1], wv, q, q2, qinv0, nf);
+                    else bfly<MODE, false>(x[k0], x[k1], wv, q, q2, qinv0, nf);
                 }
             }
         }
 #pragma unroll
-        for (int k = 0; k < E; k++) gsm[swz<B>(thi | (k << w) | tlo)] = u128_to(x[k]);
+        for (int k = 0; k < E; k++)
+            gsm[S::LINEAR ? s0 + k * st : slot<B, PADL>(l0 | (k << w))] = u128_to(x[k]);
         if (WARPSYNC) __syncwarp(); else __syncthreads();
     }
 }
@@ -285,7 +297,8 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX>
 __global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (768 / (C * PassShape<B, RBMAX>::T)) > 0 ? 768 / (C * PassShape<B, RBMAX>::T) : 1)
 k_ntt_pass(const PassArgs a) {
-    using S = PassShape<B, RBMAX, C>;
+    constexpr bool PADL = !SINGLE;
+    using S = PassShape<B, RBMAX, C, PADL>;
     constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS, TS = S::TS;
     constexpr int NT = C * T;
     constexpr int NTW = (FIRST && !SINGLE) ? 1 : C;  // twiddle sets: a multi-pass first pass shares one (L = 0)
@@ -297,15 +310,22 @@ k_ntt_pass(const PassArgs a) {
     const uint64_t gmask = (1ull << gbits) - 1;
     uint64_t gg0 = (uint64_t)blockIdx.x * C;
     // multi-pass CTAs hold groups of one polynomial: visit polynomials in the plan's order
-    // (all lazy-path moduli first) so one code path at a time is hot in the I-cache
+    // (grouped by arithmetic mode) so one code path at a time is hot in the I-cache
     if (!SINGLE && a.order) gg0 = ((uint64_t)a.order[gg0 >> gbits] << gbits) | (gg0 & gmask);
     const int tid = threadIdx.x;
 
     // ---------------- load phase: twiddles and data -> shared memory, all copies in flight
     // at once (cp.async 16-byte copies, LDGSTS), then one wait.  NT is a multiple of C, so a
-    // thread keeps one group c = tid % C and visits rows t0 + i T (t0 = tid / C): every
-    // address below is a per-thread base plus a compile-time multiple of i.
-    const int c_me = tid % C, t0 = tid / C;
+    // thread keeps one group c = tid % C and visits rows t0 + i T: every address below is
+    // a per-thread base plus a compile-time multiple of i.
+    constexpr int LT = B - RB;                   // log2 T
+    // multi-pass first pass: the rows of a lane pair/quad are T/2 (T/4) apart, so the
+    // bit-reversed rows land in different banks (8-lane phase = CM groups x 8/CM rows)
+    constexpr int RT = (!PADL || !FIRST) ? 0 : (S::CM == 8 ? 0 : (S::CM == 4 ? 1 : (S::CM == 2 ? 2 : 3)));
+    static_assert(RT <= LT || LT == 0, "row rotation needs enough rows");
+    const int c_me = tid % C;
+    const int u_me = tid / C;
+    const int t0 = (RT == 0 || LT == 0) ? u_me : ((u_me >> RT) | ((u_me & ((1 << RT) - 1)) << (LT - RT)));
     const uint64_t gg_me = gg0 + c_me;
     const bool live = gg_me < a.total_groups;
     const uint64_t ggc_me = live ? gg_me : a.total_groups - 1;
@@ -314,21 +334,21 @@ k_ntt_pass(const PassArgs a) {
     {
         // Twiddles: set c holds its group's 2^B - 1 twiddles in consumption order (slot
         // (2^sl - 1) + jj for local stage sl), precomputed per pass at plan time; the sets
-        // of one CTA (consecutive L, same polynomial) are one contiguous run of the table.
-        constexpr int TW_PER = (NTW * (G - 1) + NT - 1) / NT;
+        // of one CTA (consecutive L, same polynomial) are consecutive runs of the table.
+        constexpr int TW_IT = (G - 1 + NT - 1) / NT;
         if (NTW == 1 || !(FIRST && SINGLE)) {
             const uint64_t L0 = FIRST ? 0 : ((gg0 & gmask) & ((1ull << lo) - 1));
             const uint32_t m0 = a.nq == 1 ? 0 : (uint32_t)((gg0 < a.total_groups ? gg0 : a.total_groups - 1) >> gbits);
-            const uint4* src = a.pt + m0 * a.pt_stride + L0 * (G - 1);
+            const uint4* src = a.pt + m0 * a.pt_stride + L0 * (G - 1) + tid;
+            uint4* dst = tsm + tid;
 #pragma unroll
-            for (int i = 0; i < TW_PER; i++) {
-                const int e = tid + i * NT;
-                if (e < NTW * (G - 1)) {
-                    const int c = TS == G - 1 ? 0 : e / (G - 1);
-                    cp_async16(tsm + e + c * (TS - (G - 1)), src + e);
-                }
-            }
+            for (int c = 0; c < NTW; c++)
+#pragma unroll
+                for (int i = 0; i < TW_IT; i++)
+                    if ((G - 1) % NT == 0 || i + 1 < TW_IT || tid + i * NT < G - 1)
+                        cp_async16(dst + c * TS + i * NT, src + c * (G - 1) + i * NT);
         } else {   // single pass, C polynomials per CTA, each with its own modulus
+            constexpr int TW_PER = (NTW * (G - 1) + NT - 1) / NT;
 #pragma unroll
             for (int i = 0; i < TW_PER; i++) {
                 const int e = tid + i * NT;
@@ -342,19 +362,18 @@ k_ntt_pass(const PassArgs a) {
         }
     }
     constexpr int PER = (C * G) / NT;            // == E
-    constexpr int LT = B - RB;                   // log2 T
     // element i of this thread: row r = t0 + i T
     uint64_t gbase;                              // natural index of row t0 of group c_me
-    uint64_t gstride;                            // natural-index step per i
+    uint32_t gstride;                            // natural-index step per i (< 2^26)
     int lbase;                                   // local index of row t0
     if (FIRST) {   // gather column g of the (2^B x 2^gbits) view: row r -> local brev_B(r)
         gbase = ((uint64_t)t0 << gbits) | g_me;
-        gstride = (uint64_t)T << gbits;
+        gstride = (uint32_t)T << gbits;
         lbase = (int)brev_bits((uint32_t)t0, B);
     } else {
         const uint64_t H = g_me >> lo, L = g_me & ((1ull << lo) - 1);
         gbase = (H << (lo + B)) | ((uint64_t)t0 << lo) | L;
-        gstride = (uint64_t)T << lo;
+        gstride = (uint32_t)T << lo;
         lbase = t0;
     }
     const uint4* srcp = a.src + poly_me * N + gbase;
@@ -364,23 +383,23 @@ k_ntt_pass(const PassArgs a) {
 #pragma unroll
             for (int i = 0; i < PER; i++) {
                 const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
-                cp_async16(smc + swz<B>(l), srcp + i * gstride);
+                cp_async16(smc + slot<B, PADL>(l), srcp + (size_t)i * gstride);
             }
         }
     } else if (live) {
         uint4 stage[PER];
 #pragma unroll
-        for (int i = 0; i < PER; i++) stage[i] = srcp[i * gstride];
+        for (int i = 0; i < PER; i++) stage[i] = srcp[(size_t)i * gstride];
         const ModC& M = a.mods[m_me];
         const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
 #pragma unroll
         for (int i = 0; i < PER; i++) {
             const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
-            const uint64_t idx = gbase + i * gstride;
+            const uint64_t idx = gbase + (size_t)i * gstride;
             U128 x = u128_from(stage[i]);
             if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + m_me * a.f_stride + idx)), q, M.qinv0);
             if (a.pmul) x = mont_mul(x, u128_from(__ldg(a.pmul + poly_me * N + idx)), q, M.qinv0);
-            smc[swz<B>(l)] = u128_to(x);
+            smc[slot<B, PADL>(l)] = u128_to(x);
         }
     }
     cp_async_wait_all();
@@ -412,11 +431,11 @@ k_ntt_pass(const PassArgs a) {
 
         const int mode = SINGLE ? MODE_FULL : mode_of(q);   // uniform per CTA: its groups share the polynomial
         if (mode == MODE_LAZY)
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP>(gsm, tws, t, lo, n, q, qinv0, nf);
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
         else if (mode == MODE_HALF)
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_HALF, WARPMAP>(gsm, tws, t, lo, n, q, qinv0, nf);
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_HALF, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
         else
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_FULL, WARPMAP>(gsm, tws, t, lo, n, q, qinv0, nf);
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_FULL, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
         if (WARPMAP) __syncthreads();   // the store phase reads every group
     }
 
@@ -428,7 +447,7 @@ k_ntt_pass(const PassArgs a) {
 #pragma unroll
             for (int i = 0; i < PER; i++) {
                 const int e = tid + i * NT;
-                outv[i] = sm[(e / G) * GS + swz<B>(e % G)];
+                outv[i] = sm[(e / G) * GS + slot<B, PADL>(e % G)];
             }
 #pragma unroll
             for (int i = 0; i < PER; i++) {
@@ -450,7 +469,7 @@ k_ntt_pass(const PassArgs a) {
         } else {
             // same (c_me, rows t0 + i T) assignment as the load phase
 #pragma unroll
-            for (int i = 0; i < PER; i++) outv[i] = smc[swz<B>(lbase + (i << LT))];
+            for (int i = 0; i < PER; i++) outv[i] = smc[slot<B, PADL>(lbase + (i << LT))];
             if (!SINGLE && lo + B == n && !a.fout) {
                 // lazy classes leave the last pass in [0, 4q) / [0, 2q): canonicalize
                 const ModC& M = a.mods[m_me];
@@ -475,10 +494,10 @@ k_ntt_pass(const PassArgs a) {
 #pragma unroll
                     for (int i = 0; i < PER; i++)
                         outv[i] = u128_to(mont_mul(u128_from(outv[i]),
-                                                   u128_from(__ldg(a.fout + m_me * a.f_stride + gbase + i * gstride)), q, M.qinv0));
+                                                   u128_from(__ldg(a.fout + m_me * a.f_stride + gbase + (size_t)i * gstride)), q, M.qinv0));
                 }
 #pragma unroll
-                for (int i = 0; i < PER; i++) dstp[i * gstride] = outv[i];
+                for (int i = 0; i < PER; i++) dstp[(size_t)i * gstride] = outv[i];
             }
         }
     }
@@ -495,7 +514,7 @@ struct PassCfg {
 
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE = false, int RBMAX = 3>
 static PassCfg make_cfg() {
-    using S = PassShape<B, RBMAX, C>;
+    using S = PassShape<B, RBMAX, C, !SINGLE>;
     PassCfg c;
     c.fn = k_ntt_pass<B, C, FIRST, SCALE_LAST, SINGLE, RBMAX>;
     c.B = B;
