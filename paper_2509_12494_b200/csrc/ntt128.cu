@@ -28,7 +28,9 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
 #include <new>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/ntt128.h"
@@ -141,7 +143,22 @@ struct PassArgs {
     uint64_t total_groups; // batch << (n - B)
     uint32_t n, lo, nq;
     uint32_t ninv_r;       // SCALE_LAST multiplier: 0 -> ninv_m, 1 -> ninv_rm (point-wise R^-1 compensation)
+    // Pass overlap (programmatic dependent launch, multi-pass plans): a later pass starts
+    // on a polynomial once every CTA of the previous pass on it has signalled.
+    const uint32_t* cnt_in;  // optional [batch]: previous pass's completion counters (wait for target)
+    uint32_t* cnt_out;       // optional [batch]: this pass's completion counters (+1 per CTA)
+    uint32_t target;         // cnt_in[poly] value that means "previous pass done" (wrap-safe compare)
+    uint32_t pdl_wait;       // 1: griddepcontrol.wait before reading data (first pass of a PDL launch)
 };
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Shape of one pass: groups of G = 2^B elements, E = 2^RB elements per thread
 // (register rounds of RB stages), T threads per group.  PADL selects the shared-memory
@@ -361,6 +378,21 @@ k_ntt_pass(const PassArgs a) {
             }
         }
     }
+    // ---------------- pass overlap: the twiddles (plan constants) are already in flight;
+    // data may be read only once the producers of this polynomial are done
+    if (!SINGLE) {
+        if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (a.cnt_in) {
+            if (tid == 0) {
+                const uint32_t* cp = a.cnt_in + (gg0 >> gbits);
+                while ((int32_t)(ld_acquire_gpu(cp) - a.target) < 0) __nanosleep(128);
+            }
+            __syncthreads();
+        }
+        // our predecessors are complete (or their output for this polynomial is): the next
+        // pass may be scheduled onto SMs as this grid drains
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
     constexpr int PER = (C * G) / NT;            // == E
     // element i of this thread: row r = t0 + i T
     uint64_t gbase;                              // natural index of row t0 of group c_me
@@ -501,6 +533,11 @@ k_ntt_pass(const PassArgs a) {
             }
         }
     }
+    if (!SINGLE && a.cnt_out) {
+        // all of this CTA's stores happen-before the release (barrier + cumulative release)
+        __syncthreads();
+        if (tid == 0) red_release_gpu_add(a.cnt_out + (gg0 >> gbits), 1u);
+    }
 }
 
 // ----------------------------------------------------------------------------- launch table
@@ -579,6 +616,16 @@ struct ntt128_plan_s {
     std::vector<uint4*> d_pt_fwd, d_pt_inv, d_pt_inv_r;  // per pass, [nq][pt_stride]
     uint32_t* d_order = nullptr;                         // [batch] CTA-slot -> polynomial (nq == batch)
     std::vector<uint64_t> pt_stride;
+    // Pass-overlap completion counters, one set per stream (keyed by cudaStreamGetId):
+    // counters only grow; transform number g on a stream waits for g x (CTAs per
+    // polynomial) so in-stream order makes them exact without a reset, and different
+    // streams never share a set.
+    struct StreamCtr {
+        uint32_t* d = nullptr;   // [npass - 1][batch]
+        uint64_t gen = 0;
+    };
+    std::mutex mu;
+    std::unordered_map<unsigned long long, StreamCtr> ctrs;
 };
 
 static void plan_free(ntt128_plan_s* p) {
@@ -596,6 +643,7 @@ static void plan_free(ntt128_plan_s* p) {
     cudaFree(p->d_f_untwist_r);
     cudaFree(p->d_err);
     cudaFree(p->d_order);
+    for (auto& kv : p->ctrs) cudaFree(kv.second.d);
     for (size_t i = 0; i < p->d_pt_fwd.size(); i++) {
         if (p->d_pt_inv_r[i] != p->d_pt_inv[i]) cudaFree(p->d_pt_inv_r[i]);
         cudaFree(p->d_pt_fwd[i]);
@@ -844,12 +892,39 @@ struct RunOpts {
 
 static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaStream_t stream);
 
-static ntt128_status run_transform(const ntt128_plan_s* p, const uint4* src, uint4* dst, cudaStream_t stream,
+static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* dst, cudaStream_t stream,
                                    const RunOpts& o) {
     const int n = (int)p->log2n;
     const size_t npass = p->bits.size();
     const bool scale_last = p->kind == 0 && o.inverse;
+    // Multi-pass transforms overlap consecutive passes: every pass is a
+    // programmatic dependent launch; pass i+1 CTAs wait per polynomial on pass i's
+    // completion counters instead of on the whole grid.  Not under stream capture
+    // (a captured launch would replay stale counter targets).
+    bool overlap = npass > 1 && getenv("NTT128_NO_PDL") == nullptr;
+    if (overlap) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) return NTT128_ERR_CUDA;
+        if (cs != cudaStreamCaptureStatusNone) overlap = false;
+    }
+    uint32_t* cnt = nullptr;
+    uint64_t gen = 0;
+    std::unique_lock<std::mutex> lk(p->mu, std::defer_lock);
+    if (overlap) {
+        unsigned long long sid = 0;
+        if (cudaStreamGetId(stream, &sid) != cudaSuccess) return NTT128_ERR_CUDA;
+        lk.lock();   // held until every pass is enqueued: generations follow stream order
+        ntt128_plan_s::StreamCtr& c = p->ctrs[sid];
+        if (!c.d) {
+            const size_t bytes = (npass - 1) * (size_t)p->batch * sizeof(uint32_t);
+            if (cudaMalloc(&c.d, bytes) != cudaSuccess) return NTT128_ERR_OOM;
+            if (cudaMemsetAsync(c.d, 0, bytes, stream) != cudaSuccess) return NTT128_ERR_CUDA;
+        }
+        gen = ++c.gen;
+        cnt = c.d;
+    }
     int lo = 0;
+    uint32_t prev_ctas_per_poly = 0;
     for (size_t i = 0; i < npass; i++) {
         const int B = p->bits[i];
         PassCfg c = pass_cfg(npass, i, B, scale_last);
@@ -873,11 +948,31 @@ static ntt128_status run_transform(const ntt128_plan_s* p, const uint4* src, uin
             if (!o.inverse && first) a.fin = p->d_f_twist;
             if (o.inverse && last) a.fout = o.polymul ? p->d_f_untwist_r : p->d_f_untwist;
         }
+        const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (uint64_t)c.C);
+        if (overlap) {
+            a.pdl_wait = first ? 1u : 0u;
+            if (!first) {
+                a.cnt_in = cnt + (i - 1) * (size_t)p->batch;
+                a.target = (uint32_t)(gen * (uint64_t)prev_ctas_per_poly);
+            }
+            if (!last) a.cnt_out = cnt + i * (size_t)p->batch;
+        }
         const uint64_t ctas = (a.total_groups + c.C - 1) / c.C;
-        c.fn<<<(unsigned)ctas, c.threads, c.smem, stream>>>(a);
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof(cfg));
+        cfg.gridDim = dim3((unsigned)ctas);
+        cfg.blockDim = dim3((unsigned)c.threads);
+        cfg.dynamicSmemBytes = c.smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = overlap ? 1 : 0;
+        if (cudaLaunchKernelEx(&cfg, c.fn, a) != cudaSuccess) return NTT128_ERR_CUDA;
         ntt128_count_launch(1);
-        if (cudaGetLastError() != cudaSuccess) return NTT128_ERR_CUDA;
         lo += B;
+        prev_ctas_per_poly = ctas_per_poly;
     }
     return NTT128_OK;
 }
