@@ -43,6 +43,12 @@
 #ifndef NTT_C8
 #define NTT_C8 4              // groups per CTA of the 8-stage multi-pass kernel (8 measured 3% slower)
 #endif
+#ifndef NTT_OCC_THREADS
+#define NTT_OCC_THREADS 768   // resident threads per SM the pass kernels are register-budgeted for
+#endif
+#ifndef NTT_LDG_DATA
+#define NTT_LDG_DATA 0        // 1: data tiles via LDG + STS instead of cp.async (experiment)
+#endif
 #ifndef NTT_RB8
 #define NTT_RB8 3   // register-round radix (log2) of the 8-stage multi-pass kernel (4 measured slower)
 #endif
@@ -178,10 +184,12 @@ struct PassShape {
     static constexpr int GP = PADL ? G + G / 8 : G;     // slots a group's elements span
     static constexpr int PADG = PADL ? ((8 / CM) % 8 - GP % 8 + 8) % 8 : ((C >= 8 || C == 1) ? 1 : 8 / C);
     static constexpr int GS = GP + PADG;
-    static constexpr int TS = (C >= 8 || C == 1) ? G - 1 : G + 8 / C;
+    // twiddle-set stride: a warp-owned group (T <= 32) reads only its own set, so the sets
+    // are 128-byte aligned (full-speed cp.async); otherwise staggered across banks
+    static constexpr int TS = (PADL && T <= 32 && 32 % T == 0 && G >= 8) ? G : ((C >= 8 || C == 1) ? G - 1 : G + 8 / C);
     static constexpr int ROUNDS = (B + RB - 1) / RB;
     // every register-round window w is 0 or >= 3, so slot(l0 + k 2^w) is linear in k
-    static constexpr bool LINEAR = PADL && !(B - RB == 1 || B - RB == 2);
+    static constexpr bool LINEAR = PADL && (RB >= 3 || B == RB) && !(B - RB == 1 || B - RB == 2);
 };
 
 // XOR swizzle of the low 3 element-index bits (16-byte slots of a 128-byte bank
@@ -312,7 +320,7 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
 }
 
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX>
-__global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (768 / (C * PassShape<B, RBMAX>::T)) > 0 ? 768 / (C * PassShape<B, RBMAX>::T) : 1)
+__global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (NTT_OCC_THREADS / (C * PassShape<B, RBMAX>::T)) > 0 ? NTT_OCC_THREADS / (C * PassShape<B, RBMAX>::T) : 1)
 k_ntt_pass(const PassArgs a) {
     constexpr bool PADL = !SINGLE;
     using S = PassShape<B, RBMAX, C, PADL>;
@@ -412,11 +420,24 @@ k_ntt_pass(const PassArgs a) {
     uint4* smc = sm + c_me * GS;
     if (!a.fin && !a.pmul) {
         if (live) {
+#if NTT_LDG_DATA
+            // registers, then conflict-free STS: cp.async into the padded layout (lanes not
+            // writing consecutive 16-byte slots) costs one L1 wavefront per lane
+            uint4 v[PER];
+#pragma unroll
+            for (int i = 0; i < PER; i++) v[i] = __ldcg(srcp + (size_t)i * gstride);
+#pragma unroll
+            for (int i = 0; i < PER; i++) {
+                const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
+                smc[slot<B, PADL>(l)] = v[i];
+            }
+#else
 #pragma unroll
             for (int i = 0; i < PER; i++) {
                 const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
                 cp_async16(smc + slot<B, PADL>(l), srcp + (size_t)i * gstride);
             }
+#endif
         }
     } else if (live) {
         uint4 stage[PER];
