@@ -93,9 +93,25 @@ ntt128_status ntt128_inverse(const ntt128_plan_t plan, const uint64_t *d_in, uin
 /* Polynomial product through the transform: d_c = a * b mod (X^N + 1) for negacyclic
  * plans, mod (X^N - 1) for cyclic plans (NTT, point-wise product,
  * inverse NTT).  d_a, d_b, d_c: [batch][N][2]; d_c may alias d_a or d_b.
- * Uses 2 x batch x N x 16 bytes of stream-ordered scratch. */
+ * Uses 2 x batch x N x 16 bytes of scratch per stream, allocated by the plan on the
+ * first call on that stream and kept until ntt128_plan_destroy (an in-place multi-pass
+ * forward/inverse uses the first half). */
 ntt128_status ntt128_polymul(const ntt128_plan_t plan, const uint64_t *d_a, const uint64_t *d_b, uint64_t *d_c,
                              ntt128_stream_t stream);
+
+/* Negacyclic transforms with the spectrum in bit-reversed order (SURVEY.md §8(f) f1,
+ * DESIGN.md §6): forward_bitrev writes Y[i] = y_{brev_n(i)} = a(psi^{2 brev_n(i) + 1}), the
+ * natural-order negacyclic spectrum y (ntt128_forward) permuted by n-bit bit reversal;
+ * inverse_bitrev(forward_bitrev(a)) == a.  Computed without any permutation or twist
+ * multiply: Cooley-Tukey stages from the top index bit down with psi-merged twiddles
+ * psi^{brev_n(2^(n-1-b) + i)}, Gentleman-Sande stages back (the negacyclic NTT of
+ * PAPER.md:266-277 in the order point-wise products do not care about).  In place
+ * (d_out == d_in) is allowed.  Negacyclic plans with log2n >= 10 only; otherwise
+ * NTT128_ERR_UNSUPPORTED.  ntt128_polymul uses this path when it is available. */
+ntt128_status ntt128_forward_bitrev(const ntt128_plan_t plan, const uint64_t *d_in, uint64_t *d_out,
+                                    ntt128_stream_t stream);
+ntt128_status ntt128_inverse_bitrev(const ntt128_plan_t plan, const uint64_t *d_in, uint64_t *d_out,
+                                    ntt128_stream_t stream);
 
 /* Plan properties (host-side queries). */
 ntt128_status ntt128_plan_info(const ntt128_plan_t plan, uint32_t *log2n, uint32_t *batch, uint32_t *n_moduli,

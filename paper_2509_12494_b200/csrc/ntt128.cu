@@ -135,6 +135,42 @@ __global__ void k_gather_pass_tw(uint4* out, uint64_t out_stride, const uint4* T
     }
 }
 
+// Permutation-free negacyclic pass tables: out[m][H][k], k < 2^B - 1, local stage
+// sl = B - 1 - floor(log2(k + 1)), block i = H 2^(B-1-sl) + (k - (2^(B-1-sl) - 1)),
+// global stage b = lo + sl: psi^e (forward) or psi^-e (inverse), e = brev_n(2^(n-1-b) + i),
+// from psi_pow[m][j] = psi^j R mod q (j < N; psi^-e = -psi^(N-e) since psi^N = -1); the
+// inverse's b = n - 1 entries are multiplied by `scale` (Montgomery form) when given.
+__global__ void k_gather_nc_tw(uint4* out, uint64_t out_stride, const uint4* psi_pow, uint32_t n, uint32_t lo,
+                               uint32_t b, int inv, const uint4* scale, const ModC* mods) {
+    const int m = blockIdx.y;
+    const ModC& M = mods[m];
+    const uint32_t K = (1u << b) - 1;
+    const uint64_t count = ((uint64_t)1 << (n - lo - b)) * K;
+    const uint64_t N = 1ull << n;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t H = e / K;
+        const uint32_t k = (uint32_t)(e - H * K);
+        const int lg = 31 - __clz(k + 1);            // = B - 1 - sl
+        const uint32_t sl = b - 1 - lg;
+        const uint64_t i = (H << lg) + (k + 1 - (1u << lg));
+        const uint32_t gb = lo + sl;
+        const uint64_t idx = ((uint64_t)1 << (n - 1 - gb)) + i;   // < N
+        const uint64_t ex = __brevll(idx) >> (64 - n);
+        U128 v;
+        if (!inv) {
+            v = u128_from(psi_pow[m * N + ex]);
+        } else if (ex == 0) {
+            v = U128{{M.one_m[0], M.one_m[1], M.one_m[2], M.one_m[3]}};
+        } else {
+            const U128 x = u128_from(psi_pow[m * N + (N - ex)]);
+            const uint32_t z[4] = {0, 0, 0, 0};
+            v = sub_mod(U128{{z[0], z[1], z[2], z[3]}}, x, M.q);
+        }
+        if (inv && scale && gb == n - 1) v = mont_mul(v, u128_from(scale[m]), M.q, M.qinv0);
+        out[m * out_stride + e] = u128_to(v);
+    }
+}
+
 // ----------------------------------------------------------------------------- pass kernel
 struct PassArgs {
     const uint4* src;      // [batch][N]
@@ -561,6 +597,218 @@ k_ntt_pass(const PassArgs a) {
     }
 }
 
+// ----------------------------------------------------------------------------- permutation-free negacyclic passes
+// SURVEY §8(f) f1 (DESIGN.md §6 "Bit-reversed negacyclic path").  Forward: Cooley-Tukey
+// butterflies with psi-merged twiddles, natural-order input, stages from the top index
+// bit down, output in bit-reversed order: Y[i] = a(psi^(2 brev(i) + 1)) -- no twist
+// multiply and no permutation.  Inverse: Gentleman-Sande butterflies (u + v, (u - v) w)
+// from bit-reversed input, stages from bit 0 up, psi^-1 twiddles, N^-1 folded into the
+// last stage.  Stage on global bit b pairs j and j + 2^b (bit b of j clear) with twiddle
+// psi^(+-brev_n(2^(n-1-b) + (j >> (b+1)))).  A pass covers bits [lo, lo + B) of the
+// group (H, L): elements H 2^(lo+B) + r 2^lo + L; its twiddles depend on H and on r's
+// bits above the stage, so a table holds per H the 2^B - 1 values in [local stage][block]
+// order (offset 2^(B-1-sl) - 1 for local stage sl).
+
+// GS butterfly (u, v) -> (u + v, (u - v) w) [* nf on u in the last stage], per mode:
+// FULL canonical; HALF values in [0, 2q) (add/sub mod 2q); LAZY values in [0, 2q)
+// (u + v reduced by 2q, u - v + 2q fed to the lazy product, which accepts < 4q).
+template <int MODE, bool SCALE_U>
+__device__ __forceinline__ void gs_bfly(U128& u, U128& v, const U128& w, const uint32_t q[4], const uint32_t q2[4],
+                                        uint32_t qinv0, const U128& nf) {
+    if (MODE == MODE_FULL) {
+        const U128 s = add_mod(u, v, q);
+        const U128 d = sub_mod(u, v, q);
+        u = SCALE_U ? mont_mul(s, nf, q, qinv0) : s;
+        v = mont_mul(d, w, q, qinv0);
+    } else if (MODE == MODE_HALF) {
+        const U128 s = add_mod(u, v, q2);
+        const U128 d = sub_mod(u, v, q2);
+        u = SCALE_U ? mont_mul_lazy(s, nf, q, qinv0) : s;
+        v = mont_mul_lazy(d, w, q, qinv0);
+    } else {
+        const U128 s = add_nored(u, v);                 // < 4q
+        const U128 d = sub_add_nored(u, v, q2);         // in (0, 4q)
+        u = SCALE_U ? mont_mul_lazy(s, nf, q, qinv0) : reduce_2q(s, q2);
+        v = mont_mul_lazy(d, w, q, qinv0);
+    }
+}
+
+// Register rounds of a permutation-free pass: the windows of pass_rounds, visited top-down
+// (forward, each window's stages from its top bit) or bottom-up (inverse).
+template <int B, int C, bool INV, bool SCALE_LAST, int RBMAX, int MODE>
+__device__ __forceinline__ void nc_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
+                                          const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
+    uint32_t q2[4] = {0, 0, 0, 0};
+    if (MODE != MODE_FULL) {
+        q2[0] = q[0] << 1;
+        q2[1] = (q[1] << 1) | (q[0] >> 31);
+        q2[2] = (q[2] << 1) | (q[1] >> 31);
+        q2[3] = (q[3] << 1) | (q[2] >> 31);
+    }
+    using S = PassShape<B, RBMAX, C, true>;
+    constexpr int RB = S::RB, E = S::E, R = S::ROUNDS;
+#pragma unroll 1
+    for (int it = 0; it < R; it++) {
+        const int rd = INV ? it : R - 1 - it;
+        const int slo = rd * RB;
+        const int w = (slo + RB <= B) ? slo : B - RB;   // window [w, w + RB); its own stages are [slo, ..)
+        const int tlo = t & ((1 << w) - 1);
+        const int thi = (t >> w) << (w + RB);
+        const int l0 = thi | tlo;
+        const int s0 = S::LINEAR ? slot<B, true>(l0) : 0;
+        const int st = S::LINEAR ? (w >= 3 ? (9 << (w - 3)) : (1 << w)) : 0;
+        // window rd owns stages [slo, min(slo + RB, B)) (the last window overlaps the one
+        // below it); the forward visits windows and their stages top-down
+        U128 x[E];
+#pragma unroll
+        for (int k = 0; k < E; k++) x[k] = u128_from(gsm[S::LINEAR ? s0 + k * st : slot<B, true>(l0 | (k << w))]);
+#pragma unroll
+        for (int bb = 0; bb < RB; bb++) {
+            const int bit = INV ? bb : RB - 1 - bb;
+            const int sl = w + bit;
+            if (sl < slo) continue;
+            // twiddle (local stage sl, block r >> (sl + 1)): offset(sl) + (thi >> (w+RB) << (RB-1-bit)) + (k0 >> (bit+1))
+            const uint4* tp = tws + ((1 << (B - 1 - sl)) - 1) + ((thi >> (w + RB)) << (RB - 1 - bit));
+            U128 tw[E / 2];
+#pragma unroll
+            for (int j = 0; j < (E / 2 >> bit); j++) tw[j] = u128_from(tp[j]);
+            const bool last = INV && SCALE_LAST && lo + sl == n - 1;
+#pragma unroll
+            for (int kk = 0; kk < E / 2; kk++) {
+                const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                const int k1 = k0 | (1 << bit);
+                const U128& wv = tw[k0 >> (bit + 1)];
+                if (!INV) bfly<MODE, false>(x[k0], x[k1], wv, q, q2, qinv0, nf);
+                else if (last) gs_bfly<MODE, true>(x[k0], x[k1], wv, q, q2, qinv0, nf);
+                else gs_bfly<MODE, false>(x[k0], x[k1], wv, q, q2, qinv0, nf);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < E; k++) gsm[S::LINEAR ? s0 + k * st : slot<B, true>(l0 | (k << w))] = u128_to(x[k]);
+        __syncwarp();
+    }
+}
+
+template <int B, int C, bool INV, bool SCALE_LAST, int RBMAX>
+__global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (NTT_OCC_THREADS / (C * PassShape<B, RBMAX>::T)) > 0 ? NTT_OCC_THREADS / (C * PassShape<B, RBMAX>::T) : 1)
+k_nc_pass(const PassArgs a) {
+    using S = PassShape<B, RBMAX, C, true>;
+    constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS, TS = S::TS;
+    constexpr int NT = C * T;
+    static_assert(T <= 32 && 32 % T == 0, "permutation-free passes use warp-owned groups");
+    extern __shared__ uint4 sm[];
+    uint4* tsm = sm + C * GS;                        // [C][TS] twiddle sets (1 used when lo > 0)
+
+    const uint32_t n = a.n, lo = a.lo, gbits = n - B;
+    const uint64_t N = 1ull << n;
+    const uint64_t gmask = (1ull << gbits) - 1;
+    uint64_t gg0 = (uint64_t)blockIdx.x * C;
+    if (a.order) gg0 = ((uint64_t)a.order[gg0 >> gbits] << gbits) | (gg0 & gmask);
+    const int tid = threadIdx.x;
+    constexpr int LT = B - RB;
+    const int c_me = tid % C, t0 = tid / C;
+    const uint64_t poly = gg0 >> gbits;
+    const uint64_t g_me = (gg0 + c_me) & gmask;
+    const uint32_t m_me = a.nq == 1 ? 0 : (uint32_t)poly;
+    // twiddle sets: indexed by H = g >> lo; the C groups share one set unless lo == 0
+    const bool shared_set = lo > 0;
+    {
+        constexpr int TW_IT = (G - 1 + NT - 1) / NT;
+        const uint64_t H0 = (gg0 & gmask) >> lo;
+        const uint4* src = a.pt + m_me * a.pt_stride + H0 * (G - 1) + tid;
+        uint4* dst = tsm + tid;
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            if (c > 0 && shared_set) break;
+#pragma unroll
+            for (int i = 0; i < TW_IT; i++)
+                if ((G - 1) % NT == 0 || i + 1 < TW_IT || tid + i * NT < G - 1)
+                    cp_async16(dst + c * TS + i * NT, src + c * (G - 1) + i * NT);
+        }
+    }
+    if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.cnt_in) {
+        if (tid == 0) {
+            const uint32_t* cp = a.cnt_in + poly;
+            while ((int32_t)(ld_acquire_gpu(cp) - a.target) < 0) __nanosleep(128);
+        }
+        __syncthreads();
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    constexpr int PER = (C * G) / NT;
+    const uint64_t H = g_me >> lo, L = g_me & ((1ull << lo) - 1);
+    const uint64_t gbase = (H << (lo + B)) | ((uint64_t)t0 << lo) | L;
+    const uint32_t gstride = (uint32_t)T << lo;
+    const int lbase = t0;
+    const uint4* srcp = a.src + poly * N + gbase;
+    uint4* smc = sm + c_me * GS;
+    if (!a.pmul) {
+#pragma unroll
+        for (int i = 0; i < PER; i++) cp_async16(smc + slot<B, true>(lbase + (i << LT)), srcp + (size_t)i * gstride);
+    } else {   // fused point-wise Montgomery product of two bit-reversed spectra
+        uint4 va[PER], vb[PER];
+        const uint4* pm = a.pmul + poly * N + gbase;
+#pragma unroll
+        for (int i = 0; i < PER; i++) { va[i] = __ldcg(srcp + (size_t)i * gstride); vb[i] = __ldcg(pm + (size_t)i * gstride); }
+        const ModC& M = a.mods[m_me];
+        const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+#pragma unroll
+        for (int i = 0; i < PER; i++)
+            smc[slot<B, true>(lbase + (i << LT))] = u128_to(mont_mul(u128_from(va[i]), u128_from(vb[i]), q, M.qinv0));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    {
+        const int c = tid / T, t = tid % T;
+        uint32_t q[4], qinv0;
+        U128 nf;
+        {
+            const ModC& M = a.mods[m_me];
+            q[0] = M.q[0]; q[1] = M.q[1]; q[2] = M.q[2]; q[3] = M.q[3];
+            qinv0 = M.qinv0;
+            const uint32_t* src = a.ninv_r ? M.ninv_rm : M.ninv_m;
+            nf = U128{{src[0], src[1], src[2], src[3]}};
+        }
+        uint4* gsm = sm + c * GS;
+        const uint4* tws = tsm + (shared_set ? 0 : c) * TS;
+        const int mode = mode_of(q);
+        if (mode == MODE_LAZY) nc_rounds<B, C, INV, SCALE_LAST, RBMAX, MODE_LAZY>(gsm, tws, t, lo, n, q, qinv0, nf);
+        else if (mode == MODE_HALF) nc_rounds<B, C, INV, SCALE_LAST, RBMAX, MODE_HALF>(gsm, tws, t, lo, n, q, qinv0, nf);
+        else nc_rounds<B, C, INV, SCALE_LAST, RBMAX, MODE_FULL>(gsm, tws, t, lo, n, q, qinv0, nf);
+        __syncthreads();
+    }
+    {
+        uint4 outv[PER];
+#pragma unroll
+        for (int i = 0; i < PER; i++) outv[i] = smc[slot<B, true>(lbase + (i << LT))];
+        // the transform's last pass returns canonical values (lazy classes are in [0, 4q) / [0, 2q))
+        const bool last_pass = INV ? (lo + B == n) : (lo == 0);
+        if (last_pass) {
+            const ModC& M = a.mods[m_me];
+            const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+            const int mode = mode_of(q);
+            if (mode == MODE_LAZY && !INV) {
+                const uint32_t q2[4] = {q[0] << 1, (q[1] << 1) | (q[0] >> 31), (q[2] << 1) | (q[1] >> 31),
+                                        (q[3] << 1) | (q[2] >> 31)};
+#pragma unroll
+                for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q2));
+            }
+            if (mode != MODE_FULL) {
+#pragma unroll
+                for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q));
+            }
+        }
+        uint4* dstp = a.dst + poly * N + gbase;
+#pragma unroll
+        for (int i = 0; i < PER; i++) dstp[(size_t)i * gstride] = outv[i];
+    }
+    if (a.cnt_out) {
+        __syncthreads();
+        if (tid == 0) red_release_gpu_add(a.cnt_out + poly, 1u);
+    }
+}
+
 // ----------------------------------------------------------------------------- launch table
 typedef void (*PassKernel)(const PassArgs);
 
@@ -611,6 +859,40 @@ static PassCfg multi_cfg_t(int B) {
         default: return make_cfg<9, 4, FIRST, SL>();
     }
 }
+// Permutation-free negacyclic passes (B in [5, 8], warp-owned groups).
+template <int B, int C, bool INV, bool SL>
+static PassCfg make_nc_cfg() {
+    using S = PassShape<B, 3, C, true>;
+    PassCfg c;
+    c.fn = k_nc_pass<B, C, INV, SL, 3>;
+    c.B = B;
+    c.C = C;
+    c.threads = C * S::T;
+    c.smem = ((size_t)C * S::GS + (size_t)C * S::TS) * sizeof(uint4);
+    return c;
+}
+template <bool INV, bool SL>
+static PassCfg nc_cfg_t(int B) {
+    switch (B) {
+        case 5: return make_nc_cfg<5, 8, INV, SL>();
+        case 6: return make_nc_cfg<6, 8, INV, SL>();
+        case 7: return make_nc_cfg<7, 8, INV, SL>();
+        default: return make_nc_cfg<8, NTT_C8, INV, SL>();
+    }
+}
+static PassCfg nc_cfg(bool inv, bool scale_last, int B) {
+    if (!inv) return nc_cfg_t<false, false>(B);
+    return scale_last ? nc_cfg_t<true, true>(B) : nc_cfg_t<true, false>(B);
+}
+// pass widths of the permutation-free path: ceil(n / 8) passes, widths as equal as possible
+static std::vector<int> nc_pass_bits(int n) {
+    std::vector<int> b;
+    if (n < 10) return b;
+    const int np = (n + 7) / 8 < 2 ? 2 : (n + 7) / 8;
+    for (int i = 0; i < np; i++) b.push_back(n / np + (i < n % np ? 1 : 0));
+    return b;
+}
+
 static PassCfg pass_cfg(size_t npass, size_t i, int B, bool scale_last) {
     if (npass == 1) return scale_last ? single_cfg_t<true>(B) : single_cfg_t<false>(B);
     if (i == 0) return multi_cfg_t<true, false>(B);
@@ -635,15 +917,23 @@ struct ntt128_plan_s {
     std::vector<u128> q_host;
     int* d_err = nullptr;
     std::vector<uint4*> d_pt_fwd, d_pt_inv, d_pt_inv_r;  // per pass, [nq][pt_stride]
+    // permutation-free negacyclic path (n >= 10): pass widths bottom-up, per-pass tables
+    // [nq][2^(n - lo - B)][2^B - 1] (psi, psi^-1; the top inverse pass N^-1 / N^-1 R scaled)
+    std::vector<int> nc_bits;
+    std::vector<uint4*> d_nc_fwd, d_nc_inv, d_nc_inv_r;
+    std::vector<uint64_t> nc_stride;
     uint32_t* d_order = nullptr;                         // [batch] CTA-slot -> polynomial (nq == batch)
     std::vector<uint64_t> pt_stride;
     // Pass-overlap completion counters, one set per stream (keyed by cudaStreamGetId):
-    // counters only grow; transform number g on a stream waits for g x (CTAs per
-    // polynomial) so in-stream order makes them exact without a reset, and different
-    // streams never share a set.
+    // counters only grow; the host keeps, per counter row, the value the row reaches once
+    // every pass enqueued so far on the stream has signalled (a pass adds its CTAs per
+    // polynomial), so in-stream order makes the targets exact without a reset, for any mix
+    // of pass structures, and different streams never share a set.
+    static constexpr int MAX_ROWS = 3;                 // passes - 1 of the deepest schedule (4 passes)
     struct StreamCtr {
-        uint32_t* d = nullptr;   // [npass - 1][batch]
-        uint64_t gen = 0;
+        uint32_t* d = nullptr;                          // [MAX_ROWS][batch]
+        uint32_t expected[MAX_ROWS] = {0, 0, 0};
+        uint4* scratch = nullptr;                       // [2][batch][N]: polymul spectra, in-place copy
     };
     std::mutex mu;
     std::unordered_map<unsigned long long, StreamCtr> ctrs;
@@ -664,7 +954,15 @@ static void plan_free(ntt128_plan_s* p) {
     cudaFree(p->d_f_untwist_r);
     cudaFree(p->d_err);
     cudaFree(p->d_order);
-    for (auto& kv : p->ctrs) cudaFree(kv.second.d);
+    for (auto& kv : p->ctrs) {
+        cudaFree(kv.second.d);
+        cudaFree(kv.second.scratch);
+    }
+    for (size_t i = 0; i < p->d_nc_fwd.size(); i++) {
+        if (p->d_nc_inv_r[i] != p->d_nc_inv[i]) cudaFree(p->d_nc_inv_r[i]);
+        cudaFree(p->d_nc_fwd[i]);
+        cudaFree(p->d_nc_inv[i]);
+    }
     for (size_t i = 0; i < p->d_pt_fwd.size(); i++) {
         if (p->d_pt_inv_r[i] != p->d_pt_inv[i]) cudaFree(p->d_pt_inv_r[i]);
         cudaFree(p->d_pt_fwd[i]);
@@ -876,6 +1174,57 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
             if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = NTT128_ERR_CUDA;
             lo += b;
         }
+        // permutation-free negacyclic tables (ntt128_forward_bitrev / inverse_bitrev, polymul)
+        if (st == NTT128_OK && kind) {
+            p->nc_bits = nc_pass_bits((int)log2n);
+            std::vector<uint4> sc(n_moduli), scr(n_moduli);
+            for (uint32_t m = 0; m < n_moduli; m++) {
+                sc[m] = make_uint4(mc[m].ninv_m[0], mc[m].ninv_m[1], mc[m].ninv_m[2], mc[m].ninv_m[3]);
+                scr[m] = make_uint4(mc[m].ninv_rm[0], mc[m].ninv_rm[1], mc[m].ninv_rm[2], mc[m].ninv_rm[3]);
+            }
+            uint4 *d_sc = nullptr, *d_scr = nullptr;
+            if (!p->nc_bits.empty()) {
+                if (cudaMalloc(&d_sc, n_moduli * sizeof(uint4)) != cudaSuccess ||
+                    cudaMalloc(&d_scr, n_moduli * sizeof(uint4)) != cudaSuccess) st = NTT128_ERR_OOM;
+                if (st == NTT128_OK && (cudaMemcpy(d_sc, sc.data(), n_moduli * sizeof(uint4), cudaMemcpyHostToDevice) != cudaSuccess ||
+                                        cudaMemcpy(d_scr, scr.data(), n_moduli * sizeof(uint4), cudaMemcpyHostToDevice) != cudaSuccess))
+                    st = NTT128_ERR_CUDA;
+            }
+            int nlo = 0;
+            const size_t nnp = p->nc_bits.size();
+            for (size_t i = 0; i < nnp && st == NTT128_OK; i++) {
+                const int b = p->nc_bits[i];
+                const uint64_t stride = ((uint64_t)1 << (log2n - nlo - b)) * (((uint64_t)1 << b) - 1);
+                p->nc_stride.push_back(stride);
+                const bool top = i + 1 == nnp;
+                uint4 *f = nullptr, *v = nullptr, *vr = nullptr;
+                const size_t bytes = (size_t)stride * n_moduli * sizeof(uint4);
+                if (cudaMalloc(&f, bytes) != cudaSuccess || cudaMalloc(&v, bytes) != cudaSuccess) st = NTT128_ERR_OOM;
+                if (st == NTT128_OK && top && cudaMalloc(&vr, bytes) != cudaSuccess) st = NTT128_ERR_OOM;
+                if (!vr) vr = v;
+                p->d_nc_fwd.push_back(f);
+                p->d_nc_inv.push_back(v);
+                p->d_nc_inv_r.push_back(vr);
+                if (st != NTT128_OK) break;
+                unsigned gx = (unsigned)((stride + 255) / 256);
+                if (gx > 4096) gx = 4096;
+                const dim3 grid(gx, n_moduli);
+                k_gather_nc_tw<<<grid, 256>>>(f, stride, p->d_f_twist, log2n, nlo, b, 0, nullptr, p->d_mods);
+                k_gather_nc_tw<<<grid, 256>>>(v, stride, p->d_f_twist, log2n, nlo, b, 1, top ? d_sc : nullptr, p->d_mods);
+                if (vr != v) k_gather_nc_tw<<<grid, 256>>>(vr, stride, p->d_f_twist, log2n, nlo, b, 1, d_scr, p->d_mods);
+                ntt128_count_launch(vr != v ? 3 : 2);
+                if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = NTT128_ERR_CUDA;
+                for (int iv = 0; iv < 2 && st == NTT128_OK; iv++)
+                    for (int sl = 0; sl < 2; sl++) {
+                        PassCfg c = nc_cfg(iv == 1, sl == 1, b);
+                        if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
+                            st = NTT128_ERR_CUDA;
+                    }
+                nlo += b;
+            }
+            cudaFree(d_sc);
+            cudaFree(d_scr);
+        }
         // the power tables are only the source of the pass tables
         cudaFree(p->d_tw_fwd); p->d_tw_fwd = nullptr;
         cudaFree(p->d_tw_inv); p->d_tw_inv = nullptr;
@@ -913,6 +1262,77 @@ struct RunOpts {
 
 static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaStream_t stream);
 
+static bool overlap_allowed(size_t npass, cudaStream_t stream, bool* ok) {
+    *ok = npass > 1 && getenv("NTT128_NO_PDL") == nullptr;
+    if (*ok) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) return false;
+        if (cs != cudaStreamCaptureStatusNone) *ok = false;
+    }
+    return true;
+}
+static cudaError_t launch_pass(const PassCfg& c, const PassArgs& a, uint64_t ctas, cudaStream_t stream, bool pdl) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3((unsigned)c.threads);
+    cfg.dynamicSmemBytes = c.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, c.fn, a);
+}
+
+// The stream's counter set (allocated and zeroed in stream order on first use); `lk` is
+// locked and stays locked until the caller has enqueued every pass.
+static ntt128_status stream_counters(ntt128_plan_s* p, cudaStream_t stream, std::unique_lock<std::mutex>& lk,
+                                     ntt128_plan_s::StreamCtr** out) {
+    unsigned long long sid = 0;
+    if (cudaStreamGetId(stream, &sid) != cudaSuccess) return NTT128_ERR_CUDA;
+    lk.lock();
+    ntt128_plan_s::StreamCtr& c = p->ctrs[sid];
+    if (!c.d) {
+        const size_t bytes = (size_t)ntt128_plan_s::MAX_ROWS * p->batch * sizeof(uint32_t);
+        if (cudaMalloc(&c.d, bytes) != cudaSuccess) return NTT128_ERR_OOM;
+        if (cudaMemsetAsync(c.d, 0, bytes, stream) != cudaSuccess) return NTT128_ERR_CUDA;
+    }
+    *out = &c;
+    return NTT128_OK;
+}
+// The stream's scratch (2 x batch x N residues), allocated on first use and kept until the
+// plan is destroyed: no per-call stream-ordered allocation (a memory pool trimmed at a
+// synchronisation would re-grow inside the next call).  Work on one stream is ordered, so
+// consecutive calls may reuse it.
+static ntt128_status stream_scratch(ntt128_plan_s* p, cudaStream_t stream, uint4** out) {
+    unsigned long long sid = 0;
+    if (cudaStreamGetId(stream, &sid) != cudaSuccess) return NTT128_ERR_CUDA;
+    std::lock_guard<std::mutex> lk(p->mu);
+    ntt128_plan_s::StreamCtr& c = p->ctrs[sid];
+    if (!c.scratch && cudaMalloc(&c.scratch, 2 * (size_t)p->N * p->batch * sizeof(uint4)) != cudaSuccess) {
+        c.scratch = nullptr;
+        return NTT128_ERR_OOM;
+    }
+    *out = c.scratch;
+    return NTT128_OK;
+}
+
+// pass i (of npass, execution order) of an overlapped transform: the first pass waits for
+// the previous grid; pass i > 0 waits on row i - 1 for the previous pass's CTAs per
+// polynomial; every pass but the last signals row i.
+static void set_overlap(ntt128_plan_s* p, ntt128_plan_s::StreamCtr* ctr, PassArgs& a, size_t i, size_t npass,
+                        uint32_t prev_ctas_per_poly) {
+    a.pdl_wait = i == 0 ? 1u : 0u;
+    if (i > 0) {
+        ctr->expected[i - 1] += prev_ctas_per_poly;
+        a.cnt_in = ctr->d + (i - 1) * (size_t)p->batch;
+        a.target = ctr->expected[i - 1];
+    }
+    if (i + 1 < npass) a.cnt_out = ctr->d + i * (size_t)p->batch;
+}
+
 static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* dst, cudaStream_t stream,
                                    const RunOpts& o) {
     const int n = (int)p->log2n;
@@ -922,27 +1342,13 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
     // programmatic dependent launch; pass i+1 CTAs wait per polynomial on pass i's
     // completion counters instead of on the whole grid.  Not under stream capture
     // (a captured launch would replay stale counter targets).
-    bool overlap = npass > 1 && getenv("NTT128_NO_PDL") == nullptr;
-    if (overlap) {
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) return NTT128_ERR_CUDA;
-        if (cs != cudaStreamCaptureStatusNone) overlap = false;
-    }
-    uint32_t* cnt = nullptr;
-    uint64_t gen = 0;
+    bool overlap = false;
+    if (!overlap_allowed(npass, stream, &overlap)) return NTT128_ERR_CUDA;
+    ntt128_plan_s::StreamCtr* ctr = nullptr;
     std::unique_lock<std::mutex> lk(p->mu, std::defer_lock);
     if (overlap) {
-        unsigned long long sid = 0;
-        if (cudaStreamGetId(stream, &sid) != cudaSuccess) return NTT128_ERR_CUDA;
-        lk.lock();   // held until every pass is enqueued: generations follow stream order
-        ntt128_plan_s::StreamCtr& c = p->ctrs[sid];
-        if (!c.d) {
-            const size_t bytes = (npass - 1) * (size_t)p->batch * sizeof(uint32_t);
-            if (cudaMalloc(&c.d, bytes) != cudaSuccess) return NTT128_ERR_OOM;
-            if (cudaMemsetAsync(c.d, 0, bytes, stream) != cudaSuccess) return NTT128_ERR_CUDA;
-        }
-        gen = ++c.gen;
-        cnt = c.d;
+        ntt128_status st = stream_counters(p, stream, lk, &ctr);
+        if (st != NTT128_OK) return st;
     }
     int lo = 0;
     uint32_t prev_ctas_per_poly = 0;
@@ -970,29 +1376,59 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
             if (o.inverse && last) a.fout = o.polymul ? p->d_f_untwist_r : p->d_f_untwist;
         }
         const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (uint64_t)c.C);
-        if (overlap) {
-            a.pdl_wait = first ? 1u : 0u;
-            if (!first) {
-                a.cnt_in = cnt + (i - 1) * (size_t)p->batch;
-                a.target = (uint32_t)(gen * (uint64_t)prev_ctas_per_poly);
-            }
-            if (!last) a.cnt_out = cnt + i * (size_t)p->batch;
-        }
+        if (overlap) set_overlap(p, ctr, a, i, npass, prev_ctas_per_poly);
         const uint64_t ctas = (a.total_groups + c.C - 1) / c.C;
-        cudaLaunchConfig_t cfg;
-        memset(&cfg, 0, sizeof(cfg));
-        cfg.gridDim = dim3((unsigned)ctas);
-        cfg.blockDim = dim3((unsigned)c.threads);
-        cfg.dynamicSmemBytes = c.smem;
-        cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = overlap ? 1 : 0;
-        if (cudaLaunchKernelEx(&cfg, c.fn, a) != cudaSuccess) return NTT128_ERR_CUDA;
+        if (launch_pass(c, a, ctas, stream, overlap) != cudaSuccess) return NTT128_ERR_CUDA;
         ntt128_count_launch(1);
         lo += B;
+        prev_ctas_per_poly = ctas_per_poly;
+    }
+    return NTT128_OK;
+}
+
+// Permutation-free negacyclic transform: forward = CT passes top-down,
+// natural in, bit-reversed out; inverse = GS passes bottom-up, bit-reversed in, natural
+// out, N^-1 in the last stage; `pmul` fuses the point-wise product into the inverse's
+// first load (its R^-1 is cancelled by the R-scaled last-stage table).
+static ntt128_status run_transform_nc(ntt128_plan_s* p, const uint4* src, uint4* dst, cudaStream_t stream,
+                                      bool inverse, const uint4* pmul) {
+    const int n = (int)p->log2n;
+    const size_t npass = p->nc_bits.size();
+    bool overlap = false;
+    if (!overlap_allowed(npass, stream, &overlap)) return NTT128_ERR_CUDA;
+    ntt128_plan_s::StreamCtr* ctr = nullptr;
+    std::unique_lock<std::mutex> lk(p->mu, std::defer_lock);
+    if (overlap) {
+        ntt128_status st = stream_counters(p, stream, lk, &ctr);
+        if (st != NTT128_OK) return st;
+    }
+    std::vector<int> los(npass);
+    for (size_t k = 0, lo = 0; k < npass; k++) { los[k] = (int)lo; lo += p->nc_bits[k]; }
+    uint32_t prev_ctas_per_poly = 0;
+    for (size_t i = 0; i < npass; i++) {
+        const size_t k = inverse ? i : npass - 1 - i;      // pass k covers bits [los[k], los[k] + B)
+        const int B = p->nc_bits[k];
+        const bool top = k + 1 == npass;
+        PassCfg c = nc_cfg(inverse, inverse && top, B);
+        PassArgs a;
+        memset(&a, 0, sizeof(a));
+        a.src = i == 0 ? src : dst;
+        a.dst = dst;
+        a.mods = p->d_mods;
+        a.order = p->d_order;
+        a.pt_stride = p->nc_stride[k];
+        a.total_groups = (uint64_t)p->batch << (n - B);
+        a.n = (uint32_t)n;
+        a.lo = (uint32_t)los[k];
+        a.nq = p->nq;
+        a.pt = !inverse ? p->d_nc_fwd[k] : (pmul ? p->d_nc_inv_r[k] : p->d_nc_inv[k]);
+        if (i == 0 && pmul) a.pmul = pmul;
+        a.ninv_r = pmul ? 1 : 0;
+        const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (uint64_t)c.C);
+        if (overlap) set_overlap(p, ctr, a, i, npass, prev_ctas_per_poly);
+        const uint64_t ctas = (a.total_groups + c.C - 1) / c.C;
+        if (launch_pass(c, a, ctas, stream, overlap) != cudaSuccess) return NTT128_ERR_CUDA;
+        ntt128_count_launch(1);
         prev_ctas_per_poly = ctas_per_poly;
     }
     return NTT128_OK;
@@ -1041,11 +1477,10 @@ static ntt128_status transform(const ntt128_plan_t p, const uint64_t* d_in, uint
         // the first pass gathers bit-reversed columns: it cannot run in place
         const size_t bytes = (size_t)p->N * p->batch * sizeof(uint4);
         uint4* tmp = nullptr;
-        if (cudaMallocAsync(&tmp, bytes, stream) != cudaSuccess) return NTT128_ERR_OOM;
+        ntt128_status s = stream_scratch(p, stream, &tmp);
+        if (s != NTT128_OK) return s;
         if (cudaMemcpyAsync(tmp, src, bytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess) return NTT128_ERR_CUDA;
-        ntt128_status s = run_transform(p, tmp, dst, stream, o);
-        cudaFreeAsync(tmp, stream);
-        return s;
+        return run_transform(p, tmp, dst, stream, o);
     }
     return run_transform(p, src, dst, stream, o);
 }
@@ -1069,17 +1504,44 @@ extern "C" ntt128_status ntt128_polymul(const ntt128_plan_t p, const uint64_t* d
         if (s == NTT128_OK) s = check_range(p, (const uint4*)d_b, stream);
         if (s != NTT128_OK) return s;
     }
-    const size_t bytes = (size_t)p->N * p->batch * sizeof(uint4);
-    uint4 *fa = nullptr, *fb = nullptr;
-    if (cudaMallocAsync(&fa, bytes, stream) != cudaSuccess) return NTT128_ERR_OOM;
-    if (cudaMallocAsync(&fb, bytes, stream) != cudaSuccess) { cudaFreeAsync(fa, stream); return NTT128_ERR_OOM; }
-    RunOpts fwd{false, nullptr, false};
-    ntt128_status s = run_transform(p, (const uint4*)d_a, fa, stream, fwd);
-    if (s == NTT128_OK) s = run_transform(p, (const uint4*)d_b, fb, stream, fwd);
-    // inverse with the point-wise Montgomery product fused into its first pass's load
-    RunOpts inv{true, fb, true};
-    if (s == NTT128_OK) s = run_transform(p, fa, (uint4*)d_c, stream, inv);
-    cudaFreeAsync(fa, stream);
-    cudaFreeAsync(fb, stream);
+    uint4* fa = nullptr;
+    ntt128_status s = stream_scratch(p, stream, &fa);
+    if (s != NTT128_OK) return s;
+    uint4* fb = fa + (size_t)p->N * p->batch;
+    if (!p->nc_bits.empty() && getenv("NTT128_NO_NC") == nullptr) {
+        // permutation-free pipeline: no twist / untwist multiplies, spectra stay bit-reversed
+        s = run_transform_nc(p, (const uint4*)d_a, fa, stream, false, nullptr);
+        if (s == NTT128_OK) s = run_transform_nc(p, (const uint4*)d_b, fb, stream, false, nullptr);
+        if (s == NTT128_OK) s = run_transform_nc(p, fa, (uint4*)d_c, stream, true, fb);
+    } else {
+        RunOpts fwd{false, nullptr, false};
+        s = run_transform(p, (const uint4*)d_a, fa, stream, fwd);
+        if (s == NTT128_OK) s = run_transform(p, (const uint4*)d_b, fb, stream, fwd);
+        // inverse with the point-wise Montgomery product fused into its first pass's load
+        RunOpts inv{true, fb, true};
+        if (s == NTT128_OK) s = run_transform(p, fa, (uint4*)d_c, stream, inv);
+    }
     return s;
+}
+
+// Bit-reversed-order negacyclic transforms (include/ntt128.h): negacyclic plans, N >= 2^10.
+static ntt128_status transform_bitrev(const ntt128_plan_t p, const uint64_t* d_in, uint64_t* d_out, cudaStream_t stream,
+                                      bool inverse) {
+    if (!p || !d_in || !d_out) return NTT128_ERR_INVALID_ARG;
+    if (!aligned16(d_in) || !aligned16(d_out)) return NTT128_ERR_ALIGNMENT;
+    if (p->kind != 1 || p->nc_bits.empty()) return NTT128_ERR_UNSUPPORTED;
+    DeviceGuard g(p->device);
+    if (p->flags & NTT128_FLAG_CHECK_INPUT) {
+        ntt128_status s = check_range(p, (const uint4*)d_in, stream);
+        if (s != NTT128_OK) return s;
+    }
+    return run_transform_nc(p, (const uint4*)d_in, (uint4*)d_out, stream, inverse, nullptr);
+}
+extern "C" ntt128_status ntt128_forward_bitrev(const ntt128_plan_t p, const uint64_t* d_in, uint64_t* d_out,
+                                               ntt128_stream_t stream) {
+    return transform_bitrev(p, d_in, d_out, (cudaStream_t)stream, false);
+}
+extern "C" ntt128_status ntt128_inverse_bitrev(const ntt128_plan_t p, const uint64_t* d_in, uint64_t* d_out,
+                                               ntt128_stream_t stream) {
+    return transform_bitrev(p, d_in, d_out, (cudaStream_t)stream, true);
 }

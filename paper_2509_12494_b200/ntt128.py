@@ -26,7 +26,7 @@ _vp = ctypes.c_void_p
 _L.ntt128_plan_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_uint32, ctypes.c_uint32, _u64p, _u64p,
                                   ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int]
 _L.ntt128_plan_create.restype = ctypes.c_int
-for _name in ("ntt128_forward", "ntt128_inverse"):
+for _name in ("ntt128_forward", "ntt128_inverse", "ntt128_forward_bitrev", "ntt128_inverse_bitrev"):
     getattr(_L, _name).argtypes = [_vp, _vp, _vp, _vp]
     getattr(_L, _name).restype = ctypes.c_int
 _L.ntt128_polymul.argtypes = [_vp, _vp, _vp, _vp, _vp]
@@ -49,7 +49,8 @@ CYCLIC, NEGACYCLIC, FLAG_CHECK_INPUT = 0, 1, 0x100
 OK = 0
 _ARG_ERRORS = {1, 2, 3, 4, 5, 6, 7}
 
-EXPORTED = ("ntt128_plan_create", "ntt128_forward", "ntt128_inverse", "ntt128_polymul", "ntt128_plan_info",
+EXPORTED = ("ntt128_plan_create", "ntt128_forward", "ntt128_inverse", "ntt128_forward_bitrev",
+            "ntt128_inverse_bitrev", "ntt128_polymul", "ntt128_plan_info",
             "ntt128_plan_destroy", "vec128_add", "vec128_sub", "vec128_mul", "vec128_axpy",
             "ntt128_status_string", "ntt128_launch_count", "ntt128_fourstep_create", "ntt128_fourstep_forward_a",
             "ntt128_fourstep_forward_c", "ntt128_fourstep_inverse_a", "ntt128_fourstep_inverse_c",
@@ -151,6 +152,21 @@ class Plan:
         out = torch.empty_like(y) if out is None else out
         self._shape_ok(out, "out")
         _check(_L.ntt128_inverse(self._h, _ptr(y, "y"), _ptr(out, "out"), _stream(y)), "ntt128_inverse")
+        return out
+
+    def forward_bitrev(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """negacyclic spectrum in bit-reversed order (ntt128_forward_bitrev)"""
+        self._shape_ok(x, "x")
+        out = torch.empty_like(x) if out is None else out
+        self._shape_ok(out, "out")
+        _check(_L.ntt128_forward_bitrev(self._h, _ptr(x, "x"), _ptr(out, "out"), _stream(x)), "ntt128_forward_bitrev")
+        return out
+
+    def inverse_bitrev(self, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        self._shape_ok(y, "y")
+        out = torch.empty_like(y) if out is None else out
+        self._shape_ok(out, "out")
+        _check(_L.ntt128_inverse_bitrev(self._h, _ptr(y, "y"), _ptr(out, "out"), _stream(y)), "ntt128_inverse_bitrev")
         return out
 
     def polymul(self, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
