@@ -848,6 +848,28 @@ static PassCfg single_cfg_t(int B) {
         default: return make_cfg<12, 1, true, SL, true>();
     }
 }
+// Single pass for a few polynomials (latency, BASELINE cfg 1): one polynomial per CTA and
+// radix-4 register rounds, so N/4 threads share the work instead of N/8 with idle groups.
+template <bool SL>
+static PassCfg single_lat_cfg_t(int B) {
+    switch (B) {
+        case 6: return make_cfg<6, 1, true, SL, true, 2>();
+        case 7: return make_cfg<7, 1, true, SL, true, 2>();
+        case 8: return make_cfg<8, 1, true, SL, true, 2>();
+        case 9: return make_cfg<9, 1, true, SL, true, 2>();
+        case 10: return make_cfg<10, 1, true, SL, true, 2>();
+        case 11: return make_cfg<11, 1, true, SL, true, 2>();
+        default: return make_cfg<12, 1, true, SL, true, 2>();
+    }
+}
+#ifndef NTT_LAT_CTAS
+#define NTT_LAT_CTAS 148      // single-pass launches with fewer CTAs than this use the latency shape
+#endif
+static bool use_latency_shape(int B, uint32_t batch) {
+    if (B < 6 || B > 12) return false;
+    const PassCfg d = single_cfg_t<false>(B);
+    return ((uint64_t)batch + d.C - 1) / d.C < (uint64_t)NTT_LAT_CTAS;
+}
 // Multi-pass: first pass (gather, stage 0), middle passes, last pass (optionally scaled).
 template <bool FIRST, bool SL>
 static PassCfg multi_cfg_t(int B) {
@@ -1129,6 +1151,11 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
                 PassCfg c = pass_cfg(p->bits.size(), i, p->bits[i], sl == 1);
                 if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
                     st = NTT128_ERR_CUDA;
+                if (p->bits.size() == 1 && use_latency_shape(p->bits[i], batch)) {
+                    c = sl ? single_lat_cfg_t<true>(p->bits[i]) : single_lat_cfg_t<false>(p->bits[i]);
+                    if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
+                        st = NTT128_ERR_CUDA;
+                }
             }
         }
     }
@@ -1355,6 +1382,8 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
     for (size_t i = 0; i < npass; i++) {
         const int B = p->bits[i];
         PassCfg c = pass_cfg(npass, i, B, scale_last);
+        if (npass == 1 && use_latency_shape(B, p->batch))
+            c = scale_last ? single_lat_cfg_t<true>(B) : single_lat_cfg_t<false>(B);
         PassArgs a;
         memset(&a, 0, sizeof(a));
         a.src = i == 0 ? src : dst;
