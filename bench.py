@@ -331,9 +331,9 @@ def run_e2e(plan, x_host, args, stream, bfly_per_step, world):
     """The same metric end to end through the public API: every step uploads its input
     from pinned host memory, runs forward + inverse, and downloads the result.  Steps are
     pipelined over three streams (upload of step i+1 and download of step i-1 overlap the
-    transforms of step i; two device buffer sets), the way a serving loop would run."""
+    transforms of step i; three device buffer sets), the way a serving loop would run."""
     import torch
-    NB = 2
+    NB = 3
     hx = [torch.from_numpy(np.ascontiguousarray(x_host).view(np.int64)).pin_memory() for _ in range(NB)]
     hz = [torch.empty_like(hx[0]).pin_memory() for _ in range(NB)]
     dx = [torch.empty(hx[0].shape, dtype=hx[0].dtype, device="cuda") for _ in range(NB)]
@@ -347,11 +347,12 @@ def run_e2e(plan, x_host, args, stream, bfly_per_step, world):
 
     def step(i):
         b = i % NB
-        s_in.wait_event(down[b])                      # buffer b's previous result has left the device
+        s_in.wait_event(done[b])                      # dx[b]'s previous reader (step i - NB) is done
         with torch.cuda.stream(s_in):
             dx[b].copy_(hx[b], non_blocking=True)
             up[b].record(s_in)
         comp.wait_event(up[b])
+        comp.wait_event(down[b])                      # dz[b]'s previous result has left the device
         with torch.cuda.stream(comp):
             plan.forward(dx[b], out=dy[b])
             plan.inverse(dy[b], out=dz[b])
@@ -368,6 +369,7 @@ def run_e2e(plan, x_host, args, stream, bfly_per_step, world):
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(comp)
+    s_in.wait_event(e0)
     for i in range(steps):
         step(i)
     for b in range(NB):
@@ -379,7 +381,7 @@ def run_e2e(plan, x_host, args, stream, bfly_per_step, world):
     nbytes = hx[0].numel() * 8
     return {"value": bfly_per_step * world * steps / (ms / 1e3), "unit": "butterflies/s",
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": ms / steps,
-            "pipelined": "upload/compute/download on 3 streams, 2 buffer sets"}
+            "pipelined": "upload/compute/download on 3 streams, 3 buffer sets"}
 
 
 # ----------------------------------------------------------------------------- other §8 rows
