@@ -40,8 +40,26 @@
 #ifndef NTT_UNROLL_ROUNDS
 #define NTT_UNROLL_ROUNDS 0   // 1: unroll the register rounds (compile-time windows)
 #endif
+// Groups per CTA of the multi-pass kernels (tools/gpu_sweep_variants.sh): one warp-owned
+// (B = 8) or two-warp (B = 9) group per CTA avoids every cross-warp barrier and wins 5-8 %
+// over C = 4; 8/16-thread groups (B = 6, 7) need C = 8 for occupancy (32 CTAs/SM cap).
 #ifndef NTT_C8
-#define NTT_C8 4              // groups per CTA of the 8-stage multi-pass kernel (8 measured 3% slower)
+#define NTT_C8 1
+#endif
+#ifndef NTT_C9
+#define NTT_C9 1
+#endif
+#ifndef NTT_NC_C8
+#define NTT_NC_C8 4           // permutation-free passes share one twiddle set per CTA when lo > 0
+#endif
+#ifndef NTT_C7
+#define NTT_C7 8
+#endif
+#ifndef NTT_C6
+#define NTT_C6 8
+#endif
+#ifndef NTT_C5
+#define NTT_C5 8
 #endif
 #ifndef NTT_OCC_THREADS
 #define NTT_OCC_THREADS 768   // resident threads per SM the pass kernels are register-budgeted for
@@ -382,8 +400,8 @@ k_ntt_pass(const PassArgs a) {
     constexpr int LT = B - RB;                   // log2 T
     // multi-pass first pass: the rows of a lane pair/quad are T/2 (T/4) apart, so the
     // bit-reversed rows land in different banks (8-lane phase = CM groups x 8/CM rows)
-    constexpr int RT = (!PADL || !FIRST) ? 0 : (S::CM == 8 ? 0 : (S::CM == 4 ? 1 : (S::CM == 2 ? 2 : 3)));
-    static_assert(RT <= LT || LT == 0, "row rotation needs enough rows");
+    constexpr int RT0 = (!PADL || !FIRST) ? 0 : (S::CM == 8 ? 0 : (S::CM == 4 ? 1 : (S::CM == 2 ? 2 : 3)));
+    constexpr int RT = RT0 < LT ? RT0 : LT;
     const int c_me = tid % C;
     const int u_me = tid / C;
     const int t0 = (RT == 0 || LT == 0) ? u_me : ((u_me >> RT) | ((u_me & ((1 << RT) - 1)) << (LT - RT)));
@@ -874,11 +892,11 @@ static bool use_latency_shape(int B, uint32_t batch) {
 template <bool FIRST, bool SL>
 static PassCfg multi_cfg_t(int B) {
     switch (B) {
-        case 5: return make_cfg<5, 8, FIRST, SL>();
-        case 6: return make_cfg<6, 8, FIRST, SL>();
-        case 7: return make_cfg<7, 8, FIRST, SL>();
+        case 5: return make_cfg<5, NTT_C5, FIRST, SL>();
+        case 6: return make_cfg<6, NTT_C6, FIRST, SL>();
+        case 7: return make_cfg<7, NTT_C7, FIRST, SL>();
         case 8: return make_cfg<8, NTT_C8, FIRST, SL, false, NTT_RB8>();
-        default: return make_cfg<9, 4, FIRST, SL>();
+        default: return make_cfg<9, NTT_C9, FIRST, SL>();
     }
 }
 // Permutation-free negacyclic passes (B in [5, 8], warp-owned groups).
@@ -899,7 +917,7 @@ static PassCfg nc_cfg_t(int B) {
         case 5: return make_nc_cfg<5, 8, INV, SL>();
         case 6: return make_nc_cfg<6, 8, INV, SL>();
         case 7: return make_nc_cfg<7, 8, INV, SL>();
-        default: return make_nc_cfg<8, NTT_C8, INV, SL>();
+        default: return make_nc_cfg<8, NTT_NC_C8, INV, SL>();
     }
 }
 static PassCfg nc_cfg(bool inv, bool scale_last, int B) {
