@@ -304,12 +304,79 @@ __device__ __forceinline__ void bfly1(U128& u, U128& v, const uint32_t q[4]) {
         u = a;
     }
 }
+// Butterfly with twiddle 1 on values in the mode's lazy range (a later stage's j = 0 block).
+template <int MODE>
+__device__ __forceinline__ void bfly_tw1(U128& u, U128& v, const uint32_t q[4], const uint32_t q2[4]) {
+    if (MODE == MODE_FULL) {
+        const U128 a = add_mod(u, v, q);
+        v = sub_mod(u, v, q);
+        u = a;
+    } else if (MODE == MODE_HALF) {   // [0, 2q): arithmetic mod 2q
+        const U128 a = add_mod(u, v, q2);
+        v = sub_mod(u, v, q2);
+        u = a;
+    } else {                          // [0, 4q): both to [0, 2q), then Harvey's sums
+        const U128 us = reduce_2q(u, q2), t = reduce_2q(v, q2);
+        u = add_nored(us, t);
+        v = sub_add_nored(us, t, q2);
+    }
+}
 
 // Register rounds of one pass on a CTA's tile in shared memory: RB stages on E elements
 // per thread (window [w, w + RB) of the group's index bits), 8-lane conflict-free
 // addressing.  With the padded layout the E slots of a round are s0 + k st (one base,
 // one stride per round), and a stage's distinct twiddles are loaded once: stage w + bit
 // needs 2^bit of them (index (2^sl - 1) + tlo + (j << w), j < 2^bit).
+// R0: the first round of a first pass (w = 0, global stage = local stage), peeled so the
+// butterflies with twiddle index j = 0 (twiddle 1: all of stage 0, half of stage 1, a
+// quarter of stage 2) skip their multiply at compile time.
+template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL, bool R0>
+__device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4* tws, const int t, const uint32_t lo,
+                                           const uint32_t n, const uint32_t q[4], const uint32_t q2[4],
+                                           const uint32_t qinv0, const U128& nf) {
+    using S = PassShape<B, RBMAX, C, PADL>;
+    constexpr int RB = S::RB, E = S::E;
+    const int slo = R0 ? 0 : rd * RB;
+    const int w = R0 ? 0 : ((slo + RB <= B) ? slo : B - RB);   // E-element window [w, w + RB)
+    const int tlo = t & ((1 << w) - 1), thi = (t >> w) << (w + RB);
+    const int l0 = thi | tlo;                                 // element k of this thread: l0 + (k << w)
+    const int s0 = S::LINEAR ? slot<B, PADL>(l0) : 0;
+    const int st = S::LINEAR ? (w >= 3 ? (9 << (w - 3)) : (1 << w)) : 0;
+    U128 x[E];
+#pragma unroll
+    for (int k = 0; k < E; k++) x[k] = u128_from(gsm[S::LINEAR ? s0 + k * st : slot<B, PADL>(l0 | (k << w))]);
+#pragma unroll
+    for (int bit = 0; bit < RB; bit++) {
+        const int sl = w + bit;                      // local stage
+        if (sl < slo) continue;                      // overlap of the last window
+        const bool last = SCALE_LAST && lo + sl == n - 1;
+        if (R0 && bit == 0 && !last) {               // stage 0: twiddle 1, inputs canonical
+#pragma unroll
+            for (int kk = 0; kk < E / 2; kk++) {
+                const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                bfly1<MODE>(x[k0], x[k0 | (1 << bit)], q);
+            }
+            continue;
+        }
+        const uint4* tp = tws + tlo + ((1 << sl) - 1);
+        U128 tw[E / 2];                              // the first 2^bit are used
+#pragma unroll
+        for (int j = 0; j < (1 << bit); j++) tw[j] = u128_from(tp[j << w]);
+#pragma unroll
+        for (int kk = 0; kk < E / 2; kk++) {
+            const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+            const int k1 = k0 | (1 << bit);
+            const int j = kk & ((1 << bit) - 1);
+            if (R0 && j == 0 && !last) bfly_tw1<MODE>(x[k0], x[k1], q, q2);
+            else if (last) bfly<MODE, true>(x[k0], x[k1], tw[j], q, q2, qinv0, nf);
+            else bfly<MODE, false>(x[k0], x[k1], tw[j], q, q2, qinv0, nf);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < E; k++) gsm[S::LINEAR ? s0 + k * st : slot<B, PADL>(l0 | (k << w))] = u128_to(x[k]);
+    if (WARPSYNC) __syncwarp(); else __syncthreads();
+}
+
 template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL>
 __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
                                             const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
@@ -321,56 +388,18 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
         q2[3] = (q[3] << 1) | (q[2] >> 31);
     }
     using S = PassShape<B, RBMAX, C, PADL>;
-    constexpr int RB = S::RB, E = S::E;
+    int rd0 = 0;
+    if (FIRST) {
+        round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, true>(0, gsm, tws, t, lo, n, q, q2, qinv0, nf);
+        rd0 = 1;
+    }
 #if NTT_UNROLL_ROUNDS
 #pragma unroll
 #else
 #pragma unroll 1
 #endif
-    for (int rd = 0; rd < S::ROUNDS; rd++) {
-        const int slo = rd * RB;
-        const int w = (slo + RB <= B) ? slo : B - RB;   // E-element window [w, w + RB)
-        const int tlo = t & ((1 << w) - 1);
-        const int l0 = ((t >> w) << (w + RB)) | tlo;    // element k of this thread: l0 + (k << w)
-        const int s0 = S::LINEAR ? slot<B, PADL>(l0) : 0;
-        const int st = S::LINEAR ? (w >= 3 ? (9 << (w - 3)) : (1 << w)) : 0;
-        U128 x[E];
-#pragma unroll
-        for (int k = 0; k < E; k++)
-            x[k] = u128_from(gsm[S::LINEAR ? s0 + k * st : slot<B, PADL>(l0 | (k << w))]);
-#pragma unroll
-        for (int bit = 0; bit < RB; bit++) {
-            const int sl = w + bit;                      // local stage
-            if (sl < slo) continue;                      // overlap of the last window
-            const bool trivial = FIRST && sl == 0 && !(SCALE_LAST && n == 1);
-            const bool last = SCALE_LAST && lo + sl == n - 1;
-            if (trivial) {
-#pragma unroll
-                for (int kk = 0; kk < E / 2; kk++) {
-                    const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
-                    const int k1 = k0 | (1 << bit);
-                    bfly1<MODE>(x[k0], x[k1], q);
-                }
-            } else {
-                const uint4* tp = tws + tlo + ((1 << sl) - 1);
-                U128 tw[E / 2];                          // the first 2^bit are used
-#pragma unroll
-                for (int j = 0; j < (1 << bit); j++) tw[j] = u128_from(tp[j << w]);
-#pragma unroll
-                for (int kk = 0; kk < E / 2; kk++) {
-                    const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
-                    const int k1 = k0 | (1 << bit);
-                    const U128& wv = tw[kk & ((1 << bit) - 1)];
-                    if (last) bfly<MODE, true>(x[k0], x[k1], wv, q, q2, qinv0, nf);
-                    else bfly<MODE, false>(x[k0], x[k1], wv, q, q2, qinv0, nf);
-                }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < E; k++)
-            gsm[S::LINEAR ? s0 + k * st : slot<B, PADL>(l0 | (k << w))] = u128_to(x[k]);
-        if (WARPSYNC) __syncwarp(); else __syncthreads();
-    }
+    for (int rd = rd0; rd < S::ROUNDS; rd++)
+        round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf);
 }
 
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX>
@@ -1369,6 +1398,10 @@ static ntt128_status stream_scratch(ntt128_plan_s* p, cudaStream_t stream, uint4
 // polynomial; every pass but the last signals row i.
 static void set_overlap(ntt128_plan_s* p, ntt128_plan_s::StreamCtr* ctr, PassArgs& a, size_t i, size_t npass,
                         uint32_t prev_ctas_per_poly) {
+    if (getenv("NTT128_PDL_NOCNT")) {   // experiment: whole-grid dependencies only
+        a.pdl_wait = 1u;
+        return;
+    }
     a.pdl_wait = i == 0 ? 1u : 0u;
     if (i > 0) {
         ctr->expected[i - 1] += prev_ctas_per_poly;
