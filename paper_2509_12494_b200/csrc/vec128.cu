@@ -9,9 +9,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/ntt128.h"
 #include "arith128.cuh"
+#include "barrett128.cuh"
 #include "host128.h"
 
 using namespace ntt128;
@@ -26,9 +28,18 @@ struct VecConst {
     uint32_t qinv0;
     uint32_t a_m[4];  // axpy scalar, Montgomery form
     uint32_t r2[4];   // R^2 mod q
+    BarrettC bc;      // q and mu' = floor(2^256 / q) - 2^128 (OP_MULB: q > 2^127)
 };
 
-enum Op { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_AXPY = 3 };
+// OP_MUL: two Montgomery products (any odd q); OP_MULB: one Barrett product (q > 2^127,
+// 43 word products instead of 72: barrett128.cuh).
+enum Op { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_AXPY = 3, OP_MULB = 4 };
+
+__device__ __forceinline__ U128 mul_b(const U128& a, const U128& b, const BarrettC& bc) {
+    U128 r;
+    barrett_mul_dev(a.w, b.w, bc, r.w);
+    return r;
+}
 
 constexpr int UNROLL = 4;
 constexpr int THREADS = 256;
@@ -51,6 +62,7 @@ __global__ void __launch_bounds__(THREADS) k_vec(uint4* z, const uint4* __restri
             if (OPK == OP_ADD) r = add_mod(a, b, c.q);
             else if (OPK == OP_SUB) r = sub_mod(a, b, c.q);
             else if (OPK == OP_MUL) r = mont_mul(mont_mul(a, b, c.q, c.qinv0), U128{{c.r2[0], c.r2[1], c.r2[2], c.r2[3]}}, c.q, c.qinv0);
+            else if (OPK == OP_MULB) r = mul_b(a, b, c.bc);
             else r = add_mod(mont_mul(a, U128{{c.a_m[0], c.a_m[1], c.a_m[2], c.a_m[3]}}, c.q, c.qinv0), b, c.q);
             z[i + u * stride] = u128_to(r);
         }
@@ -60,6 +72,7 @@ __global__ void __launch_bounds__(THREADS) k_vec(uint4* z, const uint4* __restri
         if (OPK == OP_ADD) r = add_mod(a, b, c.q);
         else if (OPK == OP_SUB) r = sub_mod(a, b, c.q);
         else if (OPK == OP_MUL) r = mont_mul(mont_mul(a, b, c.q, c.qinv0), U128{{c.r2[0], c.r2[1], c.r2[2], c.r2[3]}}, c.q, c.qinv0);
+        else if (OPK == OP_MULB) r = mul_b(a, b, c.bc);
         else r = add_mod(mont_mul(a, U128{{c.a_m[0], c.a_m[1], c.a_m[2], c.a_m[3]}}, c.q, c.qinv0), b, c.q);
         z[i] = u128_to(r);
     }
@@ -81,7 +94,8 @@ int grid_for(uint64_t n) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint64_t want = (n + (uint64_t)THREADS * UNROLL - 1) / ((uint64_t)THREADS * UNROLL);
-    uint64_t cap = (uint64_t)sms * 8;  // 8 resident 256-thread CTAs per SM
+    static const int per_sm = getenv("NTT128_VEC_CTAS_PER_SM") ? atoi(getenv("NTT128_VEC_CTAS_PER_SM")) : 8;
+    uint64_t cap = (uint64_t)sms * per_sm;  // resident 256-thread CTAs per SM
     if (want > cap) want = cap;
     return want < 1 ? 1 : (int)want;
 }
@@ -106,6 +120,22 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
         if (a >= q) return NTT128_ERR_INPUT_RANGE;
     }
     words(M.to_m(a), c.a_m);
+    const bool barrett = (q >> 127) != 0 && getenv("NTT128_NO_BARRETT") == nullptr;
+    if (barrett) {
+        // mu = floor((2^256 - 1) / q) (= floor(2^256 / q), q odd) by restoring division
+        u128 rem = 0, quo_lo = 0;
+        uint32_t quo_hi = 0;   // quotient bit 128
+        for (int i = 255; i >= 0; i--) {
+            const bool top = (rem >> 127) != 0;
+            rem = (rem << 1) | 1;
+            quo_hi = (uint32_t)((quo_hi << 1) | (uint32_t)(quo_lo >> 127));
+            quo_lo <<= 1;
+            if (top || rem >= q) { rem -= q; quo_lo |= 1; }
+        }
+        (void)quo_hi;   // == 1 for 2^127 < q < 2^128: mu = 2^128 + quo_lo
+        words(q, c.bc.q);
+        words(quo_lo, c.bc.mu);
+    }
     const uint4* x = (const uint4*)d_x;
     const uint4* y = (const uint4*)d_y;
     uint4* z = (uint4*)d_z;
@@ -125,7 +155,10 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
     switch (op) {
         case OP_ADD: k_vec<OP_ADD><<<grid, THREADS, 0, stream>>>(z, x, y, n, c); break;
         case OP_SUB: k_vec<OP_SUB><<<grid, THREADS, 0, stream>>>(z, x, y, n, c); break;
-        case OP_MUL: k_vec<OP_MUL><<<grid, THREADS, 0, stream>>>(z, x, y, n, c); break;
+        case OP_MUL:
+            if (barrett) k_vec<OP_MULB><<<grid, THREADS, 0, stream>>>(z, x, y, n, c);
+            else k_vec<OP_MUL><<<grid, THREADS, 0, stream>>>(z, x, y, n, c);
+            break;
         default: k_vec<OP_AXPY><<<grid, THREADS, 0, stream>>>(z, x, y, n, c); break;
     }
     ntt128_count_launch(1);

@@ -92,3 +92,26 @@ def test_errors(N, params):
     assert N._L.vec128_add(0, 0, 0, 0, N._pairs([q]), 0, None) == 0      # n == 0 is a no-op
     with pytest.raises(N.NTT128ArgError, match="INPUT_RANGE"):
         N.axpy(q, x, x.clone(), q)                                     # scalar a >= q
+
+
+@pytest.mark.parametrize("q", [(1 << 127) + 29, (1 << 128) - 159, 0xBFFFFFFFFFFFFFFFFFFFFFFFFFFFFFF3])
+def test_vmul_barrett_hard_cases(N, q):
+    """vec128_mul on q > 2^127 runs the Barrett product (csrc/barrett128.cuh): operands whose
+    product lies just below / at / above a multiple of q exercise every correction count"""
+    import random
+    rng = random.Random(q & 0xFFFFF)
+    a, b = [], []
+    for _ in range(3000):
+        x = rng.randrange(1, q)
+        t = rng.randrange(1, q)
+        y = (t * pow(x, -1, q)) % q
+        for d in (-1, 0, 1):
+            a.append(x)
+            b.append((y + d) % q)
+    for _ in range(3000):
+        a.append(rng.randrange(q))
+        b.append(rng.randrange(q))
+    x, y = synth.from_ints(a), synth.from_ints(b)
+    got = synth.to_ints(to_host(N.vmul(to_dev(x), to_dev(y), q)))
+    assert got == [(u * v) % q for u, v in zip(a, b)]
+    assert np.array_equal(to_host(N.vmul(to_dev(x), to_dev(y), q)), O.vmul(x, y, q))
