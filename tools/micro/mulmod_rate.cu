@@ -3,14 +3,18 @@
 // A: word-serial Montgomery (CIOS), 32-bit digits, R = 2^128.
 // B: Montgomery SOS: full 256-bit product, m = lo128(t*q'), t + m*q.
 // C: Shoup with an exact bit 128 of the remainder (r in [0, 2q) may exceed 2^128).
+// D: the product code: arith128.cuh mont_mul (even/odd alternating CIOS), mont_mul_lazy,
+//    and barrett128.cuh barrett_mul_dev (general a b mod q, no Montgomery form).
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <vector>
 #include <algorithm>
+#include "../../paper_2509_12494_b200/csrc/arith128.cuh"
+#include "../../paper_2509_12494_b200/csrc/barrett128.cuh"
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
 
-struct C128 { uint32_t q[4]; uint32_t qinv0; uint32_t qp[4]; };
+struct C128 { uint32_t q[4]; uint32_t qinv0; uint32_t qp[4]; ntt128::BarrettC bc; };
 
 // ---------- A: CIOS
 __device__ __forceinline__ void mont_cios(uint32_t r[4], const uint32_t a[4], const uint32_t b[4], const uint32_t q[4], uint32_t qinv0) {
@@ -194,7 +198,12 @@ __global__ void k_mulmod(uint4* io, const C128 c, int iters, long long* cyc) {
     for (int k = 0; k < ILP; k++) {
       if (V == 0) mont_cios(x[k], x[k], w, c.q, c.qinv0);
       else if (V == 1) mont_sos(x[k], x[k], w, c.q, c.qp);
-      else mont_eo(x[k], x[k], w, c.q, c.qinv0);
+      else if (V == 2) mont_eo(x[k], x[k], w, c.q, c.qinv0);
+      else if (V == 3) { ntt128::U128 a{{x[k][0], x[k][1], x[k][2], x[k][3]}}, b{{w[0], w[1], w[2], w[3]}};
+                         ntt128::U128 r = ntt128::mont_mul(a, b, c.q, c.qinv0); for (int i = 0; i < 4; i++) x[k][i] = r.w[i]; }
+      else if (V == 4) { ntt128::U128 a{{x[k][0], x[k][1], x[k][2], x[k][3]}}, b{{w[0], w[1], w[2], w[3]}};
+                         ntt128::U128 r = ntt128::mont_mul_lazy(a, b, c.q, c.qinv0); for (int i = 0; i < 4; i++) x[k][i] = r.w[i]; }
+      else { uint32_t r[4]; ntt128::barrett_mul_dev(x[k], w, c.bc, r); for (int i = 0; i < 4; i++) x[k][i] = r[i]; }
     }
   }
   long long t1 = clock64();
@@ -210,16 +219,29 @@ int main() {
   unsigned __int128 inv = 1; for (int i = 0; i < 7; i++) inv *= 2 - q * inv;  // Newton: q*inv == 1 mod 2^128
   unsigned __int128 qp = -inv;
   C128 c; for (int i = 0; i < 4; i++) { c.q[i] = (uint32_t)(q >> (32 * i)); c.qp[i] = (uint32_t)(qp >> (32 * i)); }
+  {   // Barrett mu' = floor(2^256 / q) - 2^128 (q > 2^127), restoring division
+    unsigned __int128 rem = 0, quo = 0;
+    for (int i = 255; i >= 0; i--) { bool top = (rem >> 127) != 0; rem = (rem << 1) | 1; quo <<= 1; if (top || rem >= q) { rem -= q; quo |= 1; } }
+    for (int i = 0; i < 4; i++) { c.bc.q[i] = c.q[i]; c.bc.mu[i] = (uint32_t)(quo >> (32 * i)); }
+  }
   c.qinv0 = c.qp[0];
   const int threads = 256, blocks = sms * 4, iters = 512, ILP = 4;
   size_t n = (size_t)threads * blocks * ILP;
   std::vector<uint4> h(n); for (size_t i = 0; i < n; i++) h[i] = make_uint4(i * 2654435761u, i, 77, 0x7fffffff);
   uint4* d; long long* dc; CK(cudaMalloc(&d, n * 16)); CK(cudaMalloc(&dc, blocks * 8));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const char* names[3] = {"mont_cios", "mont_sos", "mont_eo"};
-  for (int v = 0; v < 3; v++) {
+  const char* names[6] = {"mont_cios", "mont_sos", "mont_eo", "product_mont_mul", "product_mont_mul_lazy", "product_barrett"};
+  for (int v = 0; v < 6; v++) {
     CK(cudaMemcpy(d, h.data(), n * 16, cudaMemcpyHostToDevice));
-    auto launch = [&]() { if (v == 0) k_mulmod<0><<<blocks, threads>>>(d, c, iters, dc); else if (v == 1) k_mulmod<1><<<blocks, threads>>>(d, c, iters, dc); else k_mulmod<2><<<blocks, threads>>>(d, c, iters, dc); };
+    auto launch = [&]() {
+      switch (v) {
+        case 0: k_mulmod<0><<<blocks, threads>>>(d, c, iters, dc); break;
+        case 1: k_mulmod<1><<<blocks, threads>>>(d, c, iters, dc); break;
+        case 2: k_mulmod<2><<<blocks, threads>>>(d, c, iters, dc); break;
+        case 3: k_mulmod<3><<<blocks, threads>>>(d, c, iters, dc); break;
+        case 4: k_mulmod<4><<<blocks, threads>>>(d, c, iters, dc); break;
+        default: k_mulmod<5><<<blocks, threads>>>(d, c, iters, dc); break;
+      } };
     for (int w = 0; w < 3; w++) launch();
     CK(cudaDeviceSynchronize());
     float best = 1e30f;
