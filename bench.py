@@ -465,39 +465,50 @@ def run_rows(args, P, pk, stream):
 
 def run_cfg5_fourstep(args, P, rank, world):
     """cfg 5: one N = 2^26 forward + inverse NTT as a four-step (2^13 x 2^13) transform
-    partitioned over the `world` ranks with one all-to-all per direction (SURVEY.md §8(e));
-    every rank holds N/G coefficients (columns layout), timing = max over ranks."""
+    partitioned over the `world` ranks; every rank holds N/G coefficients
+    (columns layout), timing = max over ranks.  Two transports: "nccl" (pack, one NCCL
+    all-to-all per direction, unpack) and "p2p" (the pack kernel stores
+    each block straight into its destination rank's symmetric-memory receive buffer)."""
     import torch
     from paper_2509_12494_b200 import fourstep as FS
     from paper_2509_12494_b200 import synth
     e = P["cfg5"]
     q, w = hexint(e["q"]), hexint(e["omega"])
-    group = None
-    fs = FS.FourStep(26, q, w, rank, world, group)
-    L = fs.local
-    cols = to_dev(synth.uniform_residues(q, L.R1 * L.n2, synth.stream_seed(5, 0, 100 + rank)).reshape(L.R1, L.n2, 2))
-    rows = torch.empty((L.R2, L.n1, 2), dtype=cols.dtype, device=cols.device)
-    back = torch.empty_like(cols)
-    for _ in range(2):
-        fs.forward(cols, out=rows)
-        fs.inverse(rows, out=back)
-    torch.cuda.synchronize()
-    assert torch.equal(back, cols), "cfg5 four-step round trip mismatch"
-    iters = 5
-    barrier(world)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(iters):
-        fs.forward(cols, out=rows)
-        fs.inverse(rows, out=back)
-    e1.record()
-    e1.synchronize()
-    ms = max_over_ranks(e0.elapsed_time(e1) / iters, world)
-    bfly = 2 * (1 << 25) * 26
-    return {"cfg5_fourstep_gpus": world, "cfg5_fourstep_fwd_inv_ms": ms,
-            "cfg5_fourstep_butterflies_per_s": bfly / (ms * 1e-3),
-            "cfg5_fourstep_a2a_bytes_per_rank_per_direction": 16 * L.R1 * L.R2 * (world - 1)}
+    out = {"cfg5_fourstep_gpus": world}
+    for transport in ("nccl", "p2p"):
+        try:
+            fs = FS.FourStep(26, q, w, rank, world, None, transport=transport)
+        except Exception as ex:                      # no peer mappings on this box
+            out[f"cfg5_fourstep_{transport}_unavailable"] = str(ex).splitlines()[0][:200]
+            continue
+        L = fs.local
+        cols = to_dev(synth.uniform_residues(q, L.R1 * L.n2, synth.stream_seed(5, 0, 100 + rank)).reshape(L.R1, L.n2, 2))
+        rows = torch.empty((L.R2, L.n1, 2), dtype=cols.dtype, device=cols.device)
+        back = torch.empty_like(cols)
+        for _ in range(2):
+            fs.forward(cols, out=rows)
+            fs.inverse(rows, out=back)
+        torch.cuda.synchronize()
+        assert torch.equal(back, cols), f"cfg5 four-step ({transport}) round trip mismatch"
+        iters = 5
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fs.forward(cols, out=rows)
+            fs.inverse(rows, out=back)
+        e1.record()
+        e1.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1) / iters, world)
+        bfly = 2 * (1 << 25) * 26
+        tag = "cfg5_fourstep" if transport == "nccl" else "cfg5_fourstep_p2p"
+        out[f"{tag}_fwd_inv_ms"] = ms
+        out[f"{tag}_butterflies_per_s"] = bfly / (ms * 1e-3)
+        if transport == "nccl":
+            out["cfg5_fourstep_a2a_bytes_per_rank_per_direction"] = 16 * L.R1 * L.R2 * (world - 1)
+        del fs, cols, rows, back
+    return out
 
 
 # ----------------------------------------------------------------------------- oracle legs

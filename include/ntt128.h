@@ -171,6 +171,18 @@ ntt128_status ntt128_fourstep_inverse_a(const ntt128_fourstep_t fs, const uint64
 /* inverse, after the exchange: recv [G][R2][R1] -> X_g (columns) */
 ntt128_status ntt128_fourstep_inverse_c(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_cols,
                                         ntt128_stream_t stream);
+/* Fused exchange: pass A whose twiddle + pack kernel stores block h
+ * straight into rank h's receive buffer instead of a local send buffer -- the layout
+ * ntt128_fourstep_*_c expects, as if the all-to-all had run.  peers: host array of `world`
+ * device pointers, peers[h] = rank h's [G][R1][R2] (forward) / [G][R2][R1] (inverse)
+ * receive buffer mapped into this process (peer memory over NVLink/NVSwitch, e.g. torch
+ * symmetric memory; peers[rank] is the local one).  The caller orders the writes: a
+ * barrier across ranks before the call (every peer is done reading its receive buffer)
+ * and after it (every block has landed) before pass C.  world <= 64. */
+ntt128_status ntt128_fourstep_forward_a_peers(const ntt128_fourstep_t fs, const uint64_t *d_cols,
+                                              const uint64_t *const *peers, ntt128_stream_t stream);
+ntt128_status ntt128_fourstep_inverse_a_peers(const ntt128_fourstep_t fs, const uint64_t *d_rows,
+                                              const uint64_t *const *peers, ntt128_stream_t stream);
 void ntt128_fourstep_destroy(ntt128_fourstep_t fs);
 
 /* Human-readable name of a status code (static storage). */

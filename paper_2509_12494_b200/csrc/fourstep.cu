@@ -51,6 +51,29 @@ __global__ void k_fs_twiddle_pack(const uint4* __restrict__ z, uint4* __restrict
     }
 }
 
+// Fused exchange: the same twiddle + pack, but block h is stored straight
+// into rank h's receive buffer (peer memory over NVLink / NVSwitch), at the offset the
+// all-to-all would have put it: recv_h[(src * R + r) * CG + cc].  One HBM round trip and
+// the collective disappear; the transfer overlaps the twiddle multiplications.
+#define NTT128_FS_MAX_PEERS 64
+struct FsPeers {
+    uint4* p[NTT128_FS_MAX_PEERS];
+};
+__global__ void k_fs_twiddle_pack_peers(const uint4* __restrict__ z, const FsPeers peers, uint32_t R, uint32_t C,
+                                        uint32_t G, uint32_t src, uint64_t row0, const uint4* __restrict__ TH,
+                                        const uint4* __restrict__ TL, uint32_t s, uint64_t nmask, const FsConst k) {
+    const uint32_t CG = C / G;
+    const uint64_t total = (uint64_t)R * C;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = i / C, c = i - r * C;
+        const uint64_t e = ((row0 + r) * c) & nmask;
+        const U128 w = mont_mul(u128_from(__ldg(TH + (e >> s))), u128_from(__ldg(TL + (e & ((1ull << s) - 1)))), k.q, k.qinv0);
+        const U128 v = mont_mul(u128_from(z[i]), w, k.q, k.qinv0);
+        const uint64_t h = c / CG, cc = c - h * CG;
+        peers.p[h][((uint64_t)src * R + r) * CG + cc] = u128_to(v);
+    }
+}
+
 // out[K][M] = transpose(in[M][K]) through 32 x 32 shared-memory tiles of 16-byte elements
 __global__ void k_fs_transpose(const uint4* __restrict__ in, uint4* __restrict__ out, uint32_t M, uint32_t K) {
     __shared__ uint4 tile[32][33];
@@ -194,6 +217,25 @@ ntt128_status pack(const ntt128_fourstep_s* f, const uint4* z, uint4* send, uint
     return cudaGetLastError() == cudaSuccess ? NTT128_OK : NTT128_ERR_CUDA;
 }
 
+ntt128_status pack_peers(const ntt128_fourstep_s* f, const uint4* z, const uint64_t* const* peers, uint32_t R, uint32_t C,
+                         uint64_t row0, bool inverse, cudaStream_t st) {
+    if (f->world > NTT128_FS_MAX_PEERS) return NTT128_ERR_UNSUPPORTED;
+    FsPeers pp;
+    memset(&pp, 0, sizeof(pp));
+    for (uint32_t h = 0; h < f->world; h++) {
+        if (!peers[h]) return NTT128_ERR_INVALID_ARG;
+        if (!al16(peers[h])) return NTT128_ERR_ALIGNMENT;
+        pp.p[h] = (uint4*)peers[h];
+    }
+    const uint64_t total = (uint64_t)R * C;
+    unsigned g = (unsigned)((total + 255) / 256);
+    if (g > 148 * 8) g = 148 * 8;
+    k_fs_twiddle_pack_peers<<<g, 256, 0, st>>>(z, pp, R, C, f->world, f->rank, row0, inverse ? f->d_THi : f->d_TH,
+                                               inverse ? f->d_TLi : f->d_TL, f->s, f->N - 1, f->k);
+    ntt128_count_launch(1);
+    return cudaGetLastError() == cudaSuccess ? NTT128_OK : NTT128_ERR_CUDA;
+}
+
 ntt128_status transpose(const uint4* in, uint4* out, uint64_t M, uint64_t K, cudaStream_t st) {
     dim3 grid((unsigned)((K + 31) / 32), (unsigned)((M + 31) / 32)), block(32, 8);
     k_fs_transpose<<<grid, block, 0, st>>>(in, out, (uint32_t)M, (uint32_t)K);
@@ -244,4 +286,28 @@ extern "C" ntt128_status ntt128_fourstep_inverse_c(const ntt128_fourstep_t f, co
     ntt128_status r = transpose((const uint4*)d_recv, f->d_tmp, f->n2, f->R1, (cudaStream_t)s);   // [R1][n2]
     if (r != NTT128_OK) return r;
     return ntt128_inverse(f->p2, (const uint64_t*)f->d_tmp, d_cols, s);                      // x columns, / n2
+}
+
+// Fused-exchange pass A (include/ntt128.h): peers[h] = rank h's receive buffer, mapped in
+// this process (e.g. torch symmetric memory); the caller brackets the call with barriers.
+extern "C" ntt128_status ntt128_fourstep_forward_a_peers(const ntt128_fourstep_t f, const uint64_t* d_cols,
+                                                         const uint64_t* const* peers, ntt128_stream_t s) {
+    if (!f || !d_cols || !peers) return NTT128_ERR_INVALID_ARG;
+    if (!al16(d_cols)) return NTT128_ERR_ALIGNMENT;
+    Guard g(f->device);
+    ntt128_status r = ntt128_forward(f->p2, d_cols, (uint64_t*)f->d_tmp, s);
+    if (r != NTT128_OK) return r;
+    return pack_peers(f, f->d_tmp, peers, (uint32_t)f->R1, (uint32_t)f->n2, (uint64_t)f->rank * f->R1, false,
+                      (cudaStream_t)s);
+}
+
+extern "C" ntt128_status ntt128_fourstep_inverse_a_peers(const ntt128_fourstep_t f, const uint64_t* d_rows,
+                                                         const uint64_t* const* peers, ntt128_stream_t s) {
+    if (!f || !d_rows || !peers) return NTT128_ERR_INVALID_ARG;
+    if (!al16(d_rows)) return NTT128_ERR_ALIGNMENT;
+    Guard g(f->device);
+    ntt128_status r = ntt128_inverse(f->p1, d_rows, (uint64_t*)f->d_tmp, s);
+    if (r != NTT128_OK) return r;
+    return pack_peers(f, f->d_tmp, peers, (uint32_t)f->R2, (uint32_t)f->n1, (uint64_t)f->rank * f->R2, true,
+                      (cudaStream_t)s);
 }

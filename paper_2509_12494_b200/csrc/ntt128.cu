@@ -918,14 +918,17 @@ static bool use_latency_shape(int B, uint32_t batch) {
     return ((uint64_t)batch + d.C - 1) / d.C < (uint64_t)NTT_LAT_CTAS;
 }
 // Multi-pass: first pass (gather, stage 0), middle passes, last pass (optionally scaled).
+// `wide`: rows of the pass are >= 2^NTT_WIDE_STRIDE elements apart; a one-group CTA then
+// reads 16-byte pieces of rows megabytes apart, so 8- and 9-stage passes take 4 adjacent
+// groups per CTA (64-byte row segments; N = 2^26: 12.1 -> 10.3 ms, tools/exp_large.py).
 template <bool FIRST, bool SL>
-static PassCfg multi_cfg_t(int B) {
+static PassCfg multi_cfg_t(int B, bool wide) {
     switch (B) {
         case 5: return make_cfg<5, NTT_C5, FIRST, SL>();
         case 6: return make_cfg<6, NTT_C6, FIRST, SL>();
         case 7: return make_cfg<7, NTT_C7, FIRST, SL>();
-        case 8: return make_cfg<8, NTT_C8, FIRST, SL, false, NTT_RB8>();
-        default: return make_cfg<9, NTT_C9, FIRST, SL>();
+        case 8: return wide ? make_cfg<8, 4, FIRST, SL, false, NTT_RB8>() : make_cfg<8, NTT_C8, FIRST, SL, false, NTT_RB8>();
+        default: return wide ? make_cfg<9, 4, FIRST, SL>() : make_cfg<9, NTT_C9, FIRST, SL>();
     }
 }
 // Permutation-free negacyclic passes (B in [5, 8], warp-owned groups).
@@ -962,11 +965,16 @@ static std::vector<int> nc_pass_bits(int n) {
     return b;
 }
 
-static PassCfg pass_cfg(size_t npass, size_t i, int B, bool scale_last) {
+#ifndef NTT_WIDE_STRIDE
+#define NTT_WIDE_STRIDE 17
+#endif
+// lo = index bits below the pass (0 for the first pass); n = log2 N
+static PassCfg pass_cfg(size_t npass, size_t i, int B, bool scale_last, int lo = 0, int n = 0) {
     if (npass == 1) return scale_last ? single_cfg_t<true>(B) : single_cfg_t<false>(B);
-    if (i == 0) return multi_cfg_t<true, false>(B);
-    if (i + 1 == npass && scale_last) return multi_cfg_t<false, true>(B);
-    return multi_cfg_t<false, false>(B);
+    const bool wide = (i == 0 ? n - B : lo) >= NTT_WIDE_STRIDE;   // row stride of the pass, log2 elements
+    if (i == 0) return multi_cfg_t<true, false>(B, wide);
+    if (i + 1 == npass && scale_last) return multi_cfg_t<false, true>(B, wide);
+    return multi_cfg_t<false, false>(B, wide);
 }
 
 // ----------------------------------------------------------------------------- plan
@@ -1195,7 +1203,9 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
     if (st == NTT128_OK) {
         for (size_t i = 0; i < p->bits.size(); i++) {
             for (int sl = 0; sl < 2; sl++) {
-                PassCfg c = pass_cfg(p->bits.size(), i, p->bits[i], sl == 1);
+                int lo_i = 0;
+                for (size_t k = 0; k < i; k++) lo_i += p->bits[k];
+                PassCfg c = pass_cfg(p->bits.size(), i, p->bits[i], sl == 1, lo_i, (int)log2n);
                 if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
                     st = NTT128_ERR_CUDA;
                 if (p->bits.size() == 1 && use_latency_shape(p->bits[i], batch)) {
@@ -1432,7 +1442,7 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
     uint32_t prev_ctas_per_poly = 0;
     for (size_t i = 0; i < npass; i++) {
         const int B = p->bits[i];
-        PassCfg c = pass_cfg(npass, i, B, scale_last);
+        PassCfg c = pass_cfg(npass, i, B, scale_last, lo, n);
         if (npass == 1 && use_latency_shape(B, p->batch))
             c = scale_last ? single_lat_cfg_t<true>(B) : single_lat_cfg_t<false>(B);
         PassArgs a;

@@ -28,6 +28,9 @@ for _name in ("ntt128_fourstep_forward_a", "ntt128_fourstep_forward_c", "ntt128_
               "ntt128_fourstep_inverse_c"):
     getattr(_L, _name).argtypes = [_vp, _vp, _vp, _vp]
     getattr(_L, _name).restype = ctypes.c_int
+for _name in ("ntt128_fourstep_forward_a_peers", "ntt128_fourstep_inverse_a_peers"):
+    getattr(_L, _name).argtypes = [_vp, _vp, ctypes.POINTER(ctypes.c_uint64), _vp]
+    getattr(_L, _name).restype = ctypes.c_int
 _L.ntt128_fourstep_destroy.argtypes = [_vp]
 _L.ntt128_fourstep_destroy.restype = None
 
@@ -98,6 +101,19 @@ class FourStepLocal:
     def inverse_c(self, recv, cols):
         return self._call("ntt128_fourstep_inverse_c", recv, cols)
 
+    def _call_peers(self, name, a, peer_ptrs):
+        if len(peer_ptrs) != self.world:
+            raise ValueError(f"{name}: need {self.world} peer pointers, got {len(peer_ptrs)}")
+        arr = (ctypes.c_uint64 * self.world)(*[int(p) for p in peer_ptrs])
+        _n._check(getattr(_L, name)(self._h, _n._ptr(a, "in"), arr, _n._stream(a)), name)
+
+    def forward_a_peers(self, cols, peer_ptrs):
+        """pass A with the exchange fused: block h lands in peer_ptrs[h] (rank h's recv buffer)"""
+        self._call_peers("ntt128_fourstep_forward_a_peers", cols, peer_ptrs)
+
+    def inverse_a_peers(self, rows, peer_ptrs):
+        self._call_peers("ntt128_fourstep_inverse_a_peers", rows, peer_ptrs)
+
     def close(self):
         if self._h is not None:
             _L.ntt128_fourstep_destroy(self._h)
@@ -122,28 +138,71 @@ def exchange(send, group=None, world: int = 1):
 
 
 class FourStep:
-    """Distributed forward / inverse of one N-point transform; call on every rank."""
+    """Distributed forward / inverse of one N-point transform; call on every rank.
+
+    transport="nccl": pass A packs into a local send buffer, one all-to-all moves the
+    blocks, pass C reads the received copy.  transport="p2p": the receive
+    buffer is symmetric memory (torch.distributed._symmetric_memory, NVLink peer mappings)
+    and pass A's pack kernel stores every block straight into its destination rank's
+    receive buffer; two device-side barriers order the writes (before: every peer has
+    finished reading its buffer; after: every block has landed).  No collective moves data.
+    """
 
     def __init__(self, log2n: int, q: int, omega: int, rank: int = 0, world: int = 1, group=None,
-                 device: int | None = None, local=None):
+                 device: int | None = None, local=None, transport: str = "nccl"):
         # `local` is injectable so the exchange schedule can be exercised by CPU tests (gloo)
         self.local = local if local is not None else FourStepLocal(log2n, q, omega, rank, world, device)
         self.group, self.world = group, world
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"transport must be 'nccl' or 'p2p', not {transport!r}")
+        self.transport = transport
+        self._recv = self._hdl = None
+        if transport == "p2p":
+            self._setup_p2p()
+
+    def _setup_p2p(self):
+        import torch
+        L = self.local
+        dev = torch.device("cuda", L.device)
+        elems = L.R1 * L.n2                            # = R2 * n1 = N / G: both directions fit
+        if self.world == 1:
+            self._recv = torch.empty((elems, 2), dtype=torch.int64, device=dev)
+            self._peers = [self._recv.data_ptr()]
+            return
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        self._recv = symm_mem.empty((elems, 2), dtype=torch.int64, device=dev)
+        self._hdl = symm_mem.rendezvous(self._recv, self.group if self.group is not None else dist.group.WORLD)
+        self._peers = [int(p) for p in self._hdl.buffer_ptrs]
+
+    def _barrier(self):
+        if self._hdl is not None:
+            self._hdl.barrier(channel=0)               # device-side, ordered on the current stream
 
     def forward(self, cols, out=None):
         import torch
         L = self.local
+        out = torch.empty((L.R2, L.n1, 2), dtype=cols.dtype, device=cols.device) if out is None else out
+        if self.transport == "p2p":
+            self._barrier()
+            L.forward_a_peers(cols, self._peers)
+            self._barrier()
+            return L.forward_c(self._recv.view(self.world, L.R1, L.R2, 2), out)
         send = torch.empty((self.world, L.R1, L.R2, 2), dtype=cols.dtype, device=cols.device)
         L.forward_a(cols, send)
         recv = exchange(send, self.group, self.world)
-        out = torch.empty((L.R2, L.n1, 2), dtype=cols.dtype, device=cols.device) if out is None else out
         return L.forward_c(recv, out)
 
     def inverse(self, rows, out=None):
         import torch
         L = self.local
+        out = torch.empty((L.R1, L.n2, 2), dtype=rows.dtype, device=rows.device) if out is None else out
+        if self.transport == "p2p":
+            self._barrier()
+            L.inverse_a_peers(rows, self._peers)
+            self._barrier()
+            return L.inverse_c(self._recv.view(self.world, L.R2, L.R1, 2), out)
         send = torch.empty((self.world, L.R2, L.R1, 2), dtype=rows.dtype, device=rows.device)
         L.inverse_a(rows, send)
         recv = exchange(send, self.group, self.world)
-        out = torch.empty((L.R1, L.n2, 2), dtype=rows.dtype, device=rows.device) if out is None else out
         return L.inverse_c(recv, out)

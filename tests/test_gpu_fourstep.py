@@ -50,6 +50,58 @@ def virtual_run(FS, log2n, q, w, x, world):
     return y, FS.from_columns(cols, n1, n2)
 
 
+def virtual_run_peers(FS, log2n, q, w, x, world):
+    """fused exchange (ntt128_fourstep_*_a_peers): virtual rank g's pack kernel stores its
+    blocks straight into every virtual rank's receive buffer (all on this GPU); the ranks
+    run one after another, so no kernel waits on another"""
+    import torch
+    l1, l2 = FS.split(log2n)
+    n1, n2 = 1 << l1, 1 << l2
+    locs = [FS.FourStepLocal(log2n, q, w, r, world) for r in range(world)]
+    R1, R2 = n1 // world, n2 // world
+    recvs = [torch.full((world, R1, R2, 2), -1, dtype=torch.int64, device="cuda") for _ in range(world)]
+    ptrs = [t.data_ptr() for t in recvs]
+    for r, L in enumerate(locs):
+        L.forward_a_peers(to_dev(FS.to_columns(x, n1, n2, r, world)), ptrs)
+    rows = []
+    for h, L in enumerate(locs):
+        rows.append(L.forward_c(recvs[h], torch.empty((R2, n1, 2), dtype=torch.int64, device="cuda")))
+    y = FS.from_rows([to_host(t) for t in rows], n1, n2)
+    recvs = [torch.full((world, R2, R1, 2), -1, dtype=torch.int64, device="cuda") for _ in range(world)]
+    ptrs = [t.data_ptr() for t in recvs]
+    for r, L in enumerate(locs):
+        L.inverse_a_peers(rows[r], ptrs)
+    cols = [to_host(L.inverse_c(recvs[g], torch.empty((R1, n2, 2), dtype=torch.int64, device="cuda")))
+            for g, L in enumerate(locs)]
+    return y, FS.from_columns(cols, n1, n2)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("log2n", [8, 14, 20])
+def test_fourstep_fused_exchange_virtual_ranks(FS, params, log2n, world):
+    e = params["extra"]["b126"] if log2n <= 17 else params["cfg5"]   # b126: a q < 2^126 (lazy class)
+    q = e["q"]
+    w = pow(e["psi"], 1 << (e["logn"] + 1 - log2n), q)
+    x = synth.uniform_residues(q, 1 << log2n, 400 + log2n + world)
+    y, xr = virtual_run_peers(FS, log2n, q, w, x, world)
+    assert np.array_equal(y, O.ntt(x, q, w))
+    assert np.array_equal(xr, x)
+
+
+def test_fourstep_p2p_transport_single_rank(FS, params):
+    """FourStep(transport="p2p") at world 1 (the rank's own buffer is its only peer)"""
+    e = params["cfg5"]
+    q, log2n = e["q"], 16
+    w = pow(e["omega"], 1 << (26 - log2n), q)
+    x = synth.uniform_residues(q, 1 << log2n, 77)
+    l1, l2 = FS.split(log2n)
+    fs = FS.FourStep(log2n, q, w, transport="p2p")
+    rows = fs.forward(to_dev(FS.to_columns(x, 1 << l1, 1 << l2, 0, 1)))
+    assert np.array_equal(FS.from_rows([to_host(rows)], 1 << l1, 1 << l2), O.ntt(x, q, w))
+    cols = fs.inverse(rows)
+    assert np.array_equal(FS.from_columns([to_host(cols)], 1 << l1, 1 << l2), x)
+
+
 @pytest.mark.parametrize("log2n", [2, 5, 10, 16, 20])
 def test_fourstep_g1(FS, params, log2n):
     e = params["cfg5"]

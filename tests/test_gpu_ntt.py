@@ -232,3 +232,21 @@ def test_rns_many_primes_small_sizes(N, params, logn):
     b = np.stack([synth.uniform_residues(qs[i], n, 2000 * logn + i) for i in range(B)])
     c = to_host(pn.polymul(to_dev(x), to_dev(b)))
     assert np.array_equal(c, O.negacyclic_polymul(x, b, qs, psis))
+
+
+def test_cfg5_direct_three_pass(N, params):
+    """BASELINE cfg 5 size through one plan (three passes 9/9/8, rows megabytes apart so
+    the wide-stride CTA shape runs): sampled outputs by direct O(N) evaluation of Eq. ntt
+    (independent of any radix structure) and the exact round trip"""
+    import torch
+    e = params["cfg5"]
+    q, w = e["q"], e["omega"]
+    n = 1 << 26
+    x = synth.uniform_residues(q, n, synth.stream_seed(5, 0, 900)).reshape(1, n, 2)
+    plan = N.Plan(26, q, w)
+    dx = to_dev(x)
+    dy = plan.forward(dx)
+    y = to_host(dy)
+    for k in [0, 1, 2, n // 2, n - 1, 12345678, 40000001]:
+        assert synth.to_ints(y[0, k:k + 1])[0] == O.ntt_eval(x[0], q, w, k), f"y[{k}]"
+    assert torch.equal(plan.inverse(dy), dx)

@@ -1,0 +1,34 @@
+"""Experiment: forward+inverse throughput for single large polynomials (cfg5 prime),
+N = 2^n for the n given on the command line (batch fills 2^26 coefficients)."""
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2509_12494_b200 import ntt128 as N  # noqa: E402
+from paper_2509_12494_b200 import synth  # noqa: E402
+
+P = json.load(open("tests/golden/params.json"))
+e = P["cfg5"]
+q, L = int(e["q"], 16), e["logn"]
+for logn in [int(v) for v in sys.argv[1].split(",")]:
+    w = pow(int(e["omega"], 16), 1 << (L - logn), q)
+    B = (1 << 26) >> logn
+    plan = N.Plan(logn, q, w, batch=B)
+    x = torch.from_numpy(synth.uniform_residues(q, 1 << 26, logn).reshape(B, 1 << logn, 2).view(np.int64)).cuda()
+    y, z = torch.empty_like(x), torch.empty_like(x)
+    for _ in range(2):
+        plan.forward(x, out=y); plan.inverse(y, out=z)
+    torch.cuda.synchronize()
+    assert torch.equal(z, x)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        plan.forward(x, out=y); plan.inverse(y, out=z)
+    e1.record(); e1.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    print("logn %2d passes %d  %.3f ms  %.4e bfly/s" % (logn, plan.info()["num_passes"], ms, 2 * B * (1 << (logn - 1)) * logn / (ms * 1e-3)))
+    del plan, x, y, z
+    torch.cuda.empty_cache()
