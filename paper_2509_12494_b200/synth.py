@@ -120,3 +120,60 @@ def from_ints(vals, shape=None) -> np.ndarray:
 
 def int_to_pair(v: int) -> np.ndarray:
     return np.array([v & 0xFFFFFFFFFFFFFFFF, v >> 64], dtype=np.uint64)
+
+
+# ----------------------------------------------------------------------------- 256-bit residues
+def _limbs(v: int) -> list[int]:
+    return [(v >> (64 * i)) & 0xFFFFFFFFFFFFFFFF for i in range(4)]
+
+
+def uniform_residues_w(q: int, n: int, seed: int) -> np.ndarray:
+    """n residues uniform in [0, q) for q < 2^256 (the wider-modulus path):
+    four draws per candidate, most significant first, top bitlen(q) bits, rejection.
+    Returns uint64 [n, 4] (little-endian limbs)."""
+    assert 2 <= q < (1 << 256)
+    bits = q.bit_length()
+    sh = 256 - bits
+    qa = _limbs(q)
+    out = np.empty((n, 4), dtype=np.uint64)
+    filled, pos = 0, 0
+    while filled < n:
+        want = n - filled
+        m = int(want * (2.0 ** bits / q) * 1.02) + 64
+        d = splitmix64(seed, 4 * pos, 4 * m).reshape(m, 4)
+        v = [d[:, 3], d[:, 2], d[:, 1], d[:, 0]]          # little-endian limbs of the 256-bit draw
+        # v >> sh
+        w, b = sh // 64, sh % 64
+        r = []
+        for i in range(4):
+            lo = v[i + w] if i + w < 4 else np.zeros_like(v[0])
+            hi = v[i + w + 1] if i + w + 1 < 4 else np.zeros_like(v[0])
+            r.append((lo >> np.uint64(b)) | (hi << np.uint64(64 - b)) if b else lo.copy())
+        lt = np.zeros(m, dtype=bool)
+        eq = np.ones(m, dtype=bool)
+        for i in (3, 2, 1, 0):
+            qi = np.uint64(qa[i])
+            lt |= eq & (r[i] < qi)
+            eq &= r[i] == qi
+        idx = np.nonzero(lt)[0][:want]
+        for i in range(4):
+            out[filled:filled + len(idx), i] = r[i][idx]
+        filled += len(idx)
+        pos += m
+    return out
+
+
+def uniform_residue_scalar_w(q: int, seed: int, k: int = 0) -> int:
+    """The k-th accepted 256-bit-path residue of stream `seed` (plain Python)."""
+    bits = q.bit_length()
+    found, i = 0, 0
+    while True:
+        v = 0
+        for j in range(4):
+            v = (v << 64) | splitmix64_scalar(seed, 4 * i + j)
+        v >>= 256 - bits
+        i += 1
+        if v < q:
+            if found == k:
+                return v
+            found += 1
