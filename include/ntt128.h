@@ -185,6 +185,26 @@ ntt128_status ntt128_fourstep_inverse_a_peers(const ntt128_fourstep_t fs, const 
                                               const uint64_t *const *peers, ntt128_stream_t stream);
 void ntt128_fourstep_destroy(ntt128_fourstep_t fs);
 
+/* ---------------------------------------------------------------------------
+ * Wider moduli (the paper's generalisation to larger bit widths,
+ * PAPER.md:807-808).  Residues of any odd prime q < 2^256 as four little-endian uint64
+ * limbs (32 bytes); arrays [batch][N][4] uint64, 16-byte aligned.  Cyclic NTT of Eq. ntt,
+ * natural order in and out, inverse with N^{-1}; same ownership / asynchrony / error
+ * conventions as the 128-bit plans above.  log2n in [1, 24]; flags must be 0.
+ *   q_host, root_host: [n_moduli][4] uint64 (root of exact order N); n_moduli 1 or batch.
+ * Plan creation validates primality (Miller-Rabin, 20 bases), N | q - 1 and the root's
+ * order on the host (milliseconds per modulus).
+ * ------------------------------------------------------------------------- */
+typedef struct ntt256_plan_s *ntt256_plan_t;
+ntt128_status ntt256_plan_create(ntt256_plan_t *out, uint32_t log2n, uint32_t batch, const uint64_t *q_host,
+                                 const uint64_t *root_host, uint32_t n_moduli, uint32_t flags, int device);
+ntt128_status ntt256_forward(const ntt256_plan_t plan, const uint64_t *d_in, uint64_t *d_out, ntt128_stream_t stream);
+ntt128_status ntt256_inverse(const ntt256_plan_t plan, const uint64_t *d_in, uint64_t *d_out, ntt128_stream_t stream);
+void ntt256_plan_destroy(ntt256_plan_t plan);
+/* z = x * y mod q element-wise over 256-bit residues (n elements; q: 4 host limbs) */
+ntt128_status vec256_mul(uint64_t *d_z, const uint64_t *d_x, const uint64_t *d_y, size_t n, const uint64_t *q,
+                         ntt128_stream_t stream);
+
 /* Human-readable name of a status code (static storage). */
 const char *ntt128_status_string(ntt128_status s);
 

@@ -40,6 +40,16 @@ for _name in ("vec128_add", "vec128_sub", "vec128_mul"):
     getattr(_L, _name).restype = ctypes.c_int
 _L.vec128_axpy.argtypes = [_vp, _u64p, _vp, ctypes.c_size_t, _u64p, ctypes.c_uint32, _vp]
 _L.vec128_axpy.restype = ctypes.c_int
+_L.ntt256_plan_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_uint32, ctypes.c_uint32, _u64p, _u64p,
+                                  ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int]
+_L.ntt256_plan_create.restype = ctypes.c_int
+for _name in ("ntt256_forward", "ntt256_inverse"):
+    getattr(_L, _name).argtypes = [_vp, _vp, _vp, _vp]
+    getattr(_L, _name).restype = ctypes.c_int
+_L.ntt256_plan_destroy.argtypes = [_vp]
+_L.ntt256_plan_destroy.restype = None
+_L.vec256_mul.argtypes = [_vp, _vp, _vp, ctypes.c_size_t, _u64p, _vp]
+_L.vec256_mul.restype = ctypes.c_int
 _L.ntt128_status_string.argtypes = [ctypes.c_int]
 _L.ntt128_status_string.restype = ctypes.c_char_p
 _L.ntt128_launch_count.argtypes = []
@@ -54,7 +64,8 @@ EXPORTED = ("ntt128_plan_create", "ntt128_forward", "ntt128_inverse", "ntt128_fo
             "ntt128_plan_destroy", "vec128_add", "vec128_sub", "vec128_mul", "vec128_axpy",
             "ntt128_status_string", "ntt128_launch_count", "ntt128_fourstep_create", "ntt128_fourstep_forward_a",
             "ntt128_fourstep_forward_c", "ntt128_fourstep_inverse_a", "ntt128_fourstep_inverse_c",
-            "ntt128_fourstep_forward_a_peers", "ntt128_fourstep_inverse_a_peers", "ntt128_fourstep_destroy")
+            "ntt128_fourstep_forward_a_peers", "ntt128_fourstep_inverse_a_peers", "ntt128_fourstep_destroy",
+            "ntt256_plan_create", "ntt256_forward", "ntt256_inverse", "ntt256_plan_destroy", "vec256_mul")
 
 
 class NTT128Error(RuntimeError):
@@ -91,15 +102,15 @@ def _pairs(vals) -> ctypes.Array:
     return arr
 
 
-def _ptr(t: torch.Tensor, name: str) -> int:
+def _ptr(t: torch.Tensor, name: str, limbs: int = 2) -> int:
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor")
     if t.dtype not in (torch.uint64, torch.int64):
         raise TypeError(f"{name} must have dtype uint64 or int64")
-    if not t.is_contiguous() or t.shape[-1] != 2:
-        raise ValueError(f"{name} must be contiguous with a trailing limb dimension of 2")
+    if not t.is_contiguous() or t.shape[-1] != limbs:
+        raise ValueError(f"{name} must be contiguous with a trailing limb dimension of {limbs}")
     return t.data_ptr()
 
 
@@ -220,3 +231,69 @@ def axpy(a: int, x, y, q: int, check_input=False):
     _check(_L.vec128_axpy(_ptr(y, "y"), _pairs([a]), _ptr(x, "x"), x.numel() // 2, _pairs([q]),
                           FLAG_CHECK_INPUT if check_input else 0, _stream(x)), "vec128_axpy")
     return y
+
+
+# ----------------------------------------------------------------------------- 256-bit moduli
+def _limbs4(vals) -> ctypes.Array:
+    vals = list(vals)
+    arr = (ctypes.c_uint64 * (4 * len(vals)))()
+    for i, v in enumerate(vals):
+        v = int(v)
+        if v < 0 or v >> 256:
+            raise ValueError("256-bit value out of range")
+        for k in range(4):
+            arr[4 * i + k] = (v >> (64 * k)) & 0xFFFFFFFFFFFFFFFF
+    return arr
+
+
+class Plan256:
+    """ntt256_plan_create / ntt256_forward / ntt256_inverse (include/ntt128.h, "Wider moduli").
+    Tensors are contiguous CUDA int64/uint64 [..., N, 4] (four little-endian limbs)."""
+
+    def __init__(self, log2n: int, q, root, batch: int = 1, device: int | None = None):
+        qs = list(q) if isinstance(q, (list, tuple)) else [q]
+        rs = list(root) if isinstance(root, (list, tuple)) else [root]
+        if len(qs) != len(rs):
+            raise ValueError("q and root lists differ in length")
+        self.log2n, self.batch, self.N = int(log2n), int(batch), 1 << int(log2n)
+        dev = torch.cuda.current_device() if device is None else int(device)
+        h = _vp()
+        self._h = None
+        _check(_L.ntt256_plan_create(ctypes.byref(h), self.log2n, self.batch, _limbs4(qs), _limbs4(rs), len(qs), 0, dev),
+               "ntt256_plan_create")
+        self._h = h
+
+    def _shape_ok(self, t, name):
+        if t.shape[-2:] != (self.N, 4) or t.numel() != self.batch * self.N * 4:
+            raise ValueError(f"{name}: expected [{self.batch}, {self.N}, 4], got {tuple(t.shape)}")
+
+    def forward(self, x, out=None):
+        self._shape_ok(x, "x")
+        out = torch.empty_like(x) if out is None else out
+        _check(_L.ntt256_forward(self._h, _ptr(x, "x", 4), _ptr(out, "out", 4), _stream(x)), "ntt256_forward")
+        return out
+
+    def inverse(self, y, out=None):
+        self._shape_ok(y, "y")
+        out = torch.empty_like(y) if out is None else out
+        _check(_L.ntt256_inverse(self._h, _ptr(y, "y", 4), _ptr(out, "out", 4), _stream(y)), "ntt256_inverse")
+        return out
+
+    def close(self):
+        if self._h is not None:
+            _L.ntt256_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def vmul256(x, y, q: int, out=None):
+    """z = x * y mod q over 256-bit residues ([..., 4] limbs)"""
+    out = torch.empty_like(x) if out is None else out
+    _check(_L.vec256_mul(_ptr(out, "out", 4), _ptr(x, "x", 4), _ptr(y, "y", 4), x.numel() // 4, _limbs4([q]), _stream(x)),
+           "vec256_mul")
+    return out

@@ -20,12 +20,12 @@ def N():
 def declared_functions():
     src = open(os.path.join(ROOT, "include", "ntt128.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(ntt128_\w+|vec128_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b((?:ntt128|vec128|ntt256|vec256)_\w+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(N):
     names = declared_functions()
-    assert len(names) == 22, names
+    assert len(names) == 27, names
     lib = ctypes.CDLL(N.LIB_PATH)
     for name in names:
         assert hasattr(lib, name), name

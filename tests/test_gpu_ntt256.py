@@ -1,0 +1,111 @@
+"""GPU parity of the wider-modulus path (ntt256_*, vec256_mul) against
+the 256-bit oracle (oracle/oracle256.c), bit-exact: single-pass sizes, two- and three-pass
+schedules, 256/255/254/192-bit primes, several moduli per batch, structured inputs,
+in place, and the plan's argument checks."""
+import numpy as np
+import pytest
+
+from oracle import oracle256 as O4
+from paper_2509_12494_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def N():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2509_12494_b200 import ntt128
+    return ntt128
+
+
+def dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def root(e, logn):
+    return pow(e["omega"], 1 << (e["logn"] - logn), e["q"])
+
+
+def run(N, qs, ws, logn, x):
+    B = x.shape[0]
+    plan = N.Plan256(logn, qs if len(qs) > 1 else qs[0], ws if len(ws) > 1 else ws[0], batch=B)
+    dy = plan.forward(dev(x))
+    y = host(dy)
+    ref = O4.ntt(x, qs, ws, small=logn <= 6)
+    assert np.array_equal(y, ref), f"forward mismatch N=2^{logn}"
+    assert np.array_equal(host(plan.inverse(dy)), x), f"inverse mismatch N=2^{logn}"
+
+
+@pytest.mark.parametrize("logn", [1, 2, 3, 5, 8, 9, 11, 13, 16])
+def test_ntt256_sizes(N, params, logn):
+    for key in ("b256", "b192"):
+        e = params["w256"][key]
+        x = synth.uniform_residues_w(e["q"], 2 << logn, 2000 + logn).reshape(2, 1 << logn, 4)
+        run(N, [e["q"]], [root(e, logn)], logn, x)
+
+
+def test_ntt256_three_pass(N, params):
+    e = params["w256"]["b255"]
+    logn = 18                                   # 6 + 6 + 6
+    x = synth.uniform_residues_w(e["q"], 1 << logn, 2100).reshape(1, 1 << logn, 4)
+    run(N, [e["q"]], [root(e, logn)], logn, x)
+
+
+def test_ntt256_many_moduli_and_structured(N, params):
+    keys = ["b256", "b255", "b254", "b192"]
+    logn = 10
+    qs = [params["w256"][k]["q"] for k in keys]
+    ws = [root(params["w256"][k], logn) for k in keys]
+    n = 1 << logn
+    rows = [synth.uniform_residues_w(qs[0], n, 2200), O4.to_array([1] + [0] * (n - 1)),
+            O4.to_array([qs[2] - 1] * n), synth.uniform_residues_w(qs[3], n, 2201)]
+    x = np.stack(rows)
+    run(N, qs, ws, logn, x)
+    plan = N.Plan256(logn, qs, ws, batch=4)
+    y = host(plan.forward(dev(x)))
+    assert O4.to_ints(y[1]) == [1] * n                       # delta -> ones
+
+
+def test_ntt256_in_place(N, params):
+    import torch
+    e = params["w256"]["b254"]
+    logn = 12
+    x = synth.uniform_residues_w(e["q"], 1 << logn, 2300).reshape(1, 1 << logn, 4)
+    plan = N.Plan256(logn, e["q"], root(e, logn))
+    d = dev(x)
+    plan.forward(d, out=d)
+    assert np.array_equal(host(d), O4.ntt(x, e["q"], root(e, logn)))
+    plan.inverse(d, out=d)
+    assert torch.equal(d, dev(x))
+
+
+def test_vmul256(N, params):
+    for key in ("b256", "b192"):
+        q = params["w256"][key]["q"]
+        x = synth.uniform_residues_w(q, 5000, 2400)
+        y = synth.uniform_residues_w(q, 5000, 2401)
+        edge = O4.to_array([0, 1, q - 1, q - 2, (q + 1) // 2, (1 << 128) - 1, 1 << 128])
+        x = np.concatenate([x, np.repeat(edge, len(edge), axis=0)])
+        y = np.concatenate([y, np.tile(edge, (len(edge), 1))])
+        got = host(N.vmul256(dev(x), dev(y), q))
+        assert np.array_equal(got, O4.vmul(x, y, q))
+        assert O4.to_ints(got[:50]) == [a * b % q for a, b in zip(O4.to_ints(x[:50]), O4.to_ints(y[:50]))]
+
+
+def test_plan256_errors(N, params):
+    e = params["w256"]["b256"]
+    q = e["q"]
+    with pytest.raises(N.NTT128ArgError, match="INVALID_ARG"):
+        N.Plan256(25, q, root(e, 20))
+    with pytest.raises(N.NTT128ArgError, match="MODULUS"):
+        N.Plan256(4, q + 1, root(e, 4))
+    with pytest.raises(N.NTT128ArgError, match="NOT_PRIME"):
+        N.Plan256(4, q - 2, root(e, 4))
+    with pytest.raises(N.NTT128ArgError, match="BAD_ROOT"):
+        N.Plan256(4, q, root(e, 3))                            # order 8, not 16

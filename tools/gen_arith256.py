@@ -1,0 +1,151 @@
+"""Generate paper_2509_12494_b200/csrc/arith256_gen.cuh: 8-word (256-bit) modular arithmetic
+for sm_100a as inline-PTX carry chains.  The Montgomery product is the
+even/odd alternating CIOS of arith128.cuh generalised to 8 words; its carry structure is
+checked word by word by tools/model/mont_eo_model_w.py (W = 8).
+
+    python tools/gen_arith256.py        (rewrites the header; it is committed)
+"""
+import os
+
+W = 8
+H = W // 2
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2509_12494_b200", "csrc",
+                   "arith256_gen.cuh")
+
+
+def asm_block(lines, outs, ins):
+    """lines use {name} placeholders for operands; outs/ins: lists of (constraint, expr, name)"""
+    idx = {}
+    for i, (_, _, name) in enumerate(outs + ins):
+        idx[name] = f"%{i}"
+    def one(ln):
+        if ln == "{":
+            return '        "{\\n\\t"'
+        if ln == "}":
+            return '        "}"'
+        return f'        "{ln.format(**idx)};\\n\\t"'
+    body = "\n".join(one(ln) for ln in lines)
+    o = ", ".join(f'"{c}"({e})' for c, e, _ in outs)
+    i = ", ".join(f'"{c}"({e})' for c, e, _ in ins)
+    return f"    asm({body.rstrip()}\n        : {o}\n        : {i});\n"
+
+
+def gen_mont():
+    s = []
+    s.append("// Montgomery product a b 2^-256 mod q, canonical result (a < 2^256, b < q, q odd < 2^256).\n"
+             "// Even/odd alternating CIOS over 32-bit digits of b: 2^32 T_i = X + 2^32 Y, X holding the\n"
+             "// products at even word positions, Y at odd ones (register-pair aligned); after a digit\n"
+             "// X_0 = 0 and the shift is a change of roles (X' = Y + X_1, Y' = X / 2^64 + ...).  Per\n"
+             "// digit 16 IMAD.WIDE + 1 IMAD; 128 + 8 word products in all.\n")
+    s.append("__device__ __forceinline__ void mont_mul256(const uint32_t a[8], const uint32_t b[8], const uint32_t q[8],\n"
+             "                                            uint32_t qinv0, uint32_t r[8]) {\n")
+    s.append("    uint32_t x[9], y[9], n[9], m;\n")
+    # digit 0
+    lines, outs, ins = [], [], []
+    for k in range(H):
+        lines += [f"mul.lo.u32 {{x{2*k}}}, {{a{2*k}}}, {{b0}}", f"mul.hi.u32 {{x{2*k+1}}}, {{a{2*k}}}, {{b0}}",
+                  f"mul.lo.u32 {{y{2*k}}}, {{a{2*k+1}}}, {{b0}}", f"mul.hi.u32 {{y{2*k+1}}}, {{a{2*k+1}}}, {{b0}}"]
+    outs = [("=r", f"x[{i}]", f"x{i}") for i in range(W)] + [("=r", f"y[{i}]", f"y{i}") for i in range(W)]
+    ins = [("r", f"a[{i}]", f"a{i}") for i in range(W)] + [("r", "b[0]", "b0")]
+    s.append(asm_block(lines, outs, ins))
+    s.append("    m = x[0] * qinv0;\n")
+
+    def red_chain(acc, parity, fresh_top):
+        lines = []
+        for k in range(H):
+            op_lo = "mad.lo.cc.u32" if k == 0 else "madc.lo.cc.u32"
+            lines += [f"{op_lo} {{{acc}{2*k}}}, {{m}}, {{q{2*k+parity}}}, {{{acc}{2*k}}}",
+                      f"madc.hi.cc.u32 {{{acc}{2*k+1}}}, {{m}}, {{q{2*k+parity}}}, {{{acc}{2*k+1}}}"]
+        lines.append(f"addc.u32 {{{acc}8}}, 0, 0" if fresh_top else f"addc.u32 {{{acc}8}}, {{{acc}8}}, 0")
+        outs = [("+r", f"{acc}[{i}]", f"{acc}{i}") for i in range(W)] + [("=r" if fresh_top else "+r", f"{acc}[8]", f"{acc}8")]
+        ins = [("r", "m", "m")] + [("r", f"q[{2*k+parity}]", f"q{2*k+parity}") for k in range(H)]
+        return asm_block(lines, outs, ins)
+
+    s.append(red_chain("x", 0, True))
+    s.append(red_chain("y", 1, True))
+    s.append("#pragma unroll\n    for (int i = 1; i < 8; i++) {\n")
+    # block A: y (becomes X') in place, n = Y'
+    lines = ["add.cc.u32 {y0}, {y0}, {x1}"]
+    for k in range(H):
+        lo = f"{{x{2*k+2}}}"
+        hi = f"{{x{2*k+3}}}" if 2 * k + 3 <= W else "0"
+        last = k == H - 1
+        lines += [f"madc.lo.cc.u32 {{n{2*k}}}, {{a{2*k+1}}}, {{bi}}, {lo}",
+                  f"madc.hi{'' if last else '.cc'}.u32 {{n{2*k+1}}}, {{a{2*k+1}}}, {{bi}}, {hi}"]
+    for k in range(H):
+        op_lo = "mad.lo.cc.u32" if k == 0 else "madc.lo.cc.u32"
+        lines += [f"{op_lo} {{y{2*k}}}, {{a{2*k}}}, {{bi}}, {{y{2*k}}}",
+                  f"madc.hi.cc.u32 {{y{2*k+1}}}, {{a{2*k}}}, {{bi}}, {{y{2*k+1}}}"]
+    lines.append("addc.u32 {y8}, {y8}, 0")
+    outs = [("+r", f"y[{i}]", f"y{i}") for i in range(W + 1)] + [("=&r", f"n[{i}]", f"n{i}") for i in range(W)]
+    ins = [("r", f"x[{i}]", f"x{i}") for i in range(1, W + 1)] + [("r", f"a[{i}]", f"a{i}") for i in range(W)] + \
+          [("r", "b[i]", "bi")]
+    s.append("    " + asm_block(lines, outs, ins).replace("\n    ", "\n        ").lstrip())
+    s.append("        m = y[0] * qinv0;\n")
+    s.append("    " + red_chain("y", 0, False).replace("\n    ", "\n        ").lstrip())
+    s.append("    " + red_chain("n", 1, True).replace("\n    ", "\n        ").lstrip())
+    s.append("#pragma unroll\n        for (int k = 0; k < 9; k++) { x[k] = y[k]; y[k] = n[k]; }\n    }\n")
+    # final: T = Y + X / 2^32, then T - q if T >= q (T < 2q, 257 bits)
+    lines = ["add.cc.u32 t0, {y0}, {x1}"]
+    for k in range(1, W):
+        lines.append(f"addc.cc.u32 t{k}, {{y{k}}}, {{x{k+1}}}")
+    lines.append("addc.u32 t8, {y8}, 0")
+    lines.append("sub.cc.u32 d0, t0, {q0}")
+    for k in range(1, W):
+        lines.append(f"subc.cc.u32 d{k}, t{k}, {{q{k}}}")
+    lines += ["subc.u32 bw, t8, 0", "not.b32 nb, bw"]
+    for k in range(W):
+        # bw == 0: T >= q -> d; bw == ~0: T < q -> t   (r = (t & bw) | (d & ~bw))
+        lines += [f"and.b32 t{k}, t{k}, bw", f"and.b32 d{k}, d{k}, nb", f"or.b32 {{r{k}}}, t{k}, d{k}"]
+    lines = ["{", ".reg .u32 t0, t1, t2, t3, t4, t5, t6, t7, t8, d0, d1, d2, d3, d4, d5, d6, d7, bw, nb"] + lines + ["}"]
+    outs = [("=r", f"r[{i}]", f"r{i}") for i in range(W)]
+    ins = [("r", f"y[{i}]", f"y{i}") for i in range(W + 1)] + [("r", f"x[{i}]", f"x{i}") for i in range(1, W + 1)] + \
+          [("r", f"q[{i}]", f"q{i}") for i in range(W)]
+    s.append(asm_block(lines, outs, ins))
+    s.append("}\n\n")
+    return "".join(s)
+
+
+def gen_addsub():
+    s = []
+    # add: 257-bit sum, subtract q, select
+    lines = ["{", ".reg .u32 s0, s1, s2, s3, s4, s5, s6, s7, s8, d0, d1, d2, d3, d4, d5, d6, d7, bw, nb",
+             "add.cc.u32 s0, {a0}, {b0}"] + [f"addc.cc.u32 s{k}, {{a{k}}}, {{b{k}}}" for k in range(1, W)] + \
+            ["addc.u32 s8, 0, 0", "sub.cc.u32 d0, s0, {q0}"] + [f"subc.cc.u32 d{k}, s{k}, {{q{k}}}" for k in range(1, W)] + \
+            ["subc.u32 bw, s8, 0", "not.b32 nb, bw"]
+    for k in range(W):
+        lines += [f"and.b32 s{k}, s{k}, bw", f"and.b32 d{k}, d{k}, nb", f"or.b32 {{r{k}}}, s{k}, d{k}"]
+    lines.append("}")
+    outs = [("=r", f"r[{i}]", f"r{i}") for i in range(W)]
+    ins = [("r", f"a[{i}]", f"a{i}") for i in range(W)] + [("r", f"b[{i}]", f"b{i}") for i in range(W)] + \
+          [("r", f"q[{i}]", f"q{i}") for i in range(W)]
+    blk = asm_block(lines, outs, ins)
+    s.append("// r = a + b mod q (Eq. saddmod, PAPER.md:184-192, 257-bit sum); a, b < q\n")
+    s.append("__device__ __forceinline__ void add_mod256(const uint32_t a[8], const uint32_t b[8], const uint32_t q[8],\n"
+             "                                           uint32_t r[8]) {\n" + blk + "}\n\n")
+    # sub: borrow chain, + (q & mask)
+    lines = ["{", ".reg .u32 d0, d1, d2, d3, d4, d5, d6, d7, bw, m0, m1, m2, m3, m4, m5, m6, m7",
+             "sub.cc.u32 d0, {a0}, {b0}"] + [f"subc.cc.u32 d{k}, {{a{k}}}, {{b{k}}}" for k in range(1, W)] + \
+            ["subc.u32 bw, 0, 0"] + [f"and.b32 m{k}, {{q{k}}}, bw" for k in range(W)] + \
+            ["add.cc.u32 {r0}, d0, m0"] + [f"addc.cc.u32 {{r{k}}}, d{k}, m{k}" for k in range(1, W - 1)] + \
+            [f"addc.u32 {{r{W-1}}}, d{W-1}, m{W-1}", "}"]
+    blk = asm_block(lines, outs, ins)
+    s.append("// r = a - b mod q (Eq. ssubmod, PAPER.md:193-201)\n")
+    s.append("__device__ __forceinline__ void sub_mod256(const uint32_t a[8], const uint32_t b[8], const uint32_t q[8],\n"
+             "                                           uint32_t r[8]) {\n" + blk + "}\n\n")
+    return "".join(s)
+
+
+def main():
+    head = ("// arith256_gen.cuh -- GENERATED by tools/gen_arith256.py; do not edit by hand.\n"
+            "// 256-bit (8 x 32-bit word) modular arithmetic for sm_100a (SURVEY.md §8(f) f4: wider\n"
+            "// multi-word moduli, the paper's stated generalisation, PAPER.md:807-808).  Any odd\n"
+            "// q < 2^256; residues canonical (< q) at every interface.\n"
+            "#pragma once\n#include <cstdint>\n\nnamespace ntt256 {\n\n")
+    with open(OUT, "w") as f:
+        f.write(head + gen_addsub() + gen_mont() + "}  // namespace ntt256\n")
+    print("wrote", OUT)
+
+
+if __name__ == "__main__":
+    main()
