@@ -460,6 +460,24 @@ def run_rows(args, P, pk, stream):
         rows["cfg5_butterflies_per_s"] = 2 * (1 << 25) * 26 / (ms * 1e-3)
         del p5, xx, yy, zz
         torch.cuda.empty_cache()
+    # 256-bit moduli, N = 2^16 x 32 forward + inverse (largest prime < 2^256
+    # with q = 1 mod 2^21); roofline P = 136 word products per butterfly (8-word Montgomery)
+    e = P["w256"]["b256"]
+    q = hexint(e["q"])
+    w = pow(hexint(e["omega"]), 1 << (e["logn"] - 16), q)
+    p6 = N.Plan256(16, q, w, batch=32)
+    xx = torch.from_numpy(synth.uniform_residues_w(q, 32 << 16, synth.stream_seed(10, 0, 16))
+                          .reshape(32, 1 << 16, 4).view(np.int64)).cuda()
+    yy, zz = torch.empty_like(xx), torch.empty_like(xx)
+    p6.forward(xx, out=yy); p6.inverse(yy, out=zz)
+    torch.cuda.synchronize()
+    assert torch.equal(zz, xx)
+    ms = time_events(lambda i: (p6.forward(xx, out=yy), p6.inverse(yy, out=zz)), 10, stream)
+    bf = 2 * 32 * (1 << 15) * 16 / (ms * 1e-3)
+    rows["f4_ntt256_n2^16_x32_butterflies_per_s"] = bf
+    rows["f4_ntt256_roofline_frac"] = bf * 136 / (pk["tprod_s"] * 1e12)
+    del p6, xx, yy, zz
+    torch.cuda.empty_cache()
     return rows
 
 

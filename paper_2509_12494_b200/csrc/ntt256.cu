@@ -185,29 +185,43 @@ struct Pass256Args {
 
 __device__ __forceinline__ int slot256(int l) { return l + (l >> 3); }
 
+// threads per group (E = 4 residues each) and groups per CTA (at least 64 threads)
+template <int B>
+struct Shape256 {
+    static constexpr int G = 1 << B;
+    static constexpr int RB = B >= 2 ? 2 : B;
+    static constexpr int E = 1 << RB;
+    static constexpr int T = G / E;
+    static constexpr int C = T >= 64 ? 1 : 64 / T;
+    static constexpr int GP = G + G / 8 + 1;
+};
+
 template <int B, bool FIRST, bool SCALE_LAST>
-__global__ void __launch_bounds__(((1 << B) >= 4 ? (1 << B) / 4 : 1))
+__global__ void __launch_bounds__(Shape256<B>::C * Shape256<B>::T)
 k_ntt256_pass(const Pass256Args a) {
-    constexpr int G = 1 << B;
-    constexpr int RB = B >= 2 ? 2 : B;
-    constexpr int E = 1 << RB;
-    constexpr int T = G / E;
-    constexpr int GP = G + G / 8 + 1;
+    using S = Shape256<B>;
+    constexpr int G = S::G, RB = S::RB, E = S::E, T = S::T, C = S::C, GP = S::GP;
     constexpr int ROUNDS = (B + RB - 1) / RB;
-    __shared__ uint4 lo_p[GP], hi_p[GP];      // the two 16-byte planes of each residue
-    __shared__ uint4 tw_lo[G], tw_hi[G];
+    __shared__ uint4 lo_p[C * GP], hi_p[C * GP];   // the two 16-byte planes of each residue
+    __shared__ uint4 tw_lo[C * G], tw_hi[C * G];
 
     const uint32_t n = a.n, lo = a.lo, gbits = n - B;
     const uint64_t N = 1ull << n;
-    const uint64_t gg = blockIdx.x;
+    const int c = threadIdx.x / T, t = threadIdx.x % T;
+    const uint64_t gg_raw = (uint64_t)blockIdx.x * C + c;
+    const bool live = gg_raw < a.total_groups;
+    const uint64_t gg = live ? gg_raw : a.total_groups - 1;
     const uint64_t poly = gg >> gbits, g = gg & ((1ull << gbits) - 1);
     const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
-    const int t = threadIdx.x;
-    // twiddles of this group's set (L = g mod 2^lo; the first pass has one set)
+    uint4* glo = lo_p + c * GP;
+    uint4* ghi = hi_p + c * GP;
+    uint4* twl = tw_lo + c * G;
+    uint4* twh = tw_hi + c * G;
+    // twiddles of this group's set (L = g mod 2^lo; a first pass has one set)
     {
         const uint64_t L = FIRST ? 0 : (g & ((1ull << lo) - 1));
         const uint4* src = a.pt + 2 * (m * a.pt_stride + L * (G - 1));
-        for (int e = t; e < G - 1; e += T) { tw_lo[e] = src[2 * e]; tw_hi[e] = src[2 * e + 1]; }
+        for (int e = t; e < G - 1; e += T) { twl[e] = src[2 * e]; twh[e] = src[2 * e + 1]; }
     }
     // rows t + i T of the group
     uint64_t gbase, gstride;
@@ -225,8 +239,8 @@ k_ntt256_pass(const Pass256Args a) {
         const int r = t + i * T;
         const int l = FIRST ? (int)brev_n((uint32_t)r, B) : r;
         const uint4* p = srcp + 2 * i * gstride;
-        lo_p[slot256(l)] = p[0];
-        hi_p[slot256(l)] = p[1];
+        glo[slot256(l)] = p[0];
+        ghi[slot256(l)] = p[1];
     }
     __syncthreads();
     const ModC256& M = a.mods[m];
@@ -240,7 +254,7 @@ k_ntt256_pass(const Pass256Args a) {
 #pragma unroll
         for (int k = 0; k < E; k++) {
             const int s = slot256(l0 | (k << w));
-            x[k] = e_from(lo_p[s], hi_p[s]);
+            x[k] = e_from(glo[s], ghi[s]);
         }
 #pragma unroll
         for (int bit = 0; bit < RB; bit++) {
@@ -255,7 +269,7 @@ k_ntt256_pass(const Pass256Args a) {
                 E256 v = x[k1], u = x[k0];
                 if (!trivial) {
                     const int ti = (1 << sl) - 1 + tlo + ((kk & ((1 << bit) - 1)) << w);
-                    v = mmul(v, e_from(tw_lo[ti], tw_hi[ti]), M);
+                    v = mmul(v, e_from(twl[ti], twh[ti]), M);
                     if (last) u = mmul(u, E256{{M.ninv_m[0], M.ninv_m[1], M.ninv_m[2], M.ninv_m[3], M.ninv_m[4],
                                                 M.ninv_m[5], M.ninv_m[6], M.ninv_m[7]}}, M);
                 }
@@ -266,19 +280,20 @@ k_ntt256_pass(const Pass256Args a) {
 #pragma unroll
         for (int k = 0; k < E; k++) {
             const int s = slot256(l0 | (k << w));
-            lo_p[s] = e_lo(x[k]);
-            hi_p[s] = e_hi(x[k]);
+            glo[s] = e_lo(x[k]);
+            ghi[s] = e_hi(x[k]);
         }
         __syncthreads();
     }
+    if (!live) return;
     // store: the first pass writes the group as contiguous rows (natural order within it)
     if (FIRST) {
         uint4* dstp = a.dst + 2 * (poly * N + ((uint64_t)brev_n((uint32_t)g, gbits) << B));
 #pragma unroll
         for (int i = 0; i < E; i++) {
             const int l = t + i * T;
-            dstp[2 * l] = lo_p[slot256(l)];
-            dstp[2 * l + 1] = hi_p[slot256(l)];
+            dstp[2 * l] = glo[slot256(l)];
+            dstp[2 * l + 1] = ghi[slot256(l)];
         }
     } else {
         uint4* dstp = a.dst + 2 * (poly * N + gbase);
@@ -286,8 +301,8 @@ k_ntt256_pass(const Pass256Args a) {
         for (int i = 0; i < E; i++) {
             const int l = t + i * T;
             uint4* p = dstp + 2 * i * gstride;
-            p[0] = lo_p[slot256(l)];
-            p[1] = hi_p[slot256(l)];
+            p[0] = glo[slot256(l)];
+            p[1] = ghi[slot256(l)];
         }
     }
 }
@@ -510,8 +525,9 @@ static ntt128_status run256(ntt256_plan_s* p, const uint4* src, uint4* dst, cuda
         a.n = (uint32_t)n;
         a.lo = (uint32_t)lo;
         a.nq = p->nq;
-        const int threads = (1 << B) >= 4 ? (1 << B) / 4 : 1;
-        fn<<<(unsigned)a.total_groups, threads, 0, st>>>(a);
+        const int T = (1 << B) >= 4 ? (1 << B) / 4 : 1;
+        const int C = T >= 64 ? 1 : 64 / T;
+        fn<<<(unsigned)((a.total_groups + C - 1) / C), C * T, 0, st>>>(a);
         ntt128_count_launch(1);
         if (cudaGetLastError() != cudaSuccess) return NTT128_ERR_CUDA;
         lo += B;

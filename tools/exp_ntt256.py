@@ -1,0 +1,34 @@
+"""Experiment: 256-bit NTT forward+inverse throughput (w256 b256 prime), N = 2^n, batch
+filling 2^21 residues (64 MiB)."""
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2509_12494_b200 import ntt128 as N  # noqa: E402
+from paper_2509_12494_b200 import synth  # noqa: E402
+
+P = json.load(open("tests/golden/params.json"))
+e = P["w256"]["b256"]
+q, L = int(e["q"], 16), e["logn"]
+for logn in [int(v) for v in sys.argv[1].split(",")]:
+    w = pow(int(e["omega"], 16), 1 << (L - logn), q)
+    B = (1 << 21) >> logn
+    plan = N.Plan256(logn, q, w, batch=B)
+    x = torch.from_numpy(synth.uniform_residues_w(q, 1 << 21, logn).reshape(B, 1 << logn, 4).view(np.int64)).cuda()
+    y, z = torch.empty_like(x), torch.empty_like(x)
+    for _ in range(2):
+        plan.forward(x, out=y); plan.inverse(y, out=z)
+    torch.cuda.synchronize()
+    assert torch.equal(z, x)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        plan.forward(x, out=y); plan.inverse(y, out=z)
+    e1.record(); e1.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    bf = 2 * B * (1 << (logn - 1)) * logn
+    print("256-bit logn %2d batch %4d: %.3f ms  %.4e bfly/s  %.1f%% of the 136-product roofline" %
+          (logn, B, ms, bf / (ms * 1e-3), 100 * bf / (ms * 1e-3) * 136 / 9.3062e12))
