@@ -493,7 +493,12 @@ def run_cfg5_fourstep(args, P, rank, world):
     e = P["cfg5"]
     q, w = hexint(e["q"]), hexint(e["omega"])
     out = {"cfg5_fourstep_gpus": world}
-    for transport in ("nccl", "p2p"):
+    # the peer-store transport at G > 1 needs NVLink peer mappings and device barriers across
+    # ranks: opt in with --p2p (at G = 1 it is a local fused pack and always runs)
+    transports = ("nccl", "p2p") if (world == 1 or args.p2p) else ("nccl",)
+    if world > 1 and not args.p2p:
+        out["cfg5_fourstep_p2p_skipped"] = "multi-GPU peer-store transport is opt-in: bench.py --p2p"
+    for transport in transports:
         try:
             fs = FS.FourStep(26, q, w, rank, world, None, transport=transport)
         except Exception as ex:                      # no peer mappings on this box
@@ -593,6 +598,8 @@ def main():
     ap.add_argument("--sweep", type=lambda s: [int(v) for v in s.split(",") if v], default=[10, 16])
     ap.add_argument("--no-cfg5", dest="cfg5", action="store_false", default=True)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false", default=True)
+    ap.add_argument("--p2p", action="store_true", default=False,
+                    help="also time the cfg5 four-step with the fused peer-store exchange at G > 1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -177,7 +177,7 @@ class FourStep:
 
     def _barrier(self):
         if self._hdl is not None:
-            self._hdl.barrier(channel=0)               # device-side, ordered on the current stream
+            self._hdl.barrier(channel=0, timeout_ms=30000)   # device-side, stream-ordered; errors instead of hanging
 
     def forward(self, cols, out=None):
         import torch
