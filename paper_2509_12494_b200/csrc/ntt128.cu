@@ -1346,8 +1346,21 @@ struct RunOpts {
 
 static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaStream_t stream);
 
+// Experiment switches (A/B measurements in DESIGN.md; defaults are the product behaviour),
+// read once per process: NTT128_NO_PDL (no pass overlap), NTT128_PDL_NOCNT (whole-grid
+// programmatic dependencies only), NTT128_NO_NC (polymul through the natural-order path).
+struct Switches {
+    bool no_pdl, pdl_nocnt, no_nc;
+    Switches() : no_pdl(getenv("NTT128_NO_PDL") != nullptr), pdl_nocnt(getenv("NTT128_PDL_NOCNT") != nullptr),
+                 no_nc(getenv("NTT128_NO_NC") != nullptr) {}
+};
+static const Switches& switches() {
+    static const Switches s;
+    return s;
+}
+
 static bool overlap_allowed(size_t npass, cudaStream_t stream, bool* ok) {
-    *ok = npass > 1 && getenv("NTT128_NO_PDL") == nullptr;
+    *ok = npass > 1 && !switches().no_pdl;
     if (*ok) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) return false;
@@ -1408,7 +1421,7 @@ static ntt128_status stream_scratch(ntt128_plan_s* p, cudaStream_t stream, uint4
 // polynomial; every pass but the last signals row i.
 static void set_overlap(ntt128_plan_s* p, ntt128_plan_s::StreamCtr* ctr, PassArgs& a, size_t i, size_t npass,
                         uint32_t prev_ctas_per_poly) {
-    if (getenv("NTT128_PDL_NOCNT")) {   // experiment: whole-grid dependencies only
+    if (switches().pdl_nocnt) {   // experiment: whole-grid dependencies only
         a.pdl_wait = 1u;
         return;
     }
@@ -1598,7 +1611,7 @@ extern "C" ntt128_status ntt128_polymul(const ntt128_plan_t p, const uint64_t* d
     ntt128_status s = stream_scratch(p, stream, &fa);
     if (s != NTT128_OK) return s;
     uint4* fb = fa + (size_t)p->N * p->batch;
-    if (!p->nc_bits.empty() && getenv("NTT128_NO_NC") == nullptr) {
+    if (!p->nc_bits.empty() && !switches().no_nc) {
         // permutation-free pipeline: no twist / untwist multiplies, spectra stay bit-reversed
         s = run_transform_nc(p, (const uint4*)d_a, fa, stream, false, nullptr);
         if (s == NTT128_OK) s = run_transform_nc(p, (const uint4*)d_b, fb, stream, false, nullptr);

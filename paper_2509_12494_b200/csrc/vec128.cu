@@ -120,7 +120,8 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
         if (a >= q) return NTT128_ERR_INPUT_RANGE;
     }
     words(M.to_m(a), c.a_m);
-    const bool barrett = (q >> 127) != 0 && getenv("NTT128_NO_BARRETT") == nullptr;
+    static const bool no_barrett = getenv("NTT128_NO_BARRETT") != nullptr;   // experiment switch (A/B)
+    const bool barrett = (q >> 127) != 0 && !no_barrett;
     if (barrett) {
         // mu = floor((2^256 - 1) / q) (= floor(2^256 / q), q odd) by restoring division
         u128 rem = 0, quo_lo = 0;
