@@ -265,7 +265,11 @@ __device__ __forceinline__ int slot(int l) { return PADL ? l + (l >> 3) : swz<B>
 // Single-pass CTAs (one CTA may hold several moduli) and the last pass's store keep the
 // interface canonical.
 enum { MODE_FULL = 0, MODE_HALF = 1, MODE_LAZY = 2 };
+#ifndef NTT_FORCE_FULL
+#define NTT_FORCE_FULL 0      // 1: canonical arithmetic for every modulus (experiment)
+#endif
 __device__ __forceinline__ int mode_of(const uint32_t q[4]) {
+    if (NTT_FORCE_FULL) return MODE_FULL;
     return (q[3] >> 30) == 0 ? MODE_LAZY : ((q[3] >> 31) == 0 ? MODE_HALF : MODE_FULL);
 }
 
