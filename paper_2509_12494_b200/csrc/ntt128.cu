@@ -62,13 +62,20 @@
 #define NTT_C5 8
 #endif
 #ifndef NTT_OCC_THREADS
-#define NTT_OCC_THREADS 768   // resident threads per SM the pass kernels are register-budgeted for
+#define NTT_OCC_THREADS 768   // resident threads per SM the radix-8 pass kernels are register-budgeted for
+#endif
+#ifndef NTT_OCC_THREADS_RB2
+#define NTT_OCC_THREADS_RB2 1024   // ... and the radix-4 multi-pass kernels
 #endif
 #ifndef NTT_LDG_DATA
 #define NTT_LDG_DATA 0        // 1: data tiles via LDG + STS instead of cp.async (experiment)
 #endif
+#ifndef NTT_RB9
+#define NTT_RB9 3
+#endif
 #ifndef NTT_RB8
-#define NTT_RB8 3   // register-round radix (log2) of the 8-stage multi-pass kernel (4 measured slower)
+#define NTT_RB8 2   // register-round radix (log2) of the 8-stage multi-pass kernel: radix-4 rounds
+                    // (smaller code, 32 warps/SM) beat radix-8 by 3.5 % with one group per CTA
 #endif
 
 using namespace ntt128;
@@ -406,8 +413,18 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
         round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf);
 }
 
+// Resident threads per SM each pass kernel is register-budgeted for: radix-4 multi-pass
+// kernels (16 data registers per thread, 64 registers) run 32 warps per SM, radix-8 ones
+// (32 data registers, 80) 24 warps (tools/gpu_variants.sh).
+template <int B, int RBMAX, bool SINGLE>
+struct PassOcc {
+    static constexpr int RB = PassShape<B, RBMAX>::RB;
+    static constexpr int THREADS = (RB == 2 && !SINGLE) ? NTT_OCC_THREADS_RB2 : NTT_OCC_THREADS;
+};
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX>
-__global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (NTT_OCC_THREADS / (C * PassShape<B, RBMAX>::T)) > 0 ? NTT_OCC_THREADS / (C * PassShape<B, RBMAX>::T) : 1)
+__global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T,
+                                  (PassOcc<B, RBMAX, SINGLE>::THREADS / (C * PassShape<B, RBMAX>::T)) > 0
+                                      ? PassOcc<B, RBMAX, SINGLE>::THREADS / (C * PassShape<B, RBMAX>::T) : 1)
 k_ntt_pass(const PassArgs a) {
     constexpr bool PADL = !SINGLE;
     using S = PassShape<B, RBMAX, C, PADL>;
@@ -932,7 +949,7 @@ static PassCfg multi_cfg_t(int B, bool wide) {
         case 6: return make_cfg<6, NTT_C6, FIRST, SL>();
         case 7: return make_cfg<7, NTT_C7, FIRST, SL>();
         case 8: return wide ? make_cfg<8, 4, FIRST, SL, false, NTT_RB8>() : make_cfg<8, NTT_C8, FIRST, SL, false, NTT_RB8>();
-        default: return wide ? make_cfg<9, 4, FIRST, SL>() : make_cfg<9, NTT_C9, FIRST, SL>();
+        default: return wide ? make_cfg<9, 4, FIRST, SL, false, NTT_RB9>() : make_cfg<9, NTT_C9, FIRST, SL, false, NTT_RB9>();
     }
 }
 // Permutation-free negacyclic passes (B in [5, 8], warp-owned groups).
