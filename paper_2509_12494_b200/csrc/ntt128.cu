@@ -52,6 +52,9 @@
 #ifndef NTT_NC_C8
 #define NTT_NC_C8 4           // permutation-free passes share one twiddle set per CTA when lo > 0
 #endif
+#ifndef NTT_NC_RB8
+#define NTT_NC_RB8 3
+#endif
 #ifndef NTT_C7
 #define NTT_C7 8
 #endif
@@ -775,17 +778,19 @@ __device__ __forceinline__ void nc_rounds(uint4* gsm, const uint4* tws, const in
         }
 #pragma unroll
         for (int k = 0; k < E; k++) gsm[S::LINEAR ? s0 + k * st : slot<B, true>(l0 | (k << w))] = u128_to(x[k]);
-        __syncwarp();
+        if (S::T <= 32) __syncwarp(); else __syncthreads();
     }
 }
 
 template <int B, int C, bool INV, bool SCALE_LAST, int RBMAX>
-__global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T, (NTT_OCC_THREADS / (C * PassShape<B, RBMAX>::T)) > 0 ? NTT_OCC_THREADS / (C * PassShape<B, RBMAX>::T) : 1)
+__global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T,
+                                  (PassOcc<B, RBMAX, false>::THREADS / (C * PassShape<B, RBMAX>::T)) > 0
+                                      ? PassOcc<B, RBMAX, false>::THREADS / (C * PassShape<B, RBMAX>::T) : 1)
 k_nc_pass(const PassArgs a) {
     using S = PassShape<B, RBMAX, C, true>;
     constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS, TS = S::TS;
     constexpr int NT = C * T;
-    static_assert(T <= 32 && 32 % T == 0, "permutation-free passes use warp-owned groups");
+    static_assert((T <= 32 && 32 % T == 0) || C == 1, "groups are warp-owned or alone in their CTA");
     extern __shared__ uint4 sm[];
     uint4* tsm = sm + C * GS;                        // [C][TS] twiddle sets (1 used when lo > 0)
 
@@ -977,9 +982,10 @@ static PassCfg multi_cfg_t(int B, bool wide) {
 // Permutation-free negacyclic passes (B in [5, 8], warp-owned groups).
 template <int B, int C, bool INV, bool SL>
 static PassCfg make_nc_cfg() {
-    using S = PassShape<B, 3, C, true>;
+    constexpr int RBM = B == 8 ? NTT_NC_RB8 : 3;
+    using S = PassShape<B, RBM, C, true>;
     PassCfg c;
-    c.fn = k_nc_pass<B, C, INV, SL, 3>;
+    c.fn = k_nc_pass<B, C, INV, SL, RBM>;
     c.B = B;
     c.C = C;
     c.threads = C * S::T;
