@@ -517,7 +517,7 @@ k_ntt_pass(const PassArgs a) {
     }
     // ---------------- pass overlap: the twiddles (plan constants) are already in flight;
     // data may be read only once the producers of this polynomial are done
-    if (!SINGLE) {
+    {
         if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
         if (a.cnt_in) {
             if (tid == 0) {
@@ -1500,6 +1500,9 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
         ntt128_status st = stream_counters(p, stream, lk, &ctr);
         if (st != NTT128_OK) return st;
     }
+    // a single-pass transform is one programmatic dependent launch (no counters): its
+    // launch and twiddle prologue overlap the previous kernel's tail, also under capture
+    const bool pdl_single = npass == 1 && !switches().no_pdl;
     int lo = 0;
     uint32_t prev_ctas_per_poly = 0;
     for (size_t i = 0; i < npass; i++) {
@@ -1529,8 +1532,9 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
         }
         const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (uint64_t)c.C);
         if (overlap) set_overlap(p, ctr, a, i, npass, prev_ctas_per_poly);
+        if (pdl_single) a.pdl_wait = 1u;
         const uint64_t ctas = (a.total_groups + c.C - 1) / c.C;
-        if (launch_pass(c, a, ctas, stream, overlap) != cudaSuccess) return NTT128_ERR_CUDA;
+        if (launch_pass(c, a, ctas, stream, overlap || pdl_single) != cudaSuccess) return NTT128_ERR_CUDA;
         ntt128_count_launch(1);
         lo += B;
         prev_ctas_per_poly = ctas_per_poly;
