@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <cstdlib>
 
 #include "../../include/ntt128.h"
@@ -47,6 +48,10 @@ constexpr int THREADS = 256;
 template <int OPK>
 __global__ void __launch_bounds__(THREADS) k_vec(uint4* z, const uint4* __restrict__ x,
                                                  const uint4* y, uint64_t n, const VecConst c) {
+    // programmatic dependent launch: wait for the previous kernel's writes, then let the
+    // next one be scheduled as this grid drains (its launch latency overlaps our tail)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; i + (UNROLL - 1) * stride < n; i += UNROLL * stride) {
@@ -153,17 +158,28 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
         if (cudaStreamSynchronize(stream) != cudaSuccess) return NTT128_ERR_CUDA;
         if (h) return NTT128_ERR_INPUT_RANGE;
     }
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
     switch (op) {
-        case OP_ADD: k_vec<OP_ADD><<<grid, THREADS, 0, stream>>>(z, x, y, n, c); break;
-        case OP_SUB: k_vec<OP_SUB><<<grid, THREADS, 0, stream>>>(z, x, y, n, c); break;
+        case OP_ADD: e = cudaLaunchKernelEx(&cfg, k_vec<OP_ADD>, z, x, y, (uint64_t)n, c); break;
+        case OP_SUB: e = cudaLaunchKernelEx(&cfg, k_vec<OP_SUB>, z, x, y, (uint64_t)n, c); break;
         case OP_MUL:
-            if (barrett) k_vec<OP_MULB><<<grid, THREADS, 0, stream>>>(z, x, y, n, c);
-            else k_vec<OP_MUL><<<grid, THREADS, 0, stream>>>(z, x, y, n, c);
+            e = barrett ? cudaLaunchKernelEx(&cfg, k_vec<OP_MULB>, z, x, y, (uint64_t)n, c)
+                        : cudaLaunchKernelEx(&cfg, k_vec<OP_MUL>, z, x, y, (uint64_t)n, c);
             break;
-        default: k_vec<OP_AXPY><<<grid, THREADS, 0, stream>>>(z, x, y, n, c); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_vec<OP_AXPY>, z, x, y, (uint64_t)n, c); break;
     }
     ntt128_count_launch(1);
-    return cudaGetLastError() == cudaSuccess ? NTT128_OK : NTT128_ERR_CUDA;
+    return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NTT128_OK : NTT128_ERR_CUDA;
 }
 
 }  // namespace
