@@ -904,6 +904,129 @@ k_nc_pass(const PassArgs a) {
     }
 }
 
+// ----------------------------------------------------------------------------- cluster latency kernel
+// One polynomial on a cluster of 8 CTAs (8 SMs) with distributed shared memory, for the
+// latency configuration (BASELINE cfg 1: one N = 2^10 transform; cyclic single-pass plans
+// with N = 2^8 .. 2^11 and few polynomials).  One SM is throughput-bound on N/2 log N
+// butterflies (3.7 us for N = 2^10 at 0.7 butterflies/clk); eight SMs leave the stage
+// latency (one butterfly per thread per stage) as the bound.  N = 8 M, CTA r of the
+// cluster owns positions [r M, (r + 1) M) of the bit-reversed working order:
+//  * phase 1 (stages 0 .. LM - 1, LM = log2 M): positions p = r M + i, i < M, gathered
+//    from x[brev_LM(i) 8 + brev_3(r)]; radix-2 stages in the CTA's shared memory, one
+//    butterfly per thread per stage;
+//  * phase 2 (stages LM .. LM + 2): the group of g < M is {g + k M : k < 8}, element k in
+//    CTA k's shared memory at offset g.  CTA r takes groups [r M/8, (r + 1) M/8), reads its
+//    first-stage pairs straight from the owners' shared memory (ld.shared::cluster), and
+//    the last stage stores natural-order outputs p = g + k M to global memory.
+// Every twiddle a thread uses (LM + 3 of them) is loaded into registers before the
+// dependency wait.  Values stay canonical (any odd q < 2^128).
+#include <cooperative_groups.h>
+constexpr int CLU_LOG = 3, CLU = 1 << CLU_LOG;
+
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint4 ld_dsmem(const uint4* local, uint32_t rank) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(local);
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    uint4 v;
+    asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ra) : "memory");
+    return v;
+}
+
+template <int LB, bool SCALE_LAST>
+__global__ void __launch_bounds__(1 << (LB - CLU_LOG - 1)) k_ntt_cluster(const PassArgs a) {
+    constexpr int LM = LB - CLU_LOG, M = 1 << LM, NT = M / 2, GPC = M / CLU;   // groups per CTA
+    __shared__ uint4 loc[M];     // phase 1 working set, read by the whole cluster
+    __shared__ uint4 buf[M];     // phase 2: [GPC][8]
+    const uint32_t r = cluster_rank();
+    const uint64_t poly = blockIdx.x >> CLU_LOG;
+    const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
+    const int t = threadIdx.x;
+    const uint4* pt = a.pt + m * a.pt_stride;                   // stage s, twiddle j at (2^s - 1) + j
+    const int gl = t >> (CLU_LOG - 1), bb = t & (CLU / 2 - 1);  // phase 2: group, butterfly in group
+    const int g = (int)r * GPC + gl;
+    U128 tw[LB];
+#pragma unroll
+    for (int s = 1; s < LM; s++) tw[s] = u128_from(__ldg(pt + (1 << s) - 1 + (t & ((1 << s) - 1))));
+#pragma unroll
+    for (int sp = 0; sp < CLU_LOG; sp++) {
+        const int k0 = ((bb >> sp) << (sp + 1)) | (bb & ((1 << sp) - 1));
+        tw[LM + sp] = u128_from(__ldg(pt + (1 << (LM + sp)) - 1 + g + ((k0 & ((1 << sp) - 1)) << LM)));
+    }
+    const ModC& MC = a.mods[m];
+    const uint32_t q[4] = {MC.q[0], MC.q[1], MC.q[2], MC.q[3]};
+    const uint32_t q2[4] = {0, 0, 0, 0};
+    const uint32_t qinv0 = MC.qinv0;
+    U128 nf = U128{{0, 0, 0, 0}};
+    if (SCALE_LAST) {
+        const uint32_t* sp = a.ninv_r ? MC.ninv_rm : MC.ninv_m;
+        nf = U128{{sp[0], sp[1], sp[2], sp[3]}};
+    }
+    if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    // ---- phase 1: stage 0 on the two gathered inputs in registers, then stages 1 .. LM - 1
+    {
+        const uint4* src = a.src + (poly << LB);
+        const uint32_t br = brev_bits(r, CLU_LOG);
+        U128 u = u128_from(__ldcg(src + ((brev_bits(2 * t, LM) << CLU_LOG) | br)));
+        U128 v = u128_from(__ldcg(src + ((brev_bits(2 * t + 1, LM) << CLU_LOG) | br)));
+        bfly1<MODE_FULL>(u, v, q);
+        loc[2 * t] = u128_to(u);
+        loc[2 * t + 1] = u128_to(v);
+        __syncthreads();
+#pragma unroll
+        for (int s = 1; s < LM; s++) {
+            const int j = t & ((1 << s) - 1), i0 = ((t >> s) << (s + 1)) | j, i1 = i0 | (1 << s);
+            u = u128_from(loc[i0]);
+            v = u128_from(loc[i1]);
+            bfly<MODE_FULL, false>(u, v, tw[s], q, q2, qinv0, nf);
+            loc[i0] = u128_to(u);
+            loc[i1] = u128_to(v);
+            if (s + 1 < LM) __syncthreads();
+        }
+    }
+    cluster_arrive();            // phase-1 values of every CTA visible cluster-wide
+    cluster_wait();
+
+    // ---- phase 2: stages LM .. LM + 2 on groups of 8 (one element per CTA)
+    {
+        U128 u = u128_from(ld_dsmem(loc + g, 2 * bb)), v = u128_from(ld_dsmem(loc + g, 2 * bb + 1));
+        cluster_arrive();        // this CTA's remote reads are done (owners wait before exiting)
+        bfly<MODE_FULL, false>(u, v, tw[LM], q, q2, qinv0, nf);   // LM < LB - 1: never the last stage
+        uint4* gb = buf + gl * CLU;
+        gb[2 * bb] = u128_to(u);
+        gb[2 * bb + 1] = u128_to(v);
+        constexpr unsigned WM = NT >= 32 ? 0xffffffffu : ((1u << NT) - 1);   // a group's 4 threads share a warp
+        __syncwarp(WM);
+#pragma unroll
+        for (int sp = 1; sp < CLU_LOG; sp++) {
+            const int k0 = ((bb >> sp) << (sp + 1)) | (bb & ((1 << sp) - 1)), k1 = k0 | (1 << sp);
+            u = u128_from(gb[k0]);
+            v = u128_from(gb[k1]);
+            if (SCALE_LAST && LM + sp == LB - 1) bfly<MODE_FULL, true>(u, v, tw[LM + sp], q, q2, qinv0, nf);
+            else bfly<MODE_FULL, false>(u, v, tw[LM + sp], q, q2, qinv0, nf);
+            if (sp + 1 < CLU_LOG) {
+                gb[k0] = u128_to(u);
+                gb[k1] = u128_to(v);
+                __syncwarp(WM);
+            } else {             // natural-order outputs p = g + k M
+                uint4* dst = a.dst + (poly << LB);
+                dst[g + (k0 << LM)] = u128_to(u);
+                dst[g + (k1 << LM)] = u128_to(v);
+            }
+        }
+    }
+    cluster_wait();              // nobody still reads this CTA's shared memory
+}
+
 // ----------------------------------------------------------------------------- launch table
 typedef void (*PassKernel)(const PassArgs);
 
@@ -1399,9 +1522,9 @@ static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaS
 // read once per process: NTT128_NO_PDL (no pass overlap), NTT128_PDL_NOCNT (whole-grid
 // programmatic dependencies only), NTT128_NO_NC (polymul through the natural-order path).
 struct Switches {
-    bool no_pdl, pdl_nocnt, no_nc;
+    bool no_pdl, pdl_nocnt, no_nc, no_cluster;
     Switches() : no_pdl(getenv("NTT128_NO_PDL") != nullptr), pdl_nocnt(getenv("NTT128_PDL_NOCNT") != nullptr),
-                 no_nc(getenv("NTT128_NO_NC") != nullptr) {}
+                 no_nc(getenv("NTT128_NO_NC") != nullptr), no_cluster(getenv("NTT128_NO_CLUSTER") != nullptr) {}
 };
 static const Switches& switches() {
     static const Switches s;
@@ -1483,8 +1606,62 @@ static void set_overlap(ntt128_plan_s* p, ntt128_plan_s::StreamCtr* ctr, PassArg
     if (i + 1 < npass) a.cnt_out = ctr->d + i * (size_t)p->batch;
 }
 
+// Cluster latency path (k_ntt_cluster): cyclic single-pass plans, N = 2^8 .. 2^11, at most
+// NTT_CLU_MAX_BATCH polynomials (8 CTAs each).
+#ifndef NTT_CLU_MAX_BATCH
+#define NTT_CLU_MAX_BATCH 16
+#endif
+static bool use_cluster(const ntt128_plan_s* p, const RunOpts& o) {
+    if (switches().no_cluster || p->kind != 0 || o.pmul || p->bits.size() != 1) return false;
+    return p->log2n >= 8 && p->log2n <= 11 && p->batch <= NTT_CLU_MAX_BATCH;
+}
+template <bool SL>
+static PassKernel cluster_fn(int B) {
+    switch (B) {
+        case 8: return k_ntt_cluster<8, SL>;
+        case 9: return k_ntt_cluster<9, SL>;
+        case 10: return k_ntt_cluster<10, SL>;
+        default: return k_ntt_cluster<11, SL>;
+    }
+}
+static ntt128_status run_cluster(ntt128_plan_s* p, const uint4* src, uint4* dst, cudaStream_t stream, const RunOpts& o) {
+    const int n = (int)p->log2n;
+    const bool scale_last = o.inverse;
+    PassArgs a;
+    memset(&a, 0, sizeof(a));
+    a.src = src;
+    a.dst = dst;
+    a.mods = p->d_mods;
+    a.pt = !o.inverse ? p->d_pt_fwd[0] : (o.polymul ? p->d_pt_inv_r[0] : p->d_pt_inv[0]);
+    a.pt_stride = p->pt_stride[0];
+    a.n = (uint32_t)n;
+    a.nq = p->nq;
+    a.ninv_r = o.polymul ? 1 : 0;
+    const bool pdl = !switches().no_pdl;
+    a.pdl_wait = pdl ? 1u : 0u;
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(p->batch * CLU);
+    cfg.blockDim = dim3(1u << (n - CLU_LOG - 1));
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CLU;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 2 : 1;
+    const PassKernel fn = scale_last ? cluster_fn<true>(n) : cluster_fn<false>(n);
+    if (cudaLaunchKernelEx(&cfg, fn, a) != cudaSuccess) return NTT128_ERR_CUDA;
+    ntt128_count_launch(1);
+    return NTT128_OK;
+}
+
 static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* dst, cudaStream_t stream,
                                    const RunOpts& o) {
+    if (use_cluster(p, o)) return run_cluster(p, src, dst, stream, o);
     const int n = (int)p->log2n;
     const size_t npass = p->bits.size();
     const bool scale_last = p->kind == 0 && o.inverse;

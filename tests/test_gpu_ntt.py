@@ -250,3 +250,24 @@ def test_cfg5_direct_three_pass(N, params):
     for k in [0, 1, 2, n // 2, n - 1, 12345678, 40000001]:
         assert synth.to_ints(y[0, k:k + 1])[0] == O.ntt_eval(x[0], q, w, k), f"y[{k}]"
     assert torch.equal(plan.inverse(dy), dx)
+
+
+@pytest.mark.parametrize("logn", [8, 9, 10, 11])
+def test_cluster_latency_path(N, params, logn):
+    """few polynomials at N = 2^8 .. 2^11 run on 8-CTA clusters (distributed shared
+    memory exchange between the in-CTA stages and the last three); batch 17 is past the
+    cluster threshold (the one-CTA-per-polynomial shape), all moduli classes, in place"""
+    mods = params["cfg3"]["moduli"][:17]
+    for B in (1, 5, 16, 17):
+        qs = [m["q"] for m in mods[:B]]
+        ws = [sub_root(m, logn) for m in mods[:B]]
+        n = 1 << logn
+        x = np.stack([synth.uniform_residues(qs[i], n, 3000 * logn + 10 * B + i) for i in range(B)])
+        plan = N.Plan(logn, qs, ws, batch=B)
+        d = to_dev(x)
+        y = to_host(plan.forward(d))
+        assert np.array_equal(y, O.ntt(x, qs, ws)), f"B={B}"
+        plan.forward(d, out=d)
+        assert np.array_equal(to_host(d), y)
+        plan.inverse(d, out=d)
+        assert np.array_equal(to_host(d), x), f"B={B}"

@@ -3,6 +3,7 @@
 // A: word-serial Montgomery (CIOS), 32-bit digits, R = 2^128.
 // B: Montgomery SOS: full 256-bit product, m = lo128(t*q'), t + m*q.
 // C: Shoup with an exact bit 128 of the remainder (r in [0, 2q) may exceed 2^128).
+// E: Karatsuba (double-word level) full product and SOS Montgomery on it (f2 ablation).
 // D: the product code: arith128.cuh mont_mul (even/odd alternating CIOS), mont_mul_lazy,
 //    and barrett128.cuh barrett_mul_dev (general a b mod q, no Montgomery form).
 #include <cstdio>
@@ -183,6 +184,70 @@ __device__ __forceinline__ void mont_eo(uint32_t r[4], const uint32_t a[4], cons
   r[0] = (e0 & bw) | (d0 & ~bw); r[1] = (e1 & bw) | (d1 & ~bw); r[2] = (e2 & bw) | (d2 & ~bw); r[3] = (e3 & bw) | (d3 & ~bw);
 }
 
+// ---------- E: Karatsuba at the paper's double-word level (Eq. mulk):
+// a = a1 2^64 + a0, b = b1 2^64 + b0; a b = p2 2^128 + (s_a s_b - p0 - p2) 2^64 + p0 with
+// p0 = a0 b0, p2 = a1 b1, s = 65-bit half sums.  3 double-word products = 12 word products
+// (vs 16) plus the 65-bit corrections and the middle subtraction on the ALU pipe.
+__device__ __forceinline__ void mul128x(uint32_t p[4], uint32_t x0, uint32_t x1, uint32_t y0, uint32_t y1) {
+  asm("mul.lo.u32 %0, %4, %6;\n\t"
+      "mul.hi.u32 %1, %4, %6;\n\t"
+      "mul.lo.u32 %2, %5, %7;\n\t"
+      "mul.hi.u32 %3, %5, %7;\n\t"
+      "mad.lo.cc.u32 %1, %4, %7, %1;\n\t"
+      "madc.hi.cc.u32 %2, %4, %7, %2;\n\t"
+      "addc.u32 %3, %3, 0;\n\t"
+      "mad.lo.cc.u32 %1, %5, %6, %1;\n\t"
+      "madc.hi.cc.u32 %2, %5, %6, %2;\n\t"
+      "addc.u32 %3, %3, 0;"
+      : "=r"(p[0]), "=r"(p[1]), "=r"(p[2]), "=r"(p[3]) : "r"(x0), "r"(x1), "r"(y0), "r"(y1));
+}
+__device__ __forceinline__ void kara256(uint32_t t[8], const uint32_t a[4], const uint32_t b[4]) {
+  uint32_t p0[4], p2[4], m[4], sa0, sa1, ca, sb0, sb1, cb, m4;
+  mul128x(p0, a[0], a[1], b[0], b[1]);
+  mul128x(p2, a[2], a[3], b[2], b[3]);
+  asm("add.cc.u32 %0, %6, %8;\n\t addc.cc.u32 %1, %7, %9;\n\t addc.u32 %2, 0, 0;\n\t"
+      "add.cc.u32 %3, %10, %12;\n\t addc.cc.u32 %4, %11, %13;\n\t addc.u32 %5, 0, 0;"
+      : "=r"(sa0), "=r"(sa1), "=r"(ca), "=r"(sb0), "=r"(sb1), "=r"(cb)
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]));
+  mul128x(m, sa0, sa1, sb0, sb1);
+  const uint32_t ma = 0u - ca, mb = 0u - cb;
+  // m += (ca sb_lo + cb sa_lo) 2^64 + ca cb 2^128
+  asm("add.cc.u32 %0, %0, %3;\n\t addc.cc.u32 %1, %1, %4;\n\t addc.u32 %2, %7, 0;\n\t"
+      "add.cc.u32 %0, %0, %5;\n\t addc.cc.u32 %1, %1, %6;\n\t addc.u32 %2, %2, 0;"
+      : "+r"(m[2]), "+r"(m[3]), "=&r"(m4)
+      : "r"(sb0 & ma), "r"(sb1 & ma), "r"(sa0 & mb), "r"(sa1 & mb), "r"(ca & cb));
+  // middle = m - p0 - p2 (>= 0, < 2^129)
+  asm("sub.cc.u32 %0, %0, %5;\n\t subc.cc.u32 %1, %1, %6;\n\t subc.cc.u32 %2, %2, %7;\n\t subc.cc.u32 %3, %3, %8;\n\t subc.u32 %4, %4, 0;\n\t"
+      "sub.cc.u32 %0, %0, %9;\n\t subc.cc.u32 %1, %1, %10;\n\t subc.cc.u32 %2, %2, %11;\n\t subc.cc.u32 %3, %3, %12;\n\t subc.u32 %4, %4, 0;"
+      : "+r"(m[0]), "+r"(m[1]), "+r"(m[2]), "+r"(m[3]), "+r"(m4)
+      : "r"(p0[0]), "r"(p0[1]), "r"(p0[2]), "r"(p0[3]), "r"(p2[0]), "r"(p2[1]), "r"(p2[2]), "r"(p2[3]));
+  t[0] = p0[0]; t[1] = p0[1];
+  asm("add.cc.u32 %0, %6, %10;\n\t addc.cc.u32 %1, %7, %11;\n\t addc.cc.u32 %2, %8, %12;\n\t"
+      "addc.cc.u32 %3, %9, %13;\n\t addc.cc.u32 %4, %15, %14;\n\t addc.u32 %5, %16, 0;"
+      : "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]), "=r"(t[6]), "=r"(t[7])
+      : "r"(p0[2]), "r"(p0[3]), "r"(p2[0]), "r"(p2[1]), "r"(m[0]), "r"(m[1]), "r"(m[2]), "r"(m[3]), "r"(m4),
+        "r"(p2[2]), "r"(p2[3]));
+}
+// SOS Montgomery with both 256-bit products by Karatsuba (bit-identical to mont_sos)
+__device__ __forceinline__ void mont_sos_kara(uint32_t r[4], const uint32_t a[4], const uint32_t b[4], const uint32_t q[4], const uint32_t qp[4]) {
+  uint32_t t[8], m[4], u[8];
+  kara256(t, a, b);
+  uint32_t tl[4] = {t[0], t[1], t[2], t[3]};
+  mullo128(m, tl, qp);
+  kara256(u, m, q);
+  uint32_t c = (t[0] | t[1] | t[2] | t[3]) != 0;
+  uint32_t s0, s1, s2, s3, s4;
+  asm("add.cc.u32 %0, %5, %9;\n\t addc.cc.u32 %1, %6, %10;\n\t addc.cc.u32 %2, %7, %11;\n\t addc.cc.u32 %3, %8, %12;\n\t addc.u32 %4, 0, 0;"
+      : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3), "=r"(s4) : "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]));
+  asm("add.cc.u32 %0, %0, %5;\n\t addc.cc.u32 %1, %1, 0;\n\t addc.cc.u32 %2, %2, 0;\n\t addc.cc.u32 %3, %3, 0;\n\t addc.u32 %4, %4, 0;"
+      : "+r"(s0), "+r"(s1), "+r"(s2), "+r"(s3), "+r"(s4) : "r"(c));
+  uint32_t d0, d1, d2, d3, bw;
+  asm("sub.cc.u32 %0, %5, %10;\n\t subc.cc.u32 %1, %6, %11;\n\t subc.cc.u32 %2, %7, %12;\n\t subc.cc.u32 %3, %8, %13;\n\t subc.u32 %4, %9, 0;"
+      : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(d3), "=r"(bw) : "r"(s0), "r"(s1), "r"(s2), "r"(s3), "r"(s4), "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]));
+  bool ge = (bw == 0);
+  r[0] = ge ? d0 : s0; r[1] = ge ? d1 : s1; r[2] = ge ? d2 : s2; r[3] = ge ? d3 : s3;
+}
+
 template <int V>
 __global__ void k_mulmod(uint4* io, const C128 c, int iters, long long* cyc) {
   constexpr int ILP = 4;
@@ -203,7 +268,13 @@ __global__ void k_mulmod(uint4* io, const C128 c, int iters, long long* cyc) {
                          ntt128::U128 r = ntt128::mont_mul(a, b, c.q, c.qinv0); for (int i = 0; i < 4; i++) x[k][i] = r.w[i]; }
       else if (V == 4) { ntt128::U128 a{{x[k][0], x[k][1], x[k][2], x[k][3]}}, b{{w[0], w[1], w[2], w[3]}};
                          ntt128::U128 r = ntt128::mont_mul_lazy(a, b, c.q, c.qinv0); for (int i = 0; i < 4; i++) x[k][i] = r.w[i]; }
-      else { uint32_t r[4]; ntt128::barrett_mul_dev(x[k], w, c.bc, r); for (int i = 0; i < 4; i++) x[k][i] = r[i]; }
+      else if (V == 5) { uint32_t r[4]; ntt128::barrett_mul_dev(x[k], w, c.bc, r); for (int i = 0; i < 4; i++) x[k][i] = r[i]; }
+      else if (V == 6 || V == 7) {      // bare 128x128 -> 256 product, folded back to 128 bits
+        uint32_t t[8];
+        if (V == 6) mul256(t, x[k], w); else kara256(t, x[k], w);
+        for (int i = 0; i < 4; i++) x[k][i] = t[i] ^ t[i + 4];
+      }
+      else mont_sos_kara(x[k], x[k], w, c.q, c.qp);
     }
   }
   long long t1 = clock64();
@@ -230,8 +301,9 @@ int main() {
   std::vector<uint4> h(n); for (size_t i = 0; i < n; i++) h[i] = make_uint4(i * 2654435761u, i, 77, 0x7fffffff);
   uint4* d; long long* dc; CK(cudaMalloc(&d, n * 16)); CK(cudaMalloc(&dc, blocks * 8));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const char* names[6] = {"mont_cios", "mont_sos", "mont_eo", "product_mont_mul", "product_mont_mul_lazy", "product_barrett"};
-  for (int v = 0; v < 6; v++) {
+  const char* names[9] = {"mont_cios", "mont_sos", "mont_eo", "product_mont_mul", "product_mont_mul_lazy", "product_barrett",
+                          "mul256_schoolbook", "mul256_karatsuba", "mont_sos_karatsuba"};
+  for (int v = 0; v < 9; v++) {
     CK(cudaMemcpy(d, h.data(), n * 16, cudaMemcpyHostToDevice));
     auto launch = [&]() {
       switch (v) {
@@ -240,7 +312,10 @@ int main() {
         case 2: k_mulmod<2><<<blocks, threads>>>(d, c, iters, dc); break;
         case 3: k_mulmod<3><<<blocks, threads>>>(d, c, iters, dc); break;
         case 4: k_mulmod<4><<<blocks, threads>>>(d, c, iters, dc); break;
-        default: k_mulmod<5><<<blocks, threads>>>(d, c, iters, dc); break;
+        case 5: k_mulmod<5><<<blocks, threads>>>(d, c, iters, dc); break;
+        case 6: k_mulmod<6><<<blocks, threads>>>(d, c, iters, dc); break;
+        case 7: k_mulmod<7><<<blocks, threads>>>(d, c, iters, dc); break;
+        default: k_mulmod<8><<<blocks, threads>>>(d, c, iters, dc); break;
       } };
     for (int w = 0; w < 3; w++) launch();
     CK(cudaDeviceSynchronize());
