@@ -37,6 +37,12 @@
 #include "arith128.cuh"
 #include "host128.h"
 
+#ifndef NTT_COMPUTE_REPEAT
+#define NTT_COMPUTE_REPEAT 1  // experiment: run a pass's register rounds k times (0: memory phases only)
+#endif
+#ifndef NTT_TRACE
+#define NTT_TRACE 0           // experiment: per-tile timeline (tools/exp_trace.py)
+#endif
 #ifndef NTT_UNROLL_ROUNDS
 #define NTT_UNROLL_ROUNDS 0   // 1: unroll the register rounds (compile-time windows)
 #endif
@@ -97,6 +103,32 @@ using ntt128h::u128;
 static std::atomic<uint64_t> g_launches{0};
 extern "C" uint64_t ntt128_launch_count(void) { return g_launches.load(); }
 void ntt128_count_launch(uint64_t k) { g_launches += k; }
+
+// Experiment builds only (-DNTT_TRACE=1): every multi-pass tile records globaltimer at its
+// start, after its loads and after its stores, with its SM and pass, into a device buffer
+// the caller provides (tools/exp_trace.py).  Not part of the product ABI.
+#if NTT_TRACE
+__device__ uint4* g_trace = nullptr;
+__device__ unsigned long long g_trace_n = 0;
+__device__ unsigned long long g_trace_cap = 0;
+__device__ __forceinline__ uint32_t gtimer_lo() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (uint32_t)(t & 0xffffffffu);
+}
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+extern "C" int ntt128_debug_trace(void* buf, unsigned long long cap) {
+    unsigned long long z = 0;
+    if (cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)) != cudaSuccess) return 1;
+    if (cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof(cap)) != cudaSuccess) return 1;
+    if (cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z)) != cudaSuccess) return 1;
+    return 0;
+}
+#endif
 
 extern "C" const char* ntt128_status_string(ntt128_status s) {
     switch (s) {
@@ -462,6 +494,9 @@ k_ntt_pass(const PassArgs a) {
     const uint32_t n = a.n, lo = a.lo, gbits = n - B;
     const uint64_t N = 1ull << n;
     const uint64_t gmask = (1ull << gbits) - 1;
+#if NTT_TRACE
+    const uint32_t tr_t0 = gtimer_lo();
+#endif
     uint64_t gg0 = (uint64_t)blockIdx.x * C;
     // multi-pass CTAs hold groups of one polynomial: visit polynomials in the plan's order
     // (grouped by arithmetic mode) so one code path at a time is hot in the I-cache
@@ -586,6 +621,9 @@ k_ntt_pass(const PassArgs a) {
     }
     cp_async_wait_all();
     __syncthreads();
+#if NTT_TRACE
+    const uint32_t tr_t1 = gtimer_lo();
+#endif
 
     // ---------------- register rounds: RB stages on E elements per thread
     // Groups of at most 32 threads are owned by whole warps (c = tid / T), so the exchanges
@@ -612,6 +650,10 @@ k_ntt_pass(const PassArgs a) {
         const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
         const int mode = SINGLE ? MODE_FULL : mode_of(q);   // uniform per CTA: its groups share the polynomial
+#if NTT_COMPUTE_REPEAT != 1
+#pragma unroll 1
+        for (int rep = 0; rep < NTT_COMPUTE_REPEAT; rep++)
+#endif
         if (mode == MODE_LAZY)
             pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
         else if (mode == MODE_HALF)
@@ -688,6 +730,12 @@ k_ntt_pass(const PassArgs a) {
         __syncthreads();
         if (tid == 0) red_release_gpu_add(a.cnt_out + (gg0 >> gbits), 1u);
     }
+#if NTT_TRACE
+    if (tid == 0 && !SINGLE && g_trace) {
+        const unsigned long long k = atomicAdd(&g_trace_n, 1ull);
+        if (k < g_trace_cap) g_trace[k] = make_uint4(tr_t0, tr_t1, gtimer_lo(), (smid() << 16) | (a.lo << 8) | (FIRST ? 1u : 0u));
+    }
+#endif
 }
 
 // ----------------------------------------------------------------------------- permutation-free negacyclic passes

@@ -68,9 +68,10 @@ __global__ void __launch_bounds__(256) k_bfly(uint4* io, const uint4* tw, const 
     for (int k = 0; k < E; k++) x[k] = u128_from(io[tid * E + k]);
 #pragma unroll
     for (int k = 0; k < E / 2; k++) w[k] = u128_from(tw[k]);
+    constexpr int RB = E == 2 ? 1 : (E == 4 ? 2 : 3);   // stages per register round
     for (int it = 0; it < iters; it++) {
 #pragma unroll
-        for (int bit = 0; bit < 3; bit++) {
+        for (int bit = 0; bit < RB; bit++) {
 #pragma unroll
             for (int kk = 0; kk < E / 2; kk++) {
                 const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
@@ -124,8 +125,22 @@ int main() {
             launch(); CK(cudaDeviceSynchronize());
             float best = 1e30f;
             for (int r = 0; r < 3; r++) { cudaEventRecord(e0); launch(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms); }
-            double bf = (double)threads * blocks * iters * 3 * (E / 2);
+            double bf = (double)threads * blocks * iters * (E == 4 ? 2 : 3) * (E / 2);
             printf("{\"q125_variant\":%d,\"bfly_per_clk_sm_at1965\":%.3f}\n", v, bf / (best * 1e-3) / (sms * 1.965e9));
+        }
+        // saturation curve: butterflies/clk/SM against resident warps (8 .. 32 per SM)
+        for (int bpsm : {1, 2, 3, 4}) {
+            const int blocks2 = sms * bpsm;
+            for (int v : {0, 3}) {
+                auto launch = [&]() { if (v == 0) k_bfly<0, E><<<blocks2, threads>>>(d, dtw, dm5, iters, dbad); else k_bfly<3, E><<<blocks2, threads>>>(d, dtw, dm5, iters, dbad); };
+                if (bpsm > 3) { cudaFree(d); CK(cudaMalloc(&d, (size_t)threads * blocks2 * E * 16)); CK(cudaMemset(d, 0, (size_t)threads * blocks2 * E * 16)); }
+                launch(); CK(cudaDeviceSynchronize());
+                float best = 1e30f;
+                for (int r = 0; r < 3; r++) { cudaEventRecord(e0); launch(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms); }
+                double bf = (double)threads * blocks2 * iters * (E == 4 ? 2 : 3) * (E / 2);
+                int occ = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v == 0 ? (const void*)k_bfly<0, E> : (const void*)k_bfly<3, E>, threads, 0);
+                printf("{\"curve_variant\":%d,\"ept\":%d,\"warps_per_sm\":%d,\"occ_blocks\":%d,\"bfly_per_clk_sm_at1965\":%.3f}\n", v, E, bpsm * 8, occ, bf / (best * 1e-3) / (sms * 1.965e9));
+            }
         }
         cudaFree(d);
     }
@@ -143,7 +158,7 @@ int main() {
             unsigned long long hs = 0; for (size_t i = 0; i < n; i++) hs = hs * 1000003ull + res[i].x + 7ull * res[i].w; hsh[v] = hs;
             float best = 1e30f;
             for (int r = 0; r < 3; r++) { cudaEventRecord(e0); launch(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms); }
-            double bf = (double)threads * blocks * iters * 3 * (E / 2);
+            double bf = (double)threads * blocks * iters * (E == 4 ? 2 : 3) * (E / 2);
             printf("{\"variant\":%d,\"blocks_per_sm\":%d,\"ms\":%.4f,\"bfly_per_s\":%.4e,\"bfly_per_clk_sm_at1965\":%.3f}\n", v, bpsm, best, bf / (best * 1e-3), bf / (best * 1e-3) / (sms * 1.965e9));
         }
         printf("{\"blocks_per_sm\":%d,\"hash_equal\":%d}\n", bpsm, hsh[0] == hsh[1] && hsh[0] == hsh[2] && hsh[0] == hsh[3]);
