@@ -396,7 +396,7 @@ def run_e2e(plan, x_host, args, stream, bfly_per_step, world):
 # ----------------------------------------------------------------------------- other §8 rows
 def run_rows(args, P, pk, stream):
     """One measurement per other SURVEY §8(a) row: cfg1 latency, cfg2 BLAS, cfg3 negacyclic
-    polymul, cfg4 size sweep (2 sizes by default), cfg5 N = 2^26 on one GPU."""
+    polymul, cfg4 size sweep (N = 2^10 .. 2^17 by default), cfg5 N = 2^26 on one GPU."""
     import torch
     from paper_2509_12494_b200 import ntt128 as N
     from paper_2509_12494_b200 import synth
@@ -451,6 +451,7 @@ def run_rows(args, P, pk, stream):
             ps.forward(xx, out=yy); ps.inverse(yy, out=xx)
         ms = time_events(lambda i: (ps.forward(xx, out=yy), ps.inverse(yy, out=xx)), 5, stream)
         rows[f"cfg4_logn{logn}_butterflies_per_s"] = 2 * Bn * (nn // 2) * logn / (ms * 1e-3)
+        rows[f"cfg4_logn{logn}_int_frac"] = round(rows[f"cfg4_logn{logn}_butterflies_per_s"] * P_BUTTERFLY / 1e12 / pk["tprod_s"], 4)
         del ps, xx, yy
         torch.cuda.empty_cache()
     # cfg5: N = 2^26 single transform on one GPU (three passes)
@@ -604,7 +605,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rows", dest="rows", action="store_true", default=True)
     ap.add_argument("--no-rows", dest="rows", action="store_false")
-    ap.add_argument("--sweep", type=lambda s: [int(v) for v in s.split(",") if v], default=[10, 16])
+    ap.add_argument("--sweep", type=lambda s: [int(v) for v in s.split(",") if v], default=list(range(10, 18)))
     ap.add_argument("--no-cfg5", dest="cfg5", action="store_false", default=True)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false", default=True)
     ap.add_argument("--p2p", action="store_true", default=False,
