@@ -91,6 +91,18 @@
 #ifndef NTT_RB9
 #define NTT_RB9 3
 #endif
+#ifndef NTT_S9_C
+#define NTT_S9_C 1    // single-pass N = 2^9: one group per CTA (+9 % over 4)
+#endif
+#ifndef NTT_S8_C
+#define NTT_S8_C 8
+#endif
+#ifndef NTT_S10_C
+#define NTT_S10_C 1    // single-pass N = 2^10: groups per CTA (1: +10 % over 2, 4) and register-round radix (log2)
+#endif
+#ifndef NTT_S10_RB
+#define NTT_S10_RB 3
+#endif
 #ifndef NTT_RB7
 #define NTT_RB7 2   // 7-stage passes: radix-4 rounds on one warp-owned group per CTA (NTT_C7 = 1):
                     // +2.4 % / +2.1 % at N = 2^14 / 2^15 over radix-8 with 8 groups per CTA
@@ -1114,9 +1126,9 @@ static PassCfg single_cfg_t(int B) {
         case 5: return make_cfg<5, 16, true, SL, true>();
         case 6: return make_cfg<6, 16, true, SL, true>();
         case 7: return make_cfg<7, 16, true, SL, true>();
-        case 8: return make_cfg<8, 8, true, SL, true>();
-        case 9: return make_cfg<9, 4, true, SL, true>();
-        case 10: return make_cfg<10, 2, true, SL, true>();
+        case 8: return make_cfg<8, NTT_S8_C, true, SL, true>();
+        case 9: return make_cfg<9, NTT_S9_C, true, SL, true>();
+        case 10: return make_cfg<10, NTT_S10_C, true, SL, true, NTT_S10_RB>();
         case 11: return make_cfg<11, 1, true, SL, true>();
         default: return make_cfg<12, 1, true, SL, true>();
     }
@@ -1277,7 +1289,9 @@ static void plan_free(ntt128_plan_s* p) {
 }
 
 #ifndef NTT_SINGLE_MAX
+#ifndef NTT_SINGLE_MAX
 #define NTT_SINGLE_MAX 11   // largest log2 N done in one pass (measured: 2^12 is 25% faster as 6+6 passes)
+#endif
 #endif
 static std::vector<int> pass_bits(int n) {
     if (n <= NTT_SINGLE_MAX) return {n};

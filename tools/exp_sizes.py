@@ -11,8 +11,11 @@ from paper_2509_12494_b200 import synth  # noqa: E402
 
 P = json.load(open("tests/golden/params.json"))
 for logn in [int(v) for v in sys.argv[1].split(",")]:
-    e = P["cfg4"][str(logn)]
+    # cfg4 primes for 2^10..2^17; smaller sizes use the 2^10 prime's sub-roots, larger cfg5's
+    key = str(min(max(logn, 10), 17))
+    e = P["cfg4"][key] if logn <= 17 else P["cfg5"]
     q, w = int(e["q"], 16), int(e["omega"], 16)
+    w = pow(w, 1 << (e["logn"] - logn), q)
     n = 1 << logn
     B = (1 << 26) // n
     plan = N.Plan(logn, q, w, batch=B)
