@@ -988,7 +988,10 @@ k_nc_pass(const PassArgs a) {
 // Every twiddle a thread uses (LM + 3 of them) is loaded into registers before the
 // dependency wait.  Values stay canonical (any odd q < 2^128).
 #include <cooperative_groups.h>
-constexpr int CLU_LOG = 3, CLU = 1 << CLU_LOG;
+#ifndef NTT_CLU_LOG
+#define NTT_CLU_LOG 3    // log2 CTAs per cluster (8: portable cluster size)
+#endif
+constexpr int CLU_LOG = NTT_CLU_LOG, CLU = 1 << CLU_LOG;
 
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
@@ -1723,6 +1726,7 @@ static ntt128_status run_cluster(ntt128_plan_s* p, const uint4* src, uint4* dst,
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 2 : 1;
     const PassKernel fn = scale_last ? cluster_fn<true>(n) : cluster_fn<false>(n);
+    if (CLU > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (cudaLaunchKernelEx(&cfg, fn, a) != cudaSuccess) return NTT128_ERR_CUDA;
     ntt128_count_launch(1);
     return NTT128_OK;
