@@ -223,6 +223,29 @@ __global__ void k_gather_pass_tw(uint4* out, uint64_t out_stride, const uint4* T
     }
 }
 
+// Shoup form of a pass table for the lazy-class moduli (q < 2^126; MODE_LAZY_S): each
+// Montgomery-form entry w R becomes plain w = mont(w R, 1), its companion floor(w 2^128 / q)
+// by restoring division; the other moduli's rows are left as they are.
+__global__ void k_shoup_table(uint4* t, uint4* tp, uint64_t stride, const ModC* mods) {
+    const int m = blockIdx.y;
+    const ModC& M = mods[m];
+    if ((M.q[3] >> 30) != 0) return;
+    const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+    const unsigned __int128 qq = ((unsigned __int128)(((uint64_t)q[3] << 32) | q[2]) << 64) | (((uint64_t)q[1] << 32) | q[0]);
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < stride; e += (uint64_t)gridDim.x * blockDim.x) {
+        const U128 pl = mont_mul(u128_from(t[m * stride + e]), U128{{1, 0, 0, 0}}, q, M.qinv0);
+        unsigned __int128 r = ((unsigned __int128)(((uint64_t)pl.w[3] << 32) | pl.w[2]) << 64) | (((uint64_t)pl.w[1] << 32) | pl.w[0]);
+        unsigned __int128 quo = 0;
+        for (int i = 0; i < 128; i++) {     // r < q < 2^126: 2r fits
+            r <<= 1;
+            quo <<= 1;
+            if (r >= qq) { r -= qq; quo |= 1; }
+        }
+        t[m * stride + e] = u128_to(pl);
+        tp[m * stride + e] = make_uint4((uint32_t)quo, (uint32_t)(quo >> 32), (uint32_t)(quo >> 64), (uint32_t)(quo >> 96));
+    }
+}
+
 // Permutation-free negacyclic pass tables: out[m][H][k], k < 2^B - 1, local stage
 // sl = B - 1 - floor(log2(k + 1)), block i = H 2^(B-1-sl) + (k - (2^(B-1-sl) - 1)),
 // global stage b = lo + sl: psi^e (forward) or psi^-e (inverse), e = brev_n(2^(n-1-b) + i),
@@ -265,6 +288,8 @@ struct PassArgs {
     uint4* dst;            // [batch][N]
     const uint4* pmul;     // optional point-wise multiplicand, same layout as src (Montgomery product)
     const uint4* pt;       // [nq][pt_stride] pass twiddles in consumption order: [L][k], k < 2^B - 1
+    const uint4* pts;      // optional, same layout: Shoup companions floor(w 2^128 / q); where given,
+                           // the lazy-class moduli's entries of `pt` are plain (not Montgomery form)
     const uint4* fin;      // optional [nq][f_stride]: factor applied at load, by natural input index
     const uint4* fout;     // optional [nq][f_stride]: factor applied at store, by natural output index
     const ModC* mods;      // [nq]
@@ -342,7 +367,12 @@ __device__ __forceinline__ int slot(int l) {
 //   MODE_LAZY (q < 2^126): values in [0, 4q), Harvey butterflies, lazy Montgomery.
 // Single-pass CTAs (one CTA may hold several moduli) and the last pass's store keep the
 // interface canonical.
-enum { MODE_FULL = 0, MODE_HALF = 1, MODE_LAZY = 2 };
+enum { MODE_FULL = 0, MODE_HALF = 1, MODE_LAZY = 2, MODE_LAZY_S = 3 };
+// MODE_LAZY_S: the lazy class with Shoup products by plain twiddles and their companions
+// (8-stage multi-pass kernels, NTT_SHOUP).
+#ifndef NTT_SHOUP
+#define NTT_SHOUP 0           // 0: off (measured slower in the pass kernel), 1: every 8-stage multi-pass pass, 2: first passes only
+#endif
 #ifndef NTT_FORCE_FULL
 #define NTT_FORCE_FULL 0      // 1: canonical arithmetic for every modulus (experiment)
 #endif
@@ -372,6 +402,16 @@ __device__ __forceinline__ void bfly(U128& u, U128& v, const U128& w, const uint
         u = add_nored(us, t);
         v = sub_add_nored(us, t, q2);
     }
+}
+// Harvey butterfly of the lazy class with a Shoup product: u, v in [0, 4q); w plain, wp its
+// companion; t = v w mod q in [0, 2q); u' = u mod 2q + t, v' = u mod 2q - t + 2q.
+template <bool SCALE_U>
+__device__ __forceinline__ void bfly_s(U128& u, U128& v, const U128& w, const U128& wp, const uint32_t q[4],
+                                       const uint32_t q2[4], const uint32_t qn[4], uint32_t qinv0, const U128& nf) {
+    const U128 us = SCALE_U ? mont_mul_lazy(u, nf, q, qinv0) : reduce_2q(u, q2);
+    const U128 t = shoup_mul_lazy(v, w, wp, qn, q2);
+    u = add_nored(us, t);
+    v = sub_add_nored(us, t, q2);
 }
 // Stage with twiddle 1 (first stage of a first pass): inputs canonical (< q).
 template <int MODE>
@@ -412,10 +452,10 @@ __device__ __forceinline__ void bfly_tw1(U128& u, U128& v, const uint32_t q[4], 
 // R0: the first round of a first pass (w = 0, global stage = local stage), peeled so the
 // butterflies with twiddle index j = 0 (twiddle 1: all of stage 0, half of stage 1, a
 // quarter of stage 2) skip their multiply at compile time.
-template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL, bool R0>
+template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL, bool R0, int TSP = 0>
 __device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4* tws, const int t, const uint32_t lo,
                                            const uint32_t n, const uint32_t q[4], const uint32_t q2[4],
-                                           const uint32_t qinv0, const U128& nf) {
+                                           const uint32_t qinv0, const U128& nf, const uint32_t* qn = nullptr) {
     using S = PassShape<B, RBMAX, C, PADL>;
     constexpr int RB = S::RB, E = S::E;
     const int slo = R0 ? 0 : rd * RB;
@@ -442,14 +482,22 @@ __device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4
         }
         const uint4* tp = tws + tlo + ((1 << sl) - 1);
         U128 tw[E / 2];                              // the first 2^bit are used
+        U128 twp[MODE == MODE_LAZY_S ? E / 2 : 1];   // Shoup companions (MODE_LAZY_S)
 #pragma unroll
-        for (int j = 0; j < (1 << bit); j++) tw[j] = u128_from(tp[j << w]);
+        for (int j = 0; j < (1 << bit); j++) {
+            tw[j] = u128_from(tp[j << w]);
+            if (MODE == MODE_LAZY_S) twp[MODE == MODE_LAZY_S ? j : 0] = u128_from(tp[(j << w) + TSP]);
+        }
 #pragma unroll
         for (int kk = 0; kk < E / 2; kk++) {
             const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
             const int k1 = k0 | (1 << bit);
             const int j = kk & ((1 << bit) - 1);
             if (R0 && j == 0 && !last) bfly_tw1<MODE>(x[k0], x[k1], q, q2);
+            else if (MODE == MODE_LAZY_S) {
+                if (last) bfly_s<true>(x[k0], x[k1], tw[j], twp[MODE == MODE_LAZY_S ? j : 0], q, q2, qn, qinv0, nf);
+                else bfly_s<false>(x[k0], x[k1], tw[j], twp[MODE == MODE_LAZY_S ? j : 0], q, q2, qn, qinv0, nf);
+            }
             else if (last) bfly<MODE, true>(x[k0], x[k1], tw[j], q, q2, qinv0, nf);
             else bfly<MODE, false>(x[k0], x[k1], tw[j], q, q2, qinv0, nf);
         }
@@ -459,7 +507,7 @@ __device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4
     if (WARPSYNC) __syncwarp(); else __syncthreads();
 }
 
-template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL>
+template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL, int TSP = 0>
 __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
                                             const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
     uint32_t q2[4] = {0, 0, 0, 0};
@@ -469,15 +517,20 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
         q2[2] = (q[2] << 1) | (q[1] >> 31);
         q2[3] = (q[3] << 1) | (q[2] >> 31);
     }
+    uint32_t qn[4] = {0, 0, 0, 0};                  // 2^128 - q (Shoup remainders)
+    if (MODE == MODE_LAZY_S) {
+        asm("sub.cc.u32 %0, 0, %4;\n\t subc.cc.u32 %1, 0, %5;\n\t subc.cc.u32 %2, 0, %6;\n\t subc.u32 %3, 0, %7;"
+            : "=r"(qn[0]), "=r"(qn[1]), "=r"(qn[2]), "=r"(qn[3]) : "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]));
+    }
     using S = PassShape<B, RBMAX, C, PADL>;
     constexpr int rd0 = FIRST ? 1 : 0;
     if (FIRST)
-        round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, true>(0, gsm, tws, t, lo, n, q, q2, qinv0, nf);
+        round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, true, TSP>(0, gsm, tws, t, lo, n, q, q2, qinv0, nf, qn);
     if (S::RB == 2 && PADL && NTT_RB2_UNROLL) {
         // radix-4 rounds: unrolled, so every window and XOR-swizzle offset is a constant
 #pragma unroll
         for (int rd = rd0; rd < S::ROUNDS; rd++)
-            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf);
+            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false, TSP>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf, qn);
     } else {
 #if NTT_UNROLL_ROUNDS
 #pragma unroll
@@ -485,7 +538,7 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
 #pragma unroll 1
 #endif
         for (int rd = rd0; rd < S::ROUNDS; rd++)
-            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf);
+            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false, TSP>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf, qn);
     }
 }
 
@@ -507,8 +560,10 @@ k_ntt_pass(const PassArgs a) {
     constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS, TS = S::TS;
     constexpr int NT = C * T;
     constexpr int NTW = (FIRST && !SINGLE) ? 1 : C;  // twiddle sets: a multi-pass first pass shares one (L = 0)
+    constexpr bool SHOUPK = NTT_SHOUP && !SINGLE && B == 8 && (NTT_SHOUP == 1 || FIRST);   // lazy-class Shoup products (MODE_LAZY_S)
+    constexpr int TSP = NTW * TS;                    // companion sets follow the twiddle sets
     extern __shared__ uint4 sm[];
-    uint4* tsm = sm + C * GS;                        // [NTW][TS] pass-local twiddles
+    uint4* tsm = sm + C * GS;                        // [NTW][TS] pass-local twiddles (+ [NTW][TS] companions)
 
     const uint32_t n = a.n, lo = a.lo, gbits = n - B;
     const uint64_t N = 1ull << n;
@@ -555,6 +610,15 @@ k_ntt_pass(const PassArgs a) {
                 for (int i = 0; i < TW_IT; i++)
                     if ((G - 1) % NT == 0 || i + 1 < TW_IT || tid + i * NT < G - 1)
                         cp_async16(dst + c * TS + i * NT, src + c * (G - 1) + i * NT);
+            if (SHOUPK && a.pts && (a.mods[m0].q[3] >> 30) == 0) {   // lazy class: the companions too
+                const uint4* srcp = a.pts + m0 * a.pt_stride + L0 * (G - 1) + tid;
+#pragma unroll
+                for (int c = 0; c < NTW; c++)
+#pragma unroll
+                    for (int i = 0; i < TW_IT; i++)
+                        if ((G - 1) % NT == 0 || i + 1 < TW_IT || tid + i * NT < G - 1)
+                            cp_async16(dst + TSP + c * TS + i * NT, srcp + c * (G - 1) + i * NT);
+            }
         } else {   // single pass, C polynomials per CTA, each with its own modulus
             constexpr int TW_PER = (NTW * (G - 1) + NT - 1) / NT;
 #pragma unroll
@@ -673,7 +737,9 @@ k_ntt_pass(const PassArgs a) {
 #pragma unroll 1
         for (int rep = 0; rep < NTT_COMPUTE_REPEAT; rep++)
 #endif
-        if (mode == MODE_LAZY)
+        if (SHOUPK && mode == MODE_LAZY && a.pts)
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, SHOUPK ? MODE_LAZY_S : MODE_LAZY, WARPMAP, PADL, TSP>(gsm, tws, t, lo, n, q, qinv0, nf);
+        else if (mode == MODE_LAZY)
             pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
         else if (mode == MODE_HALF)
             pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_HALF, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
@@ -1114,7 +1180,8 @@ static PassCfg make_cfg() {
     c.B = B;
     c.C = C;
     c.threads = C * S::T;
-    c.smem = ((size_t)C * S::GS + (size_t)((FIRST && !SINGLE) ? 1 : C) * S::TS) * sizeof(uint4);
+    const size_t ntw = (size_t)((FIRST && !SINGLE) ? 1 : C) * S::TS;
+    c.smem = ((size_t)C * S::GS + ntw * ((NTT_SHOUP && !SINGLE && B == 8 && (NTT_SHOUP == 1 || FIRST)) ? 2 : 1)) * sizeof(uint4);
     return c;
 }
 
@@ -1236,6 +1303,8 @@ struct ntt128_plan_s {
     std::vector<u128> q_host;
     int* d_err = nullptr;
     std::vector<uint4*> d_pt_fwd, d_pt_inv, d_pt_inv_r;  // per pass, [nq][pt_stride]
+    std::vector<uint4*> d_ps_fwd, d_ps_inv, d_ps_inv_r;  // per pass: Shoup companions (8-stage multi-pass passes
+                                                         // of plans with lazy-class moduli), else nullptr
     // permutation-free negacyclic path (n >= 10): pass widths bottom-up, per-pass tables
     // [nq][2^(n - lo - B)][2^B - 1] (psi, psi^-1; the top inverse pass N^-1 / N^-1 R scaled)
     std::vector<int> nc_bits;
@@ -1286,6 +1355,11 @@ static void plan_free(ntt128_plan_s* p) {
         if (p->d_pt_inv_r[i] != p->d_pt_inv[i]) cudaFree(p->d_pt_inv_r[i]);
         cudaFree(p->d_pt_fwd[i]);
         cudaFree(p->d_pt_inv[i]);
+    }
+    for (size_t i = 0; i < p->d_ps_fwd.size(); i++) {
+        if (p->d_ps_inv_r[i] != p->d_ps_inv[i]) cudaFree(p->d_ps_inv_r[i]);
+        cudaFree(p->d_ps_fwd[i]);
+        cudaFree(p->d_ps_inv[i]);
     }
     cudaSetDevice(prev);
     delete p;
@@ -1477,6 +1551,8 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
     if (st == NTT128_OK) {
         int lo = 0;
         const size_t np = p->bits.size();
+        bool any_lazy = false;
+        for (uint32_t m = 0; m < n_moduli; m++) any_lazy = any_lazy || (qs[m] >> 126) == 0;
         for (size_t i = 0; i < np && st == NTT128_OK; i++) {
             const int b = p->bits[i];
             const uint64_t stride = ((uint64_t)1 << lo) * (((uint64_t)1 << b) - 1);
@@ -1500,6 +1576,23 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
             if (vr != v) k_gather_pass_tw<<<grid, 256>>>(vr, stride, p->d_tw_inv, p->d_tw_inv_last_r, half, log2n, lo, b);
             ntt128_count_launch(vr != v ? 3 : 2);
             if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = NTT128_ERR_CUDA;
+            // 8-stage passes of multi-pass plans: Shoup form for the lazy-class moduli
+            uint4 *sf = nullptr, *sv = nullptr, *svr = nullptr;
+            if (st == NTT128_OK && NTT_SHOUP && np > 1 && b == 8 && any_lazy && (NTT_SHOUP == 1 || i == 0)) {
+                if (cudaMalloc(&sf, bytes) != cudaSuccess || cudaMalloc(&sv, bytes) != cudaSuccess ||
+                    (vr != v && cudaMalloc(&svr, bytes) != cudaSuccess)) st = NTT128_ERR_OOM;
+                if (!svr) svr = sv;
+                if (st == NTT128_OK) {
+                    k_shoup_table<<<grid, 256>>>(f, sf, stride, p->d_mods);
+                    k_shoup_table<<<grid, 256>>>(v, sv, stride, p->d_mods);
+                    if (vr != v) k_shoup_table<<<grid, 256>>>(vr, svr, stride, p->d_mods);
+                    ntt128_count_launch(vr != v ? 3 : 2);
+                    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = NTT128_ERR_CUDA;
+                }
+            }
+            p->d_ps_fwd.push_back(sf);
+            p->d_ps_inv.push_back(sv);
+            p->d_ps_inv_r.push_back(svr);
             lo += b;
         }
         // permutation-free negacyclic tables (ntt128_forward_bitrev / inverse_bitrev, polymul)
@@ -1773,6 +1866,7 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
         a.lo = (uint32_t)lo;
         a.nq = p->nq;
         a.pt = !o.inverse ? p->d_pt_fwd[i] : (o.polymul ? p->d_pt_inv_r[i] : p->d_pt_inv[i]);
+        a.pts = !o.inverse ? p->d_ps_fwd[i] : (o.polymul ? p->d_ps_inv_r[i] : p->d_ps_inv[i]);
         const bool first = i == 0, last = i + 1 == npass;
         if (first && o.pmul) a.pmul = o.pmul;
         if (scale_last && last) a.ninv_r = o.polymul ? 1 : 0;
