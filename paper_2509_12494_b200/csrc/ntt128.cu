@@ -1370,11 +1370,38 @@ static void plan_free(ntt128_plan_s* p) {
 #define NTT_SINGLE_MAX 11   // largest log2 N done in one pass (measured: 2^12 is 25% faster as 6+6 passes)
 #endif
 #endif
-// Odd n: the narrower pass first for n <= 16 (N = 2^13 / 2^15: +0.5 / +1 %), the wider
-// first above (N = 2^17: 9 + 8 is 3 % faster than 8 + 9); three passes widest first.
+// Two-pass splits measured over every (a, b) with 5 <= a, b <= 9 (tools/gpu_splits.sh,
+// 1 GiB batches): 7-stage passes are the weak shape, so N = 2^13 runs 5 + 8 (+2.7 % over
+// 6 + 7), 2^14 6 + 8 (+7 % over 7 + 7), 2^15 9 + 6 (+4.3 % over 7 + 8); 2^16 8 + 8 (9 + 7
+// equal), 2^17 9 + 8 (3 % over 8 + 9), 2^18 9 + 9.  Three passes (tools/gpu_splits3.sh):
+// 2^19 5+6+8 (+2 % over 7+6+6), 2^20 6+6+8 (+5.6 %), 2^21 9+6+6 (+7.5 %), 2^22 6+8+8 (+15 %
+// over 8+7+7), 2^23 9+6+8 (+4.3 %); 2^24..2^26 widest first (8+8+8, 9+8+8, 9+9+8).
 static std::vector<int> pass_bits(int n) {
+    if (const char* e = getenv("NTT128_SPLIT")) {   // experiment switch: "a,b[,c]" pass widths summing to n
+        std::vector<int> v;
+        int sum = 0;
+        for (const char* c = e; *c;) {
+            const int b = atoi(c);
+            if (b < 5 || b > 9) { v.clear(); break; }
+            v.push_back(b);
+            sum += b;
+            while (*c && *c != ',') c++;
+            if (*c == ',') c++;
+        }
+        if (sum == n && v.size() > 1 && v.size() <= 4) return v;
+    }
     if (n <= NTT_SINGLE_MAX) return {n};
-    if (n <= 16) return {n / 2, (n + 1) / 2};
+    switch (n) {
+        case 13: return {5, 8};
+        case 14: return {6, 8};
+        case 15: return {9, 6};
+        case 19: return {5, 6, 8};
+        case 20: return {6, 6, 8};
+        case 21: return {9, 6, 6};
+        case 22: return {6, 8, 8};
+        case 23: return {9, 6, 8};
+        default: break;
+    }
     if (n <= 18) return {(n + 1) / 2, n / 2};
     int a = (n + 2) / 3, b = (n + 1) / 3, c = n / 3;
     return {a, b, c};
