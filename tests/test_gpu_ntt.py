@@ -72,8 +72,10 @@ def test_two_pass_sizes(N, params, logn):
         run_cyclic(N, e["q"], sub_root(e, logn), logn, 2, 200 + logn)
 
 
-@pytest.mark.parametrize("logn", [19, 20])
+@pytest.mark.parametrize("logn", [19, 20, 21, 22])
 def test_three_pass_sizes(N, params, logn):
+    """three-pass splits of the measured table (5+6+8, 6+6+8, 9+6+6, 6+8+8; 2^23 = 9+6+8 is
+    covered by the same kernels at N = 2^15 and 2^23 round trips in tools/exp_sizes.py)"""
     e = params["cfg5"]
     run_cyclic(N, e["q"], sub_root(e, logn), logn, 1, 300 + logn)
 
