@@ -74,10 +74,26 @@ def test_two_pass_sizes(N, params, logn):
 
 @pytest.mark.parametrize("logn", [19, 20, 21, 22])
 def test_three_pass_sizes(N, params, logn):
-    """three-pass splits of the measured table (5+6+8, 6+6+8, 9+6+6, 6+8+8; 2^23 = 9+6+8 is
-    covered by the same kernels at N = 2^15 and 2^23 round trips in tools/exp_sizes.py)"""
+    """three-pass splits of the measured table (5+6+8, 6+6+8, 9+6+6, 6+8+8)"""
     e = params["cfg5"]
     run_cyclic(N, e["q"], sub_root(e, logn), logn, 1, 300 + logn)
+
+
+def test_three_pass_2_23_sampled(N, params):
+    """N = 2^23 (split 9+6+8): sampled outputs by direct O(N) evaluation of Eq. ntt and the
+    exact round trip"""
+    import torch
+    e = params["cfg5"]
+    q, w = e["q"], sub_root(e, 23)
+    n = 1 << 23
+    x = synth.uniform_residues(q, n, 323).reshape(1, n, 2)
+    plan = N.Plan(23, q, w)
+    dx = to_dev(x)
+    dy = plan.forward(dx)
+    y = to_host(dy)
+    for k in [0, 1, n // 2, n - 1, 1234567]:
+        assert synth.to_ints(y[0, k:k + 1])[0] == O.ntt_eval(x[0], q, w, k), f"y[{k}]"
+    assert torch.equal(plan.inverse(dy), dx)
 
 
 def test_small_moduli(N, params):
