@@ -1801,10 +1801,12 @@ static void set_overlap(ntt128_plan_s* p, ntt128_plan_s::StreamCtr* ctr, PassArg
     if (i + 1 < npass) a.cnt_out = ctr->d + i * (size_t)p->batch;
 }
 
-// Cluster latency path (k_ntt_cluster): cyclic single-pass plans, N = 2^8 .. 2^11, at most
-// NTT_CLU_MAX_BATCH polynomials (8 CTAs each).
+// Cluster path (k_ntt_cluster): cyclic single-pass plans, N = 2^8 .. 2^11, at most
+// NTT_CLU_MAX_BATCH polynomials (8 CTAs each).  Measured at N = 2^10 (fwd+inv, graph
+// replay, tools/exp_cluster_batch.py): clusters win up to 512 polynomials (B = 64: 9.2 vs
+// 14.4 us, B = 512: 45 vs 58 us) and lose at 1024 (85 vs 72 us) to the batched pass.
 #ifndef NTT_CLU_MAX_BATCH
-#define NTT_CLU_MAX_BATCH 16
+#define NTT_CLU_MAX_BATCH 512
 #endif
 static bool use_cluster(const ntt128_plan_s* p, const RunOpts& o) {
     if (switches().no_cluster || p->kind != 0 || o.pmul || p->bits.size() != 1) return false;

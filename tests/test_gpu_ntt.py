@@ -272,9 +272,20 @@ def test_cfg5_direct_three_pass(N, params):
 
 @pytest.mark.parametrize("logn", [8, 9, 10, 11])
 def test_cluster_latency_path(N, params, logn):
-    """few polynomials at N = 2^8 .. 2^11 run on 8-CTA clusters (distributed shared
-    memory exchange between the in-CTA stages and the last three); batch 17 is past the
-    cluster threshold (the one-CTA-per-polynomial shape), all moduli classes, in place"""
+    """up to 512 polynomials at N = 2^8 .. 2^11 run on 8-CTA clusters (distributed shared
+    memory exchange between the in-CTA stages and the last three): one to 17 polynomials
+    with distinct primes of all classes, in place, and 600 polynomials past the threshold
+    (the batched single pass) against 512 at it"""
+    e = params["extra"]["rand128_0"]
+    q, w = e["q"], sub_root(e, logn)
+    n = 1 << logn
+    xb = synth.uniform_residues(q, n * 600, 4000 + logn).reshape(600, n, 2)
+    ref = O.ntt(xb, [q] * 600, [w] * 600)
+    for B in (512, 600):
+        plan = N.Plan(logn, q, w, batch=B)
+        y = to_host(plan.forward(to_dev(xb[:B])))
+        assert np.array_equal(y, ref[:B]), f"B={B}"
+        assert np.array_equal(to_host(plan.inverse(to_dev(y))), xb[:B]), f"B={B}"
     mods = params["cfg3"]["moduli"][:17]
     for B in (1, 5, 16, 17):
         qs = [m["q"] for m in mods[:B]]
