@@ -160,7 +160,7 @@ def cfg3_inputs(P, rank, nsets):
     qs = [hexint(m["q"]) for m in mods]
     ws = [hexint(m["omega"]) for m in mods]
     psis = [hexint(m["psi"]) for m in mods]
-    from paper_2509_12494_b200 import synth
+    import synth
     n = 1 << P["cfg3"]["logn"]
     sets = []
     for s in range(nsets):
@@ -399,7 +399,7 @@ def run_rows(args, P, pk, stream):
     polymul, cfg4 size sweep (N = 2^10 .. 2^17 by default), cfg5 N = 2^26 on one GPU."""
     import torch
     from paper_2509_12494_b200 import ntt128 as N
-    from paper_2509_12494_b200 import synth
+    import synth
     rows = {}
     # cfg1: single N = 1024 forward + inverse (latency)
     e = P["cfg1"]
@@ -499,7 +499,7 @@ def run_cfg5_fourstep(args, P, rank, world):
     each block straight into its destination rank's symmetric-memory receive buffer)."""
     import torch
     from paper_2509_12494_b200 import fourstep as FS
-    from paper_2509_12494_b200 import synth
+    import synth
     e = P["cfg5"]
     q, w = hexint(e["q"]), hexint(e["omega"])
     out = {"cfg5_fourstep_gpus": world}
@@ -551,7 +551,7 @@ def cpu_baseline(P, npolys: int = 16):
     from oracle import oracle as O
     mods = P["cfg3"]["moduli"][:npolys]
     qs, ws = [hexint(m["q"]) for m in mods], [hexint(m["omega"]) for m in mods]
-    from paper_2509_12494_b200 import synth
+    import synth
     n = 1 << P["cfg3"]["logn"]
     x = np.stack([synth.uniform_residues(qs[i], n, synth.stream_seed(3, 0, i)) for i in range(npolys)])
     t0 = time.perf_counter()

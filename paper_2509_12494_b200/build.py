@@ -29,17 +29,22 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()
     """compile csrc/ into `lib`; `defines` are extra -D flags (experiments)"""
     if not force and lib == LIB and not _stale():
         return LIB
-    objs = []
-    logs = []
-    for s in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(s):
         obj = os.path.join(CSRC, s.replace(".cu", "") + ("" if lib == LIB else "_" + os.path.basename(lib)) + ".o")
         cmd = [NVCC, *FLAGS, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, s), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {s}")
-        objs.append(obj)
+        return s, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    logs = []
+    with ThreadPoolExecutor(len(SOURCES)) as ex:   # the sources compile independently
+        for s, obj, r in ex.map(one, SOURCES):
+            logs.append(r.stdout + r.stderr)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {s}")
+            objs.append(obj)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -37,6 +37,9 @@
 #include "arith128.cuh"
 #include "host128.h"
 
+#ifndef NTT128_EXPERIMENTS
+#define NTT128_EXPERIMENTS 0   // 1: experiment build (environment switches; never the product .so)
+#endif
 #ifndef NTT_COMPUTE_REPEAT
 #define NTT_COMPUTE_REPEAT 1  // experiment: run a pass's register rounds k times (0: memory phases only)
 #endif
@@ -223,29 +226,6 @@ __global__ void k_gather_pass_tw(uint4* out, uint64_t out_stride, const uint4* T
     }
 }
 
-// Shoup form of a pass table for the lazy-class moduli (q < 2^126; MODE_LAZY_S): each
-// Montgomery-form entry w R becomes plain w = mont(w R, 1), its companion floor(w 2^128 / q)
-// by restoring division; the other moduli's rows are left as they are.
-__global__ void k_shoup_table(uint4* t, uint4* tp, uint64_t stride, const ModC* mods) {
-    const int m = blockIdx.y;
-    const ModC& M = mods[m];
-    if ((M.q[3] >> 30) != 0) return;
-    const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
-    const unsigned __int128 qq = ((unsigned __int128)(((uint64_t)q[3] << 32) | q[2]) << 64) | (((uint64_t)q[1] << 32) | q[0]);
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < stride; e += (uint64_t)gridDim.x * blockDim.x) {
-        const U128 pl = mont_mul(u128_from(t[m * stride + e]), U128{{1, 0, 0, 0}}, q, M.qinv0);
-        unsigned __int128 r = ((unsigned __int128)(((uint64_t)pl.w[3] << 32) | pl.w[2]) << 64) | (((uint64_t)pl.w[1] << 32) | pl.w[0]);
-        unsigned __int128 quo = 0;
-        for (int i = 0; i < 128; i++) {     // r < q < 2^126: 2r fits
-            r <<= 1;
-            quo <<= 1;
-            if (r >= qq) { r -= qq; quo |= 1; }
-        }
-        t[m * stride + e] = u128_to(pl);
-        tp[m * stride + e] = make_uint4((uint32_t)quo, (uint32_t)(quo >> 32), (uint32_t)(quo >> 64), (uint32_t)(quo >> 96));
-    }
-}
-
 // Permutation-free negacyclic pass tables: out[m][H][k], k < 2^B - 1, local stage
 // sl = B - 1 - floor(log2(k + 1)), block i = H 2^(B-1-sl) + (k - (2^(B-1-sl) - 1)),
 // global stage b = lo + sl: psi^e (forward) or psi^-e (inverse), e = brev_n(2^(n-1-b) + i),
@@ -288,8 +268,6 @@ struct PassArgs {
     uint4* dst;            // [batch][N]
     const uint4* pmul;     // optional point-wise multiplicand, same layout as src (Montgomery product)
     const uint4* pt;       // [nq][pt_stride] pass twiddles in consumption order: [L][k], k < 2^B - 1
-    const uint4* pts;      // optional, same layout: Shoup companions floor(w 2^128 / q); where given,
-                           // the lazy-class moduli's entries of `pt` are plain (not Montgomery form)
     const uint4* fin;      // optional [nq][f_stride]: factor applied at load, by natural input index
     const uint4* fout;     // optional [nq][f_stride]: factor applied at store, by natural output index
     const ModC* mods;      // [nq]
@@ -367,12 +345,7 @@ __device__ __forceinline__ int slot(int l) {
 //   MODE_LAZY (q < 2^126): values in [0, 4q), Harvey butterflies, lazy Montgomery.
 // Single-pass CTAs (one CTA may hold several moduli) and the last pass's store keep the
 // interface canonical.
-enum { MODE_FULL = 0, MODE_HALF = 1, MODE_LAZY = 2, MODE_LAZY_S = 3 };
-// MODE_LAZY_S: the lazy class with Shoup products by plain twiddles and their companions
-// (8-stage multi-pass kernels, NTT_SHOUP).
-#ifndef NTT_SHOUP
-#define NTT_SHOUP 0           // 0: off (measured slower in the pass kernel), 1: every 8-stage multi-pass pass, 2: first passes only
-#endif
+enum { MODE_FULL = 0, MODE_HALF = 1, MODE_LAZY = 2 };
 #ifndef NTT_FORCE_FULL
 #define NTT_FORCE_FULL 0      // 1: canonical arithmetic for every modulus (experiment)
 #endif
@@ -402,16 +375,6 @@ __device__ __forceinline__ void bfly(U128& u, U128& v, const U128& w, const uint
         u = add_nored(us, t);
         v = sub_add_nored(us, t, q2);
     }
-}
-// Harvey butterfly of the lazy class with a Shoup product: u, v in [0, 4q); w plain, wp its
-// companion; t = v w mod q in [0, 2q); u' = u mod 2q + t, v' = u mod 2q - t + 2q.
-template <bool SCALE_U>
-__device__ __forceinline__ void bfly_s(U128& u, U128& v, const U128& w, const U128& wp, const uint32_t q[4],
-                                       const uint32_t q2[4], const uint32_t qn[4], uint32_t qinv0, const U128& nf) {
-    const U128 us = SCALE_U ? mont_mul_lazy(u, nf, q, qinv0) : reduce_2q(u, q2);
-    const U128 t = shoup_mul_lazy(v, w, wp, qn, q2);
-    u = add_nored(us, t);
-    v = sub_add_nored(us, t, q2);
 }
 // Stage with twiddle 1 (first stage of a first pass): inputs canonical (< q).
 template <int MODE>
@@ -452,10 +415,10 @@ __device__ __forceinline__ void bfly_tw1(U128& u, U128& v, const uint32_t q[4], 
 // R0: the first round of a first pass (w = 0, global stage = local stage), peeled so the
 // butterflies with twiddle index j = 0 (twiddle 1: all of stage 0, half of stage 1, a
 // quarter of stage 2) skip their multiply at compile time.
-template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL, bool R0, int TSP = 0>
+template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL, bool R0>
 __device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4* tws, const int t, const uint32_t lo,
                                            const uint32_t n, const uint32_t q[4], const uint32_t q2[4],
-                                           const uint32_t qinv0, const U128& nf, const uint32_t* qn = nullptr) {
+                                           const uint32_t qinv0, const U128& nf) {
     using S = PassShape<B, RBMAX, C, PADL>;
     constexpr int RB = S::RB, E = S::E;
     const int slo = R0 ? 0 : rd * RB;
@@ -482,22 +445,14 @@ __device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4
         }
         const uint4* tp = tws + tlo + ((1 << sl) - 1);
         U128 tw[E / 2];                              // the first 2^bit are used
-        U128 twp[MODE == MODE_LAZY_S ? E / 2 : 1];   // Shoup companions (MODE_LAZY_S)
 #pragma unroll
-        for (int j = 0; j < (1 << bit); j++) {
-            tw[j] = u128_from(tp[j << w]);
-            if (MODE == MODE_LAZY_S) twp[MODE == MODE_LAZY_S ? j : 0] = u128_from(tp[(j << w) + TSP]);
-        }
+        for (int j = 0; j < (1 << bit); j++) tw[j] = u128_from(tp[j << w]);
 #pragma unroll
         for (int kk = 0; kk < E / 2; kk++) {
             const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
             const int k1 = k0 | (1 << bit);
             const int j = kk & ((1 << bit) - 1);
             if (R0 && j == 0 && !last) bfly_tw1<MODE>(x[k0], x[k1], q, q2);
-            else if (MODE == MODE_LAZY_S) {
-                if (last) bfly_s<true>(x[k0], x[k1], tw[j], twp[MODE == MODE_LAZY_S ? j : 0], q, q2, qn, qinv0, nf);
-                else bfly_s<false>(x[k0], x[k1], tw[j], twp[MODE == MODE_LAZY_S ? j : 0], q, q2, qn, qinv0, nf);
-            }
             else if (last) bfly<MODE, true>(x[k0], x[k1], tw[j], q, q2, qinv0, nf);
             else bfly<MODE, false>(x[k0], x[k1], tw[j], q, q2, qinv0, nf);
         }
@@ -507,7 +462,7 @@ __device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4
     if (WARPSYNC) __syncwarp(); else __syncthreads();
 }
 
-template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL, int TSP = 0>
+template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL>
 __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
                                             const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
     uint32_t q2[4] = {0, 0, 0, 0};
@@ -517,20 +472,15 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
         q2[2] = (q[2] << 1) | (q[1] >> 31);
         q2[3] = (q[3] << 1) | (q[2] >> 31);
     }
-    uint32_t qn[4] = {0, 0, 0, 0};                  // 2^128 - q (Shoup remainders)
-    if (MODE == MODE_LAZY_S) {
-        asm("sub.cc.u32 %0, 0, %4;\n\t subc.cc.u32 %1, 0, %5;\n\t subc.cc.u32 %2, 0, %6;\n\t subc.u32 %3, 0, %7;"
-            : "=r"(qn[0]), "=r"(qn[1]), "=r"(qn[2]), "=r"(qn[3]) : "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]));
-    }
     using S = PassShape<B, RBMAX, C, PADL>;
     constexpr int rd0 = FIRST ? 1 : 0;
     if (FIRST)
-        round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, true, TSP>(0, gsm, tws, t, lo, n, q, q2, qinv0, nf, qn);
+        round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, true>(0, gsm, tws, t, lo, n, q, q2, qinv0, nf);
     if (S::RB == 2 && PADL && NTT_RB2_UNROLL) {
         // radix-4 rounds: unrolled, so every window and XOR-swizzle offset is a constant
 #pragma unroll
         for (int rd = rd0; rd < S::ROUNDS; rd++)
-            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false, TSP>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf, qn);
+            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf);
     } else {
 #if NTT_UNROLL_ROUNDS
 #pragma unroll
@@ -538,7 +488,7 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
 #pragma unroll 1
 #endif
         for (int rd = rd0; rd < S::ROUNDS; rd++)
-            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false, TSP>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf, qn);
+            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf);
     }
 }
 
@@ -560,10 +510,8 @@ k_ntt_pass(const PassArgs a) {
     constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS, TS = S::TS;
     constexpr int NT = C * T;
     constexpr int NTW = (FIRST && !SINGLE) ? 1 : C;  // twiddle sets: a multi-pass first pass shares one (L = 0)
-    constexpr bool SHOUPK = NTT_SHOUP && !SINGLE && B == 8 && (NTT_SHOUP == 1 || FIRST);   // lazy-class Shoup products (MODE_LAZY_S)
-    constexpr int TSP = NTW * TS;                    // companion sets follow the twiddle sets
     extern __shared__ uint4 sm[];
-    uint4* tsm = sm + C * GS;                        // [NTW][TS] pass-local twiddles (+ [NTW][TS] companions)
+    uint4* tsm = sm + C * GS;                        // [NTW][TS] pass-local twiddles
 
     const uint32_t n = a.n, lo = a.lo, gbits = n - B;
     const uint64_t N = 1ull << n;
@@ -610,15 +558,6 @@ k_ntt_pass(const PassArgs a) {
                 for (int i = 0; i < TW_IT; i++)
                     if ((G - 1) % NT == 0 || i + 1 < TW_IT || tid + i * NT < G - 1)
                         cp_async16(dst + c * TS + i * NT, src + c * (G - 1) + i * NT);
-            if (SHOUPK && a.pts && (a.mods[m0].q[3] >> 30) == 0) {   // lazy class: the companions too
-                const uint4* srcp = a.pts + m0 * a.pt_stride + L0 * (G - 1) + tid;
-#pragma unroll
-                for (int c = 0; c < NTW; c++)
-#pragma unroll
-                    for (int i = 0; i < TW_IT; i++)
-                        if ((G - 1) % NT == 0 || i + 1 < TW_IT || tid + i * NT < G - 1)
-                            cp_async16(dst + TSP + c * TS + i * NT, srcp + c * (G - 1) + i * NT);
-            }
         } else {   // single pass, C polynomials per CTA, each with its own modulus
             constexpr int TW_PER = (NTW * (G - 1) + NT - 1) / NT;
 #pragma unroll
@@ -737,9 +676,7 @@ k_ntt_pass(const PassArgs a) {
 #pragma unroll 1
         for (int rep = 0; rep < NTT_COMPUTE_REPEAT; rep++)
 #endif
-        if (SHOUPK && mode == MODE_LAZY && a.pts)
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, SHOUPK ? MODE_LAZY_S : MODE_LAZY, WARPMAP, PADL, TSP>(gsm, tws, t, lo, n, q, qinv0, nf);
-        else if (mode == MODE_LAZY)
+        if (mode == MODE_LAZY)
             pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
         else if (mode == MODE_HALF)
             pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_HALF, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
@@ -1181,7 +1118,7 @@ static PassCfg make_cfg() {
     c.C = C;
     c.threads = C * S::T;
     const size_t ntw = (size_t)((FIRST && !SINGLE) ? 1 : C) * S::TS;
-    c.smem = ((size_t)C * S::GS + ntw * ((NTT_SHOUP && !SINGLE && B == 8 && (NTT_SHOUP == 1 || FIRST)) ? 2 : 1)) * sizeof(uint4);
+    c.smem = ((size_t)C * S::GS + ntw) * sizeof(uint4);
     return c;
 }
 
@@ -1301,10 +1238,7 @@ struct ntt128_plan_s {
     uint4* d_f_untwist = nullptr;             // [nq][N]    N^-1 psi^-j            (negacyclic)
     uint4* d_f_untwist_r = nullptr;           // [nq][N]    N^-1 psi^-j R          (negacyclic polymul)
     std::vector<u128> q_host;
-    int* d_err = nullptr;
     std::vector<uint4*> d_pt_fwd, d_pt_inv, d_pt_inv_r;  // per pass, [nq][pt_stride]
-    std::vector<uint4*> d_ps_fwd, d_ps_inv, d_ps_inv_r;  // per pass: Shoup companions (8-stage multi-pass passes
-                                                         // of plans with lazy-class moduli), else nullptr
     // permutation-free negacyclic path (n >= 10): pass widths bottom-up, per-pass tables
     // [nq][2^(n - lo - B)][2^B - 1] (psi, psi^-1; the top inverse pass N^-1 / N^-1 R scaled)
     std::vector<int> nc_bits;
@@ -1318,13 +1252,22 @@ struct ntt128_plan_s {
     // polynomial), so in-stream order makes the targets exact without a reset, for any mix
     // of pass structures, and different streams never share a set.
     static constexpr int MAX_ROWS = 3;                 // passes - 1 of the deepest schedule (4 passes)
+    // At most MAX_STREAMS entries are cached: a further stream evicts the least recently used
+    // entry once the event recorded after that entry's last use has completed (entries used
+    // under stream capture are pinned: a captured graph keeps referring to them).
+    static constexpr int MAX_STREAMS = 8;
     struct StreamCtr {
         uint32_t* d = nullptr;                          // [MAX_ROWS][batch]
         uint32_t expected[MAX_ROWS] = {0, 0, 0};
-        uint4* scratch = nullptr;                       // [2][batch][N]: polymul spectra, in-place copy
+        uint4* scratch = nullptr;                       // polymul spectra [2][batch][N] / in-place copy [batch][N]
+        size_t scratch_elems = 0;
+        cudaEvent_t ev = nullptr;                       // recorded after the last enqueue that used the entry
+        uint64_t tick = 0;                              // LRU clock
+        bool pinned = false;
     };
     std::mutex mu;
     std::unordered_map<unsigned long long, StreamCtr> ctrs;
+    uint64_t tick = 0;
 };
 
 static void plan_free(ntt128_plan_s* p) {
@@ -1340,11 +1283,11 @@ static void plan_free(ntt128_plan_s* p) {
     cudaFree(p->d_f_twist);
     cudaFree(p->d_f_untwist);
     cudaFree(p->d_f_untwist_r);
-    cudaFree(p->d_err);
     cudaFree(p->d_order);
     for (auto& kv : p->ctrs) {
         cudaFree(kv.second.d);
         cudaFree(kv.second.scratch);
+        if (kv.second.ev) cudaEventDestroy(kv.second.ev);
     }
     for (size_t i = 0; i < p->d_nc_fwd.size(); i++) {
         if (p->d_nc_inv_r[i] != p->d_nc_inv[i]) cudaFree(p->d_nc_inv_r[i]);
@@ -1355,11 +1298,6 @@ static void plan_free(ntt128_plan_s* p) {
         if (p->d_pt_inv_r[i] != p->d_pt_inv[i]) cudaFree(p->d_pt_inv_r[i]);
         cudaFree(p->d_pt_fwd[i]);
         cudaFree(p->d_pt_inv[i]);
-    }
-    for (size_t i = 0; i < p->d_ps_fwd.size(); i++) {
-        if (p->d_ps_inv_r[i] != p->d_ps_inv[i]) cudaFree(p->d_ps_inv_r[i]);
-        cudaFree(p->d_ps_fwd[i]);
-        cudaFree(p->d_ps_inv[i]);
     }
     cudaSetDevice(prev);
     delete p;
@@ -1377,6 +1315,7 @@ static void plan_free(ntt128_plan_s* p) {
 // 2^19 5+6+8 (+2 % over 7+6+6), 2^20 6+6+8 (+5.6 %), 2^21 9+6+6 (+7.5 %), 2^22 6+8+8 (+15 %
 // over 8+7+7), 2^23 9+6+8 (+4.3 %); 2^24..2^26 widest first (8+8+8, 9+8+8, 9+9+8).
 static std::vector<int> pass_bits(int n) {
+#if NTT128_EXPERIMENTS
     if (const char* e = getenv("NTT128_SPLIT")) {   // experiment switch: "a,b[,c]" pass widths summing to n
         std::vector<int> v;
         int sum = 0;
@@ -1390,6 +1329,7 @@ static std::vector<int> pass_bits(int n) {
         }
         if (sum == n && v.size() > 1 && v.size() <= 4) return v;
     }
+#endif
     if (n <= NTT_SINGLE_MAX) return {n};
     switch (n) {
         case 13: return {5, 8};
@@ -1526,8 +1466,7 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
         if (cudaMalloc(ptr, (size_t)per * n_moduli * sizeof(uint4)) != cudaSuccess) { st = NTT128_ERR_OOM; return false; }
         return true;
     };
-    if (cudaMalloc(&p->d_mods, n_moduli * sizeof(ModC)) != cudaSuccess ||
-        cudaMalloc(&p->d_err, sizeof(int)) != cudaSuccess) st = NTT128_ERR_OOM;
+    if (cudaMalloc(&p->d_mods, n_moduli * sizeof(ModC)) != cudaSuccess) st = NTT128_ERR_OOM;
     if (st == NTT128_OK && cudaMemcpy(p->d_mods, mc.data(), n_moduli * sizeof(ModC), cudaMemcpyHostToDevice) != cudaSuccess)
         st = NTT128_ERR_CUDA;
     std::vector<u128> scale_ninv(ninv), scale_ninv_r(ninv_r);
@@ -1581,8 +1520,6 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
     if (st == NTT128_OK) {
         int lo = 0;
         const size_t np = p->bits.size();
-        bool any_lazy = false;
-        for (uint32_t m = 0; m < n_moduli; m++) any_lazy = any_lazy || (qs[m] >> 126) == 0;
         for (size_t i = 0; i < np && st == NTT128_OK; i++) {
             const int b = p->bits[i];
             const uint64_t stride = ((uint64_t)1 << lo) * (((uint64_t)1 << b) - 1);
@@ -1606,23 +1543,6 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
             if (vr != v) k_gather_pass_tw<<<grid, 256>>>(vr, stride, p->d_tw_inv, p->d_tw_inv_last_r, half, log2n, lo, b);
             ntt128_count_launch(vr != v ? 3 : 2);
             if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = NTT128_ERR_CUDA;
-            // 8-stage passes of multi-pass plans: Shoup form for the lazy-class moduli
-            uint4 *sf = nullptr, *sv = nullptr, *svr = nullptr;
-            if (st == NTT128_OK && NTT_SHOUP && np > 1 && b == 8 && any_lazy && (NTT_SHOUP == 1 || i == 0)) {
-                if (cudaMalloc(&sf, bytes) != cudaSuccess || cudaMalloc(&sv, bytes) != cudaSuccess ||
-                    (vr != v && cudaMalloc(&svr, bytes) != cudaSuccess)) st = NTT128_ERR_OOM;
-                if (!svr) svr = sv;
-                if (st == NTT128_OK) {
-                    k_shoup_table<<<grid, 256>>>(f, sf, stride, p->d_mods);
-                    k_shoup_table<<<grid, 256>>>(v, sv, stride, p->d_mods);
-                    if (vr != v) k_shoup_table<<<grid, 256>>>(vr, svr, stride, p->d_mods);
-                    ntt128_count_launch(vr != v ? 3 : 2);
-                    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = NTT128_ERR_CUDA;
-                }
-            }
-            p->d_ps_fwd.push_back(sf);
-            p->d_ps_inv.push_back(sv);
-            p->d_ps_inv_r.push_back(svr);
             lo += b;
         }
         // permutation-free negacyclic tables (ntt128_forward_bitrev / inverse_bitrev, polymul)
@@ -1713,13 +1633,21 @@ struct RunOpts {
 
 static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaStream_t stream);
 
-// Experiment switches (A/B measurements in DESIGN.md; defaults are the product behaviour),
-// read once per process: NTT128_NO_PDL (no pass overlap), NTT128_PDL_NOCNT (whole-grid
-// programmatic dependencies only), NTT128_NO_NC (polymul through the natural-order path).
+// Experiment switches (A/B measurements in DESIGN.md).  The product library is built
+// without NTT128_EXPERIMENTS and its behaviour does not depend on the environment; an
+// experiment build (-DNTT128_EXPERIMENTS=1, a separate .so) reads, once per process,
+// NTT128_NO_PDL (no pass overlap), NTT128_PDL_NOCNT (whole-grid programmatic dependencies
+// only), NTT128_NO_NC (polymul through the natural-order path), NTT128_NO_CLUSTER.
 struct Switches {
-    bool no_pdl, pdl_nocnt, no_nc, no_cluster;
-    Switches() : no_pdl(getenv("NTT128_NO_PDL") != nullptr), pdl_nocnt(getenv("NTT128_PDL_NOCNT") != nullptr),
-                 no_nc(getenv("NTT128_NO_NC") != nullptr), no_cluster(getenv("NTT128_NO_CLUSTER") != nullptr) {}
+    bool no_pdl = false, pdl_nocnt = false, no_nc = false, no_cluster = false;
+    Switches() {
+#if NTT128_EXPERIMENTS
+        no_pdl = getenv("NTT128_NO_PDL") != nullptr;
+        pdl_nocnt = getenv("NTT128_PDL_NOCNT") != nullptr;
+        no_nc = getenv("NTT128_NO_NC") != nullptr;
+        no_cluster = getenv("NTT128_NO_CLUSTER") != nullptr;
+#endif
+    }
 };
 static const Switches& switches() {
     static const Switches s;
@@ -1750,6 +1678,51 @@ static cudaError_t launch_pass(const PassCfg& c, const PassArgs& a, uint64_t cta
     return cudaLaunchKernelEx(&cfg, c.fn, a);
 }
 
+// The stream's cache entry (created on first use; `lk` must hold p->mu).  Creating an entry
+// beyond MAX_STREAMS evicts the least recently used unpinned one after its last recorded
+// use has completed on the device.
+static ntt128_plan_s::StreamCtr* stream_entry(ntt128_plan_s* p, unsigned long long sid) {
+    auto it = p->ctrs.find(sid);
+    if (it == p->ctrs.end()) {
+        if (p->ctrs.size() >= (size_t)ntt128_plan_s::MAX_STREAMS) {
+            auto victim = p->ctrs.end();
+            for (auto jt = p->ctrs.begin(); jt != p->ctrs.end(); ++jt)
+                if (!jt->second.pinned && (victim == p->ctrs.end() || jt->second.tick < victim->second.tick)) victim = jt;
+            if (victim != p->ctrs.end()) {
+                if (victim->second.ev) {
+                    cudaEventSynchronize(victim->second.ev);
+                    cudaEventDestroy(victim->second.ev);
+                }
+                cudaFree(victim->second.d);
+                cudaFree(victim->second.scratch);
+                p->ctrs.erase(victim);
+            }
+        }
+        it = p->ctrs.emplace(sid, ntt128_plan_s::StreamCtr()).first;
+    }
+    it->second.tick = ++p->tick;
+    return &it->second;
+}
+// Record the end of this call's use of the stream's entry (or pin it under capture).
+static void stream_touch(ntt128_plan_s* p, cudaStream_t stream) {
+    unsigned long long sid = 0;
+    if (cudaStreamGetId(stream, &sid) != cudaSuccess) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cs);
+    std::lock_guard<std::mutex> lk(p->mu);
+    auto it = p->ctrs.find(sid);
+    if (it == p->ctrs.end()) return;
+    if (cs != cudaStreamCaptureStatusNone) {
+        it->second.pinned = true;
+        return;
+    }
+    if (!it->second.ev && cudaEventCreateWithFlags(&it->second.ev, cudaEventDisableTiming) != cudaSuccess) {
+        it->second.ev = nullptr;
+        it->second.pinned = true;   // cannot prove it idle: never evict
+        return;
+    }
+    cudaEventRecord(it->second.ev, stream);
+}
 // The stream's counter set (allocated and zeroed in stream order on first use); `lk` is
 // locked and stays locked until the caller has enqueued every pass.
 static ntt128_status stream_counters(ntt128_plan_s* p, cudaStream_t stream, std::unique_lock<std::mutex>& lk,
@@ -1757,27 +1730,35 @@ static ntt128_status stream_counters(ntt128_plan_s* p, cudaStream_t stream, std:
     unsigned long long sid = 0;
     if (cudaStreamGetId(stream, &sid) != cudaSuccess) return NTT128_ERR_CUDA;
     lk.lock();
-    ntt128_plan_s::StreamCtr& c = p->ctrs[sid];
+    ntt128_plan_s::StreamCtr& c = *stream_entry(p, sid);
     if (!c.d) {
         const size_t bytes = (size_t)ntt128_plan_s::MAX_ROWS * p->batch * sizeof(uint32_t);
-        if (cudaMalloc(&c.d, bytes) != cudaSuccess) return NTT128_ERR_OOM;
+        if (cudaMalloc(&c.d, bytes) != cudaSuccess) { c.d = nullptr; return NTT128_ERR_OOM; }
         if (cudaMemsetAsync(c.d, 0, bytes, stream) != cudaSuccess) return NTT128_ERR_CUDA;
+        memset(c.expected, 0, sizeof(c.expected));
     }
     *out = &c;
     return NTT128_OK;
 }
-// The stream's scratch (2 x batch x N residues), allocated on first use and kept until the
-// plan is destroyed: no per-call stream-ordered allocation (a memory pool trimmed at a
-// synchronisation would re-grow inside the next call).  Work on one stream is ordered, so
-// consecutive calls may reuse it.
-static ntt128_status stream_scratch(ntt128_plan_s* p, cudaStream_t stream, uint4** out) {
+// The stream's scratch of at least `elems` residues (polymul spectra 2 x batch x N, the
+// in-place copy batch x N), kept with the entry: no per-call stream-ordered allocation (a
+// memory pool trimmed at a synchronisation would re-grow inside the next call).  Work on
+// one stream is ordered, so consecutive calls may reuse it.
+static ntt128_status stream_scratch(ntt128_plan_s* p, cudaStream_t stream, size_t elems, uint4** out) {
     unsigned long long sid = 0;
     if (cudaStreamGetId(stream, &sid) != cudaSuccess) return NTT128_ERR_CUDA;
     std::lock_guard<std::mutex> lk(p->mu);
-    ntt128_plan_s::StreamCtr& c = p->ctrs[sid];
-    if (!c.scratch && cudaMalloc(&c.scratch, 2 * (size_t)p->N * p->batch * sizeof(uint4)) != cudaSuccess) {
+    ntt128_plan_s::StreamCtr& c = *stream_entry(p, sid);
+    if (c.scratch_elems < elems) {
+        // earlier work on this stream may still read the old buffer: cudaFree waits for it
+        cudaFree(c.scratch);
         c.scratch = nullptr;
-        return NTT128_ERR_OOM;
+        c.scratch_elems = 0;
+        if (cudaMalloc(&c.scratch, elems * sizeof(uint4)) != cudaSuccess) {
+            c.scratch = nullptr;
+            return NTT128_ERR_OOM;
+        }
+        c.scratch_elems = elems;
     }
     *out = c.scratch;
     return NTT128_OK;
@@ -1898,7 +1879,6 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
         a.lo = (uint32_t)lo;
         a.nq = p->nq;
         a.pt = !o.inverse ? p->d_pt_fwd[i] : (o.polymul ? p->d_pt_inv_r[i] : p->d_pt_inv[i]);
-        a.pts = !o.inverse ? p->d_ps_fwd[i] : (o.polymul ? p->d_ps_inv_r[i] : p->d_ps_inv[i]);
         const bool first = i == 0, last = i + 1 == npass;
         if (first && o.pmul) a.pmul = o.pmul;
         if (scale_last && last) a.ninv_r = o.polymul ? 1 : 0;
@@ -1974,16 +1954,21 @@ __global__ void k_check_range(const uint4* x, uint64_t per_poly, uint64_t total,
     }
 }
 
+// The error flag is allocated per call in stream order, so concurrent checks on other
+// streams (or threads) never share it.
 static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaStream_t stream) {
-    if (cudaMemsetAsync(p->d_err, 0, sizeof(int), stream) != cudaSuccess) return NTT128_ERR_CUDA;
+    int* d_err = nullptr;
+    if (cudaMallocAsync(&d_err, sizeof(int), stream) != cudaSuccess) return NTT128_ERR_OOM;
+    if (cudaMemsetAsync(d_err, 0, sizeof(int), stream) != cudaSuccess) { cudaFreeAsync(d_err, stream); return NTT128_ERR_CUDA; }
     const uint64_t total = p->N * p->batch;
     unsigned g = (unsigned)((total + 255) / 256);
     if (g > 148 * 16) g = 148 * 16;
-    k_check_range<<<g, 256, 0, stream>>>(src, p->N, total, p->d_mods, p->nq, p->d_err);
+    k_check_range<<<g, 256, 0, stream>>>(src, p->N, total, p->d_mods, p->nq, d_err);
     ntt128_count_launch(1);
     int h = 0;
-    if (cudaMemcpyAsync(&h, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, stream) != cudaSuccess) return NTT128_ERR_CUDA;
-    if (cudaStreamSynchronize(stream) != cudaSuccess) return NTT128_ERR_CUDA;
+    const cudaError_t e = cudaMemcpyAsync(&h, d_err, sizeof(int), cudaMemcpyDeviceToHost, stream);
+    cudaFreeAsync(d_err, stream);
+    if (e != cudaSuccess || cudaStreamSynchronize(stream) != cudaSuccess) return NTT128_ERR_CUDA;
     return h ? NTT128_ERR_INPUT_RANGE : NTT128_OK;
 }
 
@@ -2009,12 +1994,16 @@ static ntt128_status transform(const ntt128_plan_t p, const uint64_t* d_in, uint
         // the first pass gathers bit-reversed columns: it cannot run in place
         const size_t bytes = (size_t)p->N * p->batch * sizeof(uint4);
         uint4* tmp = nullptr;
-        ntt128_status s = stream_scratch(p, stream, &tmp);
+        ntt128_status s = stream_scratch(p, stream, (size_t)p->N * p->batch, &tmp);
         if (s != NTT128_OK) return s;
         if (cudaMemcpyAsync(tmp, src, bytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess) return NTT128_ERR_CUDA;
-        return run_transform(p, tmp, dst, stream, o);
+        s = run_transform(p, tmp, dst, stream, o);
+        stream_touch(p, stream);
+        return s;
     }
-    return run_transform(p, src, dst, stream, o);
+    const ntt128_status s = run_transform(p, src, dst, stream, o);
+    if (p->bits.size() > 1) stream_touch(p, stream);
+    return s;
 }
 
 extern "C" ntt128_status ntt128_forward(const ntt128_plan_t p, const uint64_t* d_in, uint64_t* d_out, ntt128_stream_t stream) {
@@ -2037,7 +2026,7 @@ extern "C" ntt128_status ntt128_polymul(const ntt128_plan_t p, const uint64_t* d
         if (s != NTT128_OK) return s;
     }
     uint4* fa = nullptr;
-    ntt128_status s = stream_scratch(p, stream, &fa);
+    ntt128_status s = stream_scratch(p, stream, 2 * (size_t)p->N * p->batch, &fa);
     if (s != NTT128_OK) return s;
     uint4* fb = fa + (size_t)p->N * p->batch;
     if (!p->nc_bits.empty() && !switches().no_nc) {
@@ -2053,6 +2042,7 @@ extern "C" ntt128_status ntt128_polymul(const ntt128_plan_t p, const uint64_t* d
         RunOpts inv{true, fb, true};
         if (s == NTT128_OK) s = run_transform(p, fa, (uint4*)d_c, stream, inv);
     }
+    stream_touch(p, stream);
     return s;
 }
 
@@ -2067,7 +2057,9 @@ static ntt128_status transform_bitrev(const ntt128_plan_t p, const uint64_t* d_i
         ntt128_status s = check_range(p, (const uint4*)d_in, stream);
         if (s != NTT128_OK) return s;
     }
-    return run_transform_nc(p, (const uint4*)d_in, (uint4*)d_out, stream, inverse, nullptr);
+    const ntt128_status s = run_transform_nc(p, (const uint4*)d_in, (uint4*)d_out, stream, inverse, nullptr);
+    stream_touch(p, stream);
+    return s;
 }
 extern "C" ntt128_status ntt128_forward_bitrev(const ntt128_plan_t p, const uint64_t* d_in, uint64_t* d_out,
                                                ntt128_stream_t stream) {

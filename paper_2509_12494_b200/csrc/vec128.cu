@@ -17,6 +17,10 @@
 #include "barrett128.cuh"
 #include "host128.h"
 
+#ifndef NTT128_EXPERIMENTS
+#define NTT128_EXPERIMENTS 0   // 1: experiment build (environment switches; never the product .so)
+#endif
+
 using namespace ntt128;
 using ntt128h::u128;
 
@@ -99,7 +103,11 @@ int grid_for(uint64_t n) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint64_t want = (n + (uint64_t)THREADS * UNROLL - 1) / ((uint64_t)THREADS * UNROLL);
+#if NTT128_EXPERIMENTS
     static const int per_sm = getenv("NTT128_VEC_CTAS_PER_SM") ? atoi(getenv("NTT128_VEC_CTAS_PER_SM")) : 8;
+#else
+    constexpr int per_sm = 8;
+#endif
     uint64_t cap = (uint64_t)sms * per_sm;  // resident 256-thread CTAs per SM
     if (want > cap) want = cap;
     return want < 1 ? 1 : (int)want;
@@ -125,7 +133,11 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
         if (a >= q) return NTT128_ERR_INPUT_RANGE;
     }
     words(M.to_m(a), c.a_m);
-    static const bool no_barrett = getenv("NTT128_NO_BARRETT") != nullptr;   // experiment switch (A/B)
+#if NTT128_EXPERIMENTS
+    static const bool no_barrett = getenv("NTT128_NO_BARRETT") != nullptr;   // experiment build only (A/B)
+#else
+    constexpr bool no_barrett = false;
+#endif
     const bool barrett = (q >> 127) != 0 && !no_barrett;
     if (barrett) {
         // mu = floor((2^256 - 1) / q) (= floor(2^256 / q), q odd) by restoring division

@@ -14,8 +14,13 @@ import os
 
 import torch
 
+from . import _lib_override
+
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("NTT128_LIB") or os.path.join(_PKG, "libntt128.so")  # override: experiments only
+# The product path always loads the in-tree library.  Experiment scripts (tools/) may point
+# `paper_2509_12494_b200._lib_override.PATH` at an experiment build BEFORE importing this
+# module; nothing here reads the environment.
+LIB_PATH = _lib_override.PATH or os.path.join(_PKG, "libntt128.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2509_12494_b200.build` (no fallback path exists)")
 
@@ -102,11 +107,13 @@ def _pairs(vals) -> ctypes.Array:
     return arr
 
 
-def _ptr(t: torch.Tensor, name: str, limbs: int = 2) -> int:
+def _ptr(t: torch.Tensor, name: str, limbs: int = 2, device: int | None = None) -> int:
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the plan on cuda:{device}")
     if t.dtype not in (torch.uint64, torch.int64):
         raise TypeError(f"{name} must have dtype uint64 or int64")
     if not t.is_contiguous() or t.shape[-1] != limbs:
@@ -155,14 +162,14 @@ class Plan:
         self._shape_ok(x, "x")
         out = torch.empty_like(x) if out is None else out
         self._shape_ok(out, "out")
-        _check(_L.ntt128_forward(self._h, _ptr(x, "x"), _ptr(out, "out"), _stream(x)), "ntt128_forward")
+        _check(_L.ntt128_forward(self._h, _ptr(x, "x", device=self.device), _ptr(out, "out", device=self.device), _stream(x)), "ntt128_forward")
         return out
 
     def inverse(self, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         self._shape_ok(y, "y")
         out = torch.empty_like(y) if out is None else out
         self._shape_ok(out, "out")
-        _check(_L.ntt128_inverse(self._h, _ptr(y, "y"), _ptr(out, "out"), _stream(y)), "ntt128_inverse")
+        _check(_L.ntt128_inverse(self._h, _ptr(y, "y", device=self.device), _ptr(out, "out", device=self.device), _stream(y)), "ntt128_inverse")
         return out
 
     def forward_bitrev(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -170,21 +177,22 @@ class Plan:
         self._shape_ok(x, "x")
         out = torch.empty_like(x) if out is None else out
         self._shape_ok(out, "out")
-        _check(_L.ntt128_forward_bitrev(self._h, _ptr(x, "x"), _ptr(out, "out"), _stream(x)), "ntt128_forward_bitrev")
+        _check(_L.ntt128_forward_bitrev(self._h, _ptr(x, "x", device=self.device), _ptr(out, "out", device=self.device), _stream(x)), "ntt128_forward_bitrev")
         return out
 
     def inverse_bitrev(self, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         self._shape_ok(y, "y")
         out = torch.empty_like(y) if out is None else out
         self._shape_ok(out, "out")
-        _check(_L.ntt128_inverse_bitrev(self._h, _ptr(y, "y"), _ptr(out, "out"), _stream(y)), "ntt128_inverse_bitrev")
+        _check(_L.ntt128_inverse_bitrev(self._h, _ptr(y, "y", device=self.device), _ptr(out, "out", device=self.device), _stream(y)), "ntt128_inverse_bitrev")
         return out
 
     def polymul(self, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         self._shape_ok(a, "a")
         self._shape_ok(b, "b")
         out = torch.empty_like(a) if out is None else out
-        _check(_L.ntt128_polymul(self._h, _ptr(a, "a"), _ptr(b, "b"), _ptr(out, "out"), _stream(a)), "ntt128_polymul")
+        self._shape_ok(out, "out")
+        _check(_L.ntt128_polymul(self._h, _ptr(a, "a", device=self.device), _ptr(b, "b", device=self.device), _ptr(out, "out", device=self.device), _stream(a)), "ntt128_polymul")
         return out
 
     def close(self) -> None:
@@ -270,12 +278,14 @@ class Plan256:
     def forward(self, x, out=None):
         self._shape_ok(x, "x")
         out = torch.empty_like(x) if out is None else out
+        self._shape_ok(out, "out")
         _check(_L.ntt256_forward(self._h, _ptr(x, "x", 4), _ptr(out, "out", 4), _stream(x)), "ntt256_forward")
         return out
 
     def inverse(self, y, out=None):
         self._shape_ok(y, "y")
         out = torch.empty_like(y) if out is None else out
+        self._shape_ok(out, "out")
         _check(_L.ntt256_inverse(self._h, _ptr(y, "y", 4), _ptr(out, "out", 4), _stream(y)), "ntt256_inverse")
         return out
 
@@ -294,6 +304,8 @@ class Plan256:
 def vmul256(x, y, q: int, out=None):
     """z = x * y mod q over 256-bit residues ([..., 4] limbs)"""
     out = torch.empty_like(x) if out is None else out
+    if y.numel() != x.numel() or out.numel() != x.numel():
+        raise ValueError("length mismatch")
     _check(_L.vec256_mul(_ptr(out, "out", 4), _ptr(x, "x", 4), _ptr(y, "y", 4), x.numel() // 4, _limbs4([q]), _stream(x)),
            "vec256_mul")
     return out

@@ -12,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import oracle as O
-from paper_2509_12494_b200 import synth
+import synth
 from paper_2509_12494_b200.fourstep import FourStep, from_columns, from_rows, split, to_columns, to_rows
 
 

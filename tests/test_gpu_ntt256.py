@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle256 as O4
-from paper_2509_12494_b200 import synth
+import synth
 
 pytestmark = pytest.mark.gpu
 

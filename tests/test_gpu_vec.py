@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from paper_2509_12494_b200 import synth
+import synth
 from tests._util import edge_pairs, to_dev, to_host
 
 pytestmark = pytest.mark.gpu

@@ -10,7 +10,7 @@ import pytest
 import sympy
 
 from oracle import oracle256 as O4
-from paper_2509_12494_b200 import synth
+import synth
 
 MODULI = [(1 << 256) - 189, (1 << 255) - 19, (1 << 192) - 237, (1 << 130) + 51, 65537, 97]
 

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from paper_2509_12494_b200 import synth
+import synth
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 EX = json.load(open(os.path.join(HERE, "golden", "paper_examples.json")))

@@ -2,7 +2,7 @@
 vectorised == sequential rejection sampling, range."""
 import numpy as np
 
-from paper_2509_12494_b200 import synth
+import synth
 
 
 def test_splitmix64_reference():

@@ -15,8 +15,10 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
+import paper_2509_12494_b200._lib_override as _libo  # noqa: E402
+_libo.PATH = __import__("os").environ.get("NTT128_LIB")  # experiment builds only (tools/)
 from paper_2509_12494_b200 import ntt128 as N  # noqa: E402
-from paper_2509_12494_b200 import synth  # noqa: E402
+import synth  # noqa: E402
 
 P = json.load(open("tests/golden/params.json"))
 mods = P["cfg3"]["moduli"]

@@ -7,7 +7,7 @@
 #include <vector>
 #include <algorithm>
 #include <cuda_runtime.h>
-#include "../../paper_2509_12494_b200/csrc/arith128.cuh"
+#include "arith_variants.cuh"
 using namespace ntt128;
 #ifndef EPT
 #define EPT 8

@@ -18,7 +18,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_12494_b200 import ntt128 as N  # noqa: E402
-from paper_2509_12494_b200 import synth  # noqa: E402
+import synth  # noqa: E402
 
 P = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
                                 "params.json")))
