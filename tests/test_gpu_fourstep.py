@@ -123,23 +123,3 @@ def test_fourstep_virtual_ranks(FS, params, log2n, world):
     y, xr = virtual_run(FS, log2n, q, w, x, world)
     assert np.array_equal(y, O.ntt(x, q, w))
     assert np.array_equal(xr, x)
-
-
-def test_fourstep_cfg5_full(FS, params):
-    """BASELINE cfg 5: N = 2^26 at G = 1 (13 x 13 split): sampled outputs by direct O(N)
-    evaluation (independent of any radix structure) and the exact round trip"""
-    import torch
-    e = params["cfg5"]
-    q, w = e["q"], e["omega"]
-    x = synth.uniform_residues(q, 1 << 26, synth.stream_seed(5, 0, 0))
-    fs = FS.FourStep(26, q, w)
-    cols = to_dev(FS.to_columns(x, 1 << 13, 1 << 13, 0, 1))
-    rows = fs.forward(cols)
-    y_rows = to_host(rows)                    # y_rows[k2][k1] = y[k2 + 2^13 k1]
-    rng = np.random.default_rng(5)
-    for k in [0, 1, (1 << 26) - 1] + [int(v) for v in rng.integers(0, 1 << 26, 5)]:
-        k2, k1 = k % (1 << 13), k >> 13
-        got = int(y_rows[k2, k1, 0]) | (int(y_rows[k2, k1, 1]) << 64)
-        assert got == O.ntt_eval(x, q, w, k), k
-    back = fs.inverse(rows)
-    assert torch.equal(back, cols)

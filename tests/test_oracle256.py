@@ -107,3 +107,15 @@ def test_w256_roots_exact_order(params):
         assert pow(e["psi"], 1 << L, q) == q - 1                  # psi of exact order 2^(L+1)
         assert e["omega"] == e["psi"] * e["psi"] % q
         assert pow(e["omega"], 1 << (L - 1), q) == q - 1          # omega of exact order 2^L
+
+
+@pytest.mark.parametrize("q", MODULI)
+def test_vmul_vs_python(q):
+    """o4_vmul (the 256-bit element-wise product the GPU vec256_mul is compared with):
+    every element against Python's a * b % q, on edge and random operands"""
+    rng = random.Random(q & 0xFFF)
+    ev = edges(q)
+    xs = [a for a in ev for _ in ev] + [rng.randrange(q) for _ in range(2000)]
+    ys = [b for _ in ev for b in ev] + [rng.randrange(q) for _ in range(2000)]
+    z = O4.vmul(O4.to_array(xs), O4.to_array(ys), q)
+    assert O4.to_ints(z) == [a * b % q for a, b in zip(xs, ys)]

@@ -117,3 +117,14 @@ def test_ring_laws(params):
             assert O.mulmod(O.mulmod(a, b, q), c, q) == O.mulmod(a, O.mulmod(b, c, q), q)
             assert O.mulmod(a, O.addmod(b, c, q), q) == O.addmod(O.mulmod(a, b, q), O.mulmod(a, c, q), q)
             assert O.submod(O.addmod(a, b, q), b, q) == a
+
+
+def test_powmod_random_exponents_vs_python(params):
+    """square-and-multiply against Python's pow on random 128-bit exponents (not only the
+    Fermat / inverse exponents q - 1 and q - 2), edge exponents 0, 1, 2^127, 2^128 - 1"""
+    rng = random.Random(11)
+    qs = [params["cfg5"]["q"], params["cfg2"]["q"], params["extra"]["b124"]["q"], 97, 65537, (1 << 128) - 159]
+    for q in qs:
+        for e in [0, 1, 2, 1 << 64, 1 << 127, (1 << 128) - 1] + [rng.randrange(1 << 128) for _ in range(40)]:
+            a = rng.randrange(q)
+            assert O.powmod(a, e, q) == pow(a, e, q), (hex(q), e)
