@@ -9,11 +9,18 @@ limbs), coefficients uniform in [0, q_i) (seeded).  One step = forward + inverse
 the whole batch through the C ABI (ntt128_forward / ntt128_inverse).  Metric: 128-bit
 NTT butterflies per second (N/2 log2 N per transform, forward and inverse counted).
 
-Multi-GPU (torchrun): every rank transforms its own 64-polynomial batch (independent
-RNS limbs; no data-path collective), value = butterflies of all ranks / max-over-ranks
-time ("scaling": "weak").  Timing: CUDA events on the launching stream, barrier +
-synchronize on both sides, max over ranks.  L2: inputs rotate over 4 disjoint buffer
-sets (each step's input was last touched >= 3 steps, >= 576 MiB of traffic, earlier).
+Multi-GPU: `--gpus G` re-launches itself under torch.distributed.run with G ranks (one
+process per GPU, NCCL) unless WORLD_SIZE is already set (the driver's torchrun form).
+Headline: every rank transforms its own 64-polynomial batch (independent RNS limbs; no
+data-path collective), value = butterflies of all ranks / max-over-ranks time
+("scaling": "weak").  Rows: the cfg4 sweep is STRONG scaling (1 GiB of coefficients in
+total, rank g owns polynomials [g B/G, (g+1) B/G); the N = 2^16 row, B = 1024, is the
+SURVEY.md §8(d) >= 7x row), cfg2 BLAS splits the vector, cfg1 / cfg3 polymul / cfg5
+three-pass / 256-bit rows run one replica per rank, the cfg5 four-step spans all ranks;
+every row is timed per rank and reported as max over ranks.  Timing: CUDA events on the
+launching stream, barrier + synchronize on both sides, max over ranks.  L2: inputs rotate
+over 4 disjoint buffer sets (each step's input was last touched >= 3 steps, >= 576 MiB of
+traffic, earlier).
 
 --impl reference runs the oracle (oracle/, the plain CPU implementation written from
 the paper) on this host's cores as the reference arm, on a bounded sample.
@@ -36,13 +43,14 @@ import numpy as np  # noqa: E402
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PARAMS_PATH = os.path.join(ROOT, "tests", "golden", "params.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+INT_PEAK_PATH = os.path.join(ROOT, "profiles", "int_peak.json")
 
 # Roofline constants.  P = algorithmic 32x32->64 products per unit
 # (SURVEY.md §8(d)): 36 per butterfly / constant mulmod, 42 per general mulmod.
 P_BUTTERFLY = 36
 P_GENERAL = 42
 SMS = 148
-IMAD_WIDE_PER_CLK_SM = 32          # measured: profiles/r01/int_rate.jsonl (IMAD.WIDE.U32 half the IMAD rate)
+IMAD_WIDE_PER_CLK_SM = 32          # fallback only: IMAD.WIDE.U32 at half the IMAD rate
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -63,12 +71,24 @@ def peaks():
             d = json.load(f)
     hbm = d.get("hbm_gbs")
     sm_max = d.get("sm_max_mhz", 1965.0)
+    # integer-multiply peak R: the measured 32x32->64 products per clock per SM (sustained
+    # >= 1.5 s with NVML clocks, tools/micro/int_peak.py -> profiles/int_peak.json) x 148 SMs
+    # x the max SM clock; the nominal 32/clk/SM only if that file is missing
+    per_clk, src = IMAD_WIDE_PER_CLK_SM, "fallback: 148 SM x 32 IMAD.WIDE.U32/clk x sm_max_mhz (DESIGN.md §6)"
+    if os.path.exists(INT_PEAK_PATH):
+        try:
+            with open(INT_PEAK_PATH) as f:
+                per_clk = float(json.load(f)["products_per_clk_per_sm"])
+            src = (f"profiles/int_peak.json: measured {per_clk:.3f} products/clk/SM (sustained, NVML clocks) "
+                   f"x 148 SM x sm_max_mhz {sm_max:.0f}")
+        except Exception:
+            per_clk = IMAD_WIDE_PER_CLK_SM
     return {
         "hbm_gbs": hbm if hbm else FALLBACK_HBM_GBS,
         "hbm_src": "measured" if hbm else "fallback",
         "sm_max_mhz": sm_max,
-        # integer-multiply peak: 148 SMs x 32 IMAD.WIDE.U32 per clock x max SM clock
-        "tprod_s": SMS * IMAD_WIDE_PER_CLK_SM * sm_max * 1e6 / 1e12,
+        "tprod_s": SMS * per_clk * sm_max * 1e6 / 1e12,
+        "tprod_src": src,
     }
 
 
@@ -124,6 +144,20 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- distributed
+def spawn_ranks(ngpus: int) -> int:
+    """re-run this script under torch.distributed.run with `ngpus` ranks (127.0.0.1
+    rendezvous); returns the launcher's exit code"""
+    import socket
+    import subprocess
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ngpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def dist_setup(ngpus: int):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -131,11 +165,17 @@ def dist_setup(ngpus: int):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:                                   # host-only self-test of the launch path (gloo)
+            dist.init_process_group("gloo")
+    elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
+
+
+from paper_2509_12494_b200.sharding import shard  # noqa: E402  (host logic, no CUDA)
 
 
 def barrier(world):
@@ -149,7 +189,7 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -287,27 +327,25 @@ def run_gpu(args):
     launch_ms = (ms_local / args.steps) / (2 * npasses)
     prod_per_launch = P_BUTTERFLY * B * (n // 2) * (logn / npasses)
     achieved = prod_per_launch / (launch_ms * 1e-3) / 1e12
-    traffic = None
+    traffic, traffic_src = None, None
     if os.path.exists(TRAFFIC_PATH):   # dram read+write bytes per launch from a committed ncu --set full capture
         try:
             with open(TRAFFIC_PATH) as f:
-                traffic = json.load(f).get("bytes_per_launch_mean")
+                tj = json.load(f)
+            traffic = tj.get("bytes_per_launch_mean")
+            traffic_src = "capture, not measured in this run: " + tj.get("source", TRAFFIC_PATH)
         except Exception:
             traffic = None
     roofline = {"bound": "alu", "kernel": "k_ntt_pass", "achieved": round(achieved, 4), "peak": round(pk["tprod_s"], 4),
                 "unit": "Tprod/s", "frac": round(achieved / pk["tprod_s"], 4), "traffic": traffic,
-                "peak_src": "148 SM x 32 IMAD.WIDE.U32/clk x sm_max_mhz (DESIGN.md §6)",
+                "traffic_src": traffic_src, "peak_src": pk["tprod_src"],
                 "step_frac": round(value / world * P_BUTTERFLY / 1e12 / pk["tprod_s"], 4)}
 
     # ---------------- end to end through the public API with host buffers
     e2e = run_e2e(plan, sets[0], args, stream, bfly_per_step, world)
 
-    rows = run_rows(args, P, pk, stream) if (args.rows and rank == 0) else None
-    if args.rows and args.cfg5:
-        r5 = run_cfg5_fourstep(args, P, rank, world)      # every rank takes part (all-to-all)
-        if rows is not None:
-            rows.update(r5)
-    cpu = cpu_baseline(P) if (rank == 0 and world == 1 and args.cpu_baseline) else None
+    rows = run_rows(args, P, pk, stream, rank, world) if args.rows else None
+    cpu = cpu_baseline(P) if (rank == 0 and args.cpu_baseline) else None
     if rank == 0:
         out = {
             "metric": "128-bit NTT butterflies/sec (N=2^16, fwd+inv, 64 RNS primes)",
@@ -394,37 +432,63 @@ def run_e2e(plan, x_host, args, stream, bfly_per_step, world):
 
 
 # ----------------------------------------------------------------------------- other §8 rows
-def run_rows(args, P, pk, stream):
-    """One measurement per other SURVEY §8(a) row: cfg1 latency, cfg2 BLAS, cfg3 negacyclic
-    polymul, cfg4 size sweep (N = 2^10 .. 2^17 by default), cfg5 N = 2^26 on one GPU."""
+def timed_rank(fn, iters, world, repeats=3):
+    """per-call ms of fn(i): `repeats` runs of `iters` calls, each bracketed by a barrier and
+    CUDA events on the current stream, max over ranks; returns the median over repeats"""
+    import torch
+    out = []
+    for r in range(repeats):
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(iters):
+            fn(i)
+        e1.record()
+        e1.synchronize()
+        out.append(max_over_ranks(e0.elapsed_time(e1) / iters, world))
+    return statistics.median(out)
+
+
+def run_rows(args, P, pk, stream, rank, world):
+    """One measurement per other SURVEY §8(a) row, on every rank (module docstring): cfg1
+    latency, cfg2 BLAS, cfg3 negacyclic polymul, cfg4 size sweep (strong scaling), cfg5
+    N = 2^26 (three-pass replicas and the four-step over all ranks), 256-bit moduli."""
     import torch
     from paper_2509_12494_b200 import ntt128 as N
     import synth
-    rows = {}
-    # cfg1: single N = 1024 forward + inverse (latency)
+    rows = {"rows_scaling": {"cfg1": "replica per rank (max latency)", "cfg2": "strong (n split over ranks)",
+                             "cfg3_polymul": "weak (64 per rank)", "cfg4": "strong (1 GiB total, batch split)",
+                             "cfg5_three_pass": "replica per rank", "cfg5_fourstep": "one transform over all ranks",
+                             "f4": "weak (32 per rank)"},
+            "rows_timing": "median of 3 repeats, each max over ranks of CUDA-event time"}
+    # cfg1: single N = 1024 forward + inverse (latency) -- one replica per rank
     e = P["cfg1"]
     q, w = hexint(e["q"]), hexint(e["omega"])
     p1 = N.Plan(10, q, w)
     x = to_dev(synth.uniform_residues(q, 1024, synth.stream_seed(1, 0, 0)).reshape(1, 1024, 2))
     y, z = torch.empty_like(x), torch.empty_like(x)
-    ms = time_graph(lambda i: (p1.forward(x, out=y), p1.inverse(y, out=z)), 50)
+    ms = max_over_ranks(time_graph(lambda i: (p1.forward(x, out=y), p1.inverse(y, out=z)), 50), world)
+    assert torch.equal(z, x), "cfg1 round trip"
     rows["cfg1_n1024_fwd_inv_us"] = ms * 1e3           # CUDA-graph replay (launch overhead excluded)
     rows["cfg1_ns_per_butterfly"] = ms * 1e6 / (2 * 5120)
-    # cfg2: BLAS n = 2^20 (HBM-bound; 48 B/element); rotate 8 buffer sets (8 x 48 MiB > L2)
+    # cfg2: BLAS n = 2^20 split over the ranks (HBM-bound; 48 B/element); 8 rotating sets
     q2, a2, n2 = hexint(P["cfg2"]["q"]), hexint(P["cfg2"]["a"]), P["cfg2"]["n"]
-    xs = [to_dev(synth.uniform_residues(q2, n2, synth.stream_seed(2, 0, s))) for s in range(8)]
-    ys = [to_dev(synth.uniform_residues(q2, n2, synth.stream_seed(2, 1, s))) for s in range(8)]
+    s0, s1 = shard(n2, world, rank)
+    nl = s1 - s0
+    xs = [to_dev(synth.uniform_residues(q2, n2, synth.stream_seed(2, 0, s))[s0:s1]) for s in range(8)]
+    ys = [to_dev(synth.uniform_residues(q2, n2, synth.stream_seed(2, 1, s))[s0:s1]) for s in range(8)]
     zs = [torch.empty_like(v) for v in xs]
     ops = {"add": lambda i: N.vadd(xs[i % 8], ys[i % 8], q2, out=zs[i % 8]),
            "sub": lambda i: N.vsub(xs[i % 8], ys[i % 8], q2, out=zs[i % 8]),
            "mul": lambda i: N.vmul(xs[i % 8], ys[i % 8], q2, out=zs[i % 8]),
            "axpy": lambda i: N.axpy(a2, xs[i % 8], ys[i % 8], q2)}
     for name, fn in ops.items():
-        ms = time_graph(fn, 64)
-        gbs = 48 * n2 / (ms * 1e-3) / 1e9
+        ms = max_over_ranks(time_graph(fn, 64), world)
         rows[f"cfg2_{name}_elem_per_s"] = n2 / (ms * 1e-3)
-        rows[f"cfg2_{name}_hbm_frac"] = gbs / pk["hbm_gbs"]
-    # cfg3 negacyclic polymul (B = 64)
+        rows[f"cfg2_{name}_hbm_frac"] = 48 * nl / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]   # per GPU
+    del xs, ys, zs
+    # cfg3 negacyclic polymul (B = 64 per rank)
     mods = P["cfg3"]["moduli"]
     qs, psis = [hexint(m["q"]) for m in mods], [hexint(m["psi"]) for m in mods]
     n3 = 1 << 16
@@ -434,27 +498,34 @@ def run_rows(args, P, pk, stream):
     c = torch.empty_like(a)
     for _ in range(3):
         pn.polymul(a, b, out=c)
-    ms = time_events(lambda i: pn.polymul(a, b, out=c), 10, stream)
-    rows["cfg3_negacyclic_polymul_per_s"] = 64 / (ms * 1e-3)
+    ms = timed_rank(lambda i: pn.polymul(a, b, out=c), 10, world)
+    rows["cfg3_negacyclic_polymul_per_s"] = 64 * world / (ms * 1e-3)
     rows["cfg3_negacyclic_polymul_ms"] = ms
     del pn, a, b, c
-    # cfg4 sweep (1 GiB of coefficients per size) -- sizes given by --sweep
+    # cfg4 sweep: 1 GiB of coefficients in TOTAL per size, rank g owns polynomials
+    # [g B/G, (g+1) B/G) of the same seeded batch (strong scaling; no collective)
     for logn in args.sweep:
         e = P["cfg4"][str(logn)]
         q, w = hexint(e["q"]), hexint(e["omega"])
         nn = 1 << logn
         Bn = (1 << 26) // nn
-        ps = N.Plan(logn, q, w, batch=Bn)
-        xx = to_dev(synth.uniform_residues(q, 1 << 26, synth.stream_seed(4, 0, logn)).reshape(Bn, nn, 2))
-        yy = torch.empty_like(xx)
+        b0, b1 = shard(Bn, world, rank)
+        xfull = synth.uniform_residues(q, 1 << 26, synth.stream_seed(4, 0, logn)).reshape(Bn, nn, 2)
+        ps = N.Plan(logn, q, w, batch=b1 - b0)
+        xx = to_dev(xfull[b0:b1])
+        del xfull
+        yy, zz = torch.empty_like(xx), torch.empty_like(xx)
         for _ in range(2):
-            ps.forward(xx, out=yy); ps.inverse(yy, out=xx)
-        ms = time_events(lambda i: (ps.forward(xx, out=yy), ps.inverse(yy, out=xx)), 5, stream)
-        rows[f"cfg4_logn{logn}_butterflies_per_s"] = 2 * Bn * (nn // 2) * logn / (ms * 1e-3)
-        rows[f"cfg4_logn{logn}_int_frac"] = round(rows[f"cfg4_logn{logn}_butterflies_per_s"] * P_BUTTERFLY / 1e12 / pk["tprod_s"], 4)
-        del ps, xx, yy
+            ps.forward(xx, out=yy); ps.inverse(yy, out=zz)
+        torch.cuda.synchronize()
+        assert torch.equal(zz, xx), f"cfg4 N=2^{logn} round trip"
+        ms = timed_rank(lambda i: (ps.forward(xx, out=yy), ps.inverse(yy, out=zz)), 20, world)
+        bf = 2 * Bn * (nn // 2) * logn / (ms * 1e-3)
+        rows[f"cfg4_logn{logn}_butterflies_per_s"] = bf
+        rows[f"cfg4_logn{logn}_int_frac"] = round(bf / world * P_BUTTERFLY / 1e12 / pk["tprod_s"], 4)   # per GPU
+        del ps, xx, yy, zz
         torch.cuda.empty_cache()
-    # cfg5: N = 2^26 single transform on one GPU (three passes)
+    # cfg5: N = 2^26 single transform through one plan (three passes), a replica per rank
     if args.cfg5:
         e = P["cfg5"]
         q, w = hexint(e["q"]), hexint(e["omega"])
@@ -465,13 +536,14 @@ def run_rows(args, P, pk, stream):
         p5.forward(xx, out=yy); p5.inverse(yy, out=zz)
         torch.cuda.synchronize()
         assert torch.equal(zz, xx)
-        ms = time_events(lambda i: (p5.forward(xx, out=yy), p5.inverse(yy, out=zz)), 5, stream)
+        ms = timed_rank(lambda i: (p5.forward(xx, out=yy), p5.inverse(yy, out=zz)), 5, world)
         rows["cfg5_n2^26_fwd_inv_ms"] = ms
         rows["cfg5_butterflies_per_s"] = 2 * (1 << 25) * 26 / (ms * 1e-3)
         del p5, xx, yy, zz
         torch.cuda.empty_cache()
-    # 256-bit moduli, N = 2^16 x 32 forward + inverse (largest prime < 2^256
-    # with q = 1 mod 2^21); roofline P = 136 word products per butterfly (8-word Montgomery)
+        rows.update(run_cfg5_fourstep(args, P, rank, world))
+    # 256-bit moduli, N = 2^16 x 32 forward + inverse per rank (largest prime
+    # < 2^256 with q = 1 mod 2^21); roofline P = 136 word products per butterfly
     e = P["w256"]["b256"]
     q = hexint(e["q"])
     w = pow(hexint(e["omega"]), 1 << (e["logn"] - 16), q)
@@ -482,9 +554,9 @@ def run_rows(args, P, pk, stream):
     p6.forward(xx, out=yy); p6.inverse(yy, out=zz)
     torch.cuda.synchronize()
     assert torch.equal(zz, xx)
-    ms = time_events(lambda i: (p6.forward(xx, out=yy), p6.inverse(yy, out=zz)), 10, stream)
+    ms = timed_rank(lambda i: (p6.forward(xx, out=yy), p6.inverse(yy, out=zz)), 10, world)
     bf = 2 * 32 * (1 << 15) * 16 / (ms * 1e-3)
-    rows["f4_ntt256_n2^16_x32_butterflies_per_s"] = bf
+    rows["f4_ntt256_n2^16_x32_butterflies_per_s"] = bf * world
     rows["f4_ntt256_roofline_frac"] = bf * 136 / (pk["tprod_s"] * 1e12)
     del p6, xx, yy, zz
     torch.cuda.empty_cache()
@@ -492,27 +564,28 @@ def run_rows(args, P, pk, stream):
 
 
 def run_cfg5_fourstep(args, P, rank, world):
-    """cfg 5: one N = 2^26 forward + inverse NTT as a four-step (2^13 x 2^13) transform
+    """cfg 5: one N = 2^26 forward + inverse NTT as a four-step (2^9 x 2^17) transform
     partitioned over the `world` ranks; every rank holds N/G coefficients
-    (columns layout), timing = max over ranks.  Two transports: "nccl" (pack, one NCCL
-    all-to-all per direction, unpack) and "p2p" (the pack kernel stores
-    each block straight into its destination rank's symmetric-memory receive buffer)."""
+    (columns layout), timing = max over ranks.  Two transports: "nccl" (pass A stores into
+    the send blocks, one NCCL all-to-all per direction) and "p2p" (pass A's
+    last pass stores each block straight into its destination rank's symmetric-memory
+    receive buffer); a transport the box cannot provide is reported as *_unavailable."""
     import torch
     from paper_2509_12494_b200 import fourstep as FS
     import synth
     e = P["cfg5"]
     q, w = hexint(e["q"]), hexint(e["omega"])
-    out = {"cfg5_fourstep_gpus": world}
-    # the peer-store transport at G > 1 needs NVLink peer mappings and device barriers across
-    # ranks: opt in with --p2p (at G = 1 it is a local fused pack and always runs)
-    transports = ("nccl", "p2p") if (world == 1 or args.p2p) else ("nccl",)
-    if world > 1 and not args.p2p:
-        out["cfg5_fourstep_p2p_skipped"] = "multi-GPU peer-store transport is opt-in: bench.py --p2p"
-    for transport in transports:
+    out = {"cfg5_fourstep_gpus": world, "cfg5_fourstep_split": list(FS.split(26))}
+    for transport in ("nccl", "p2p"):
+        tag = "cfg5_fourstep" if transport == "nccl" else "cfg5_fourstep_p2p"
         try:
             fs = FS.FourStep(26, q, w, rank, world, None, transport=transport)
-        except Exception as ex:                      # no peer mappings on this box
-            out[f"cfg5_fourstep_{transport}_unavailable"] = str(ex).splitlines()[0][:200]
+            ok = 1.0
+        except Exception as ex:                      # e.g. no peer mappings on this box
+            fs, ok = None, 0.0
+            out[f"{tag}_unavailable"] = str(ex).splitlines()[0][:200]
+        if max_over_ranks(1.0 - ok, world) > 0:      # every rank runs the transport or none does
+            out.setdefault(f"{tag}_unavailable", "unavailable on another rank")
             continue
         L = fs.local
         cols = to_dev(synth.uniform_residues(q, L.R1 * L.n2, synth.stream_seed(5, 0, 100 + rank)).reshape(L.R1, L.n2, 2))
@@ -523,24 +596,14 @@ def run_cfg5_fourstep(args, P, rank, world):
             fs.inverse(rows, out=back)
         torch.cuda.synchronize()
         assert torch.equal(back, cols), f"cfg5 four-step ({transport}) round trip mismatch"
-        iters = 5
-        barrier(world)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(iters):
-            fs.forward(cols, out=rows)
-            fs.inverse(rows, out=back)
-        e1.record()
-        e1.synchronize()
-        ms = max_over_ranks(e0.elapsed_time(e1) / iters, world)
+        ms = timed_rank(lambda i: (fs.forward(cols, out=rows), fs.inverse(rows, out=back)), 5, world)
         bfly = 2 * (1 << 25) * 26
-        tag = "cfg5_fourstep" if transport == "nccl" else "cfg5_fourstep_p2p"
         out[f"{tag}_fwd_inv_ms"] = ms
         out[f"{tag}_butterflies_per_s"] = bfly / (ms * 1e-3)
         if transport == "nccl":
             out["cfg5_fourstep_a2a_bytes_per_rank_per_direction"] = 16 * L.R1 * L.R2 * (world - 1)
         del fs, cols, rows, back
+        torch.cuda.empty_cache()
     return out
 
 
@@ -597,6 +660,22 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def launch_selftest(args):
+    """every rank reports its rank, world size and its shards of the cfg4 N = 2^16 batch and
+    the cfg2 vector; rank 0 gathers them (gloo) and prints one JSON line"""
+    import torch.distributed as dist
+    rank, world, _ = dist_setup(args.gpus)
+    mine = {"rank": rank, "world": world, "cfg4_logn16": shard(1024, world, rank), "cfg2": shard(1 << 20, world, rank)}
+    allv = [None] * world
+    if world > 1:
+        dist.all_gather_object(allv, mine)
+        dist.destroy_process_group()
+    else:
+        allv = [mine]
+    if rank == 0:
+        print(json.dumps({"launch_selftest": allv}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -608,9 +687,16 @@ def main():
     ap.add_argument("--sweep", type=lambda s: [int(v) for v in s.split(",") if v], default=list(range(10, 18)))
     ap.add_argument("--no-cfg5", dest="cfg5", action="store_false", default=True)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false", default=True)
-    ap.add_argument("--p2p", action="store_true", default=False,
-                    help="also time the cfg5 four-step with the fused peer-store exchange at G > 1")
+    ap.add_argument("--no-spawn", dest="spawn", action="store_false", default=True,
+                    help="with --gpus > 1 and no WORLD_SIZE: run one process instead of launching the ranks")
+    ap.add_argument("--launch-selftest", action="store_true", default=False,
+                    help="host-only check of the rank launch and the batch shards (gloo; no GPU work)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.spawn:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.launch_selftest:
+        launch_selftest(args)
+        return
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

@@ -64,7 +64,10 @@ typedef enum {
 #define NTT128_NEGACYCLIC 1u        /* root = psi of exact order 2N; y_k = sum_j x_j psi^{j(2k+1)}, the evaluation at psi^{2k+1} */
 #define NTT128_FLAG_CHECK_INPUT 0x100u /* validate inputs < q on every call (synchronises the stream) */
 
-typedef struct ntt128_plan_s *ntt128_plan_t; /* opaque; immutable after create; safe to share across streams */
+/* opaque; its tables are immutable after create; safe to share across streams and threads
+ * (per-stream pass-overlap counters and scratch are cached inside, at most 8 streams: a
+ * further stream evicts the least recently used entry once its last use has completed) */
+typedef struct ntt128_plan_s *ntt128_plan_t;
 
 /* Create a plan for `batch` transforms of length N = 2^log2n (1 <= log2n <= 26).
  *   q_host:    [n_moduli][2] uint64 {lo, hi}: odd primes 3 <= q < 2^128 (any width;
@@ -93,9 +96,9 @@ ntt128_status ntt128_inverse(const ntt128_plan_t plan, const uint64_t *d_in, uin
 /* Polynomial product through the transform: d_c = a * b mod (X^N + 1) for negacyclic
  * plans, mod (X^N - 1) for cyclic plans (NTT, point-wise product,
  * inverse NTT).  d_a, d_b, d_c: [batch][N][2]; d_c may alias d_a or d_b.
- * Uses 2 x batch x N x 16 bytes of scratch per stream, allocated by the plan on the
- * first call on that stream and kept until ntt128_plan_destroy (an in-place multi-pass
- * forward/inverse uses the first half). */
+ * Uses 2 x batch x N x 16 bytes of scratch per stream (an in-place multi-pass forward /
+ * inverse: batch x N x 16), allocated by the plan on the first such call on that stream
+ * and kept in the plan's per-stream cache. */
 ntt128_status ntt128_polymul(const ntt128_plan_t plan, const uint64_t *d_a, const uint64_t *d_b, uint64_t *d_c,
                              ntt128_stream_t stream);
 
@@ -140,45 +143,53 @@ ntt128_status vec128_axpy(uint64_t *d_y, const uint64_t *a, const uint64_t *d_x,
 
 /* ---------------------------------------------------------------------------
  * Distributed four-step NTT of one huge polynomial (BASELINE cfg 5, N = 2^26; SURVEY.md
- * §8(a) row a13, §8(e)).  N = n1 n2, j = j1 + n1 j2, k = k2 + n2 k1:
- *   z[j1][k2] = sum_{j2} x[j1 + n1 j2] w^{n1 j2 k2}       (n2-point NTTs, w = omega)
- *   z[j1][k2] *= w^{j1 k2}                                 (twiddle)
- *   y[k2 + n2 k1] = sum_{j1} z[j1][k2] w^{n2 j1 k1}        (n1-point NTTs)
- * which equals Eq. ntt exactly.  G = world ranks (a power of two
- * dividing n1 and n2), one process per GPU; the caller moves the packed blocks between
- * ranks with an all-to-all of equal splits (NCCL over NVLink), e.g.
- * torch.distributed.all_to_all_single.  Layouts (R1 = n1/G, R2 = n2/G, rank g):
+ * §8(a) row a13, §8(e)).  N = n1 n2, j = j1 + n1 j2, k = k2 + n2 k1, w = omega; since
+ * jk = j1 k2 + n2 j1 k1 + n1 j2 k2 (mod N), Eq. ntt is exactly
+ *   pass A:  z[j1][k2] = sum_{j2} x[j1 + n1 j2] w^{n1 j2 k2}               (n2-point NTTs)
+ *   pass C:  y[k2 + n2 k1] = sum_{j1} (w^{j1 k2} z[j1][k2]) w^{n2 j1 k1}    (n1-point NTTs)
+ * with the twiddle w^{j1 k2} applied by pass C as it loads z (one product per element).
+ * G = world ranks (a power of two, G <= 8, dividing n1 and n2), one process per GPU; the
+ * caller moves the blocks between ranks with an all-to-all of equal splits (NCCL over
+ * NVLink), e.g. torch.distributed.all_to_all_single.  Layouts (R1 = n1/G, R2 = n2/G, rank g):
  *   "columns" X_g[R1][n2]: X_g[r][j2] = x[(g R1 + r) + n1 j2]       (forward input / inverse output)
  *   "rows"    Y_g[R2][n1]: Y_g[r][k1] = y[(g R2 + r) + n2 k1]       (forward output / inverse input)
- *   send/recv [G][R1][R2] (forward) and [G][R2][R1] (inverse): block h goes to / came from rank h.
- * The inverse applies (n1 n2)^{-1} (each sub-transform scales by its own length).
+ *   send [G][R1][R2] (forward): send[h][r][c] = z[g R1 + r][h R2 + c], block h goes to rank h;
+ *   recv [G][R1][R2]: recv[g'][r][c] = z[g' R1 + r][g R2 + c] (block g' came from rank g').
+ * Inverse: pass A = Z[k2][j1] = n1^{-1} sum_{k1} y[k2 + n2 k1] w^{-n2 j1 k1} (rows), send /
+ * recv [G][R2][R1] by the destination of j1; pass C = x[j1 + n1 j2] = n2^{-1} sum_{k2}
+ * (w^{-j1 k2} Z[k2][j1]) w^{-n1 j2 k2}.  A four-step object holds one working buffer of
+ * N/G residues: use it on one stream at a time.
  * ------------------------------------------------------------------------- */
 typedef struct ntt128_fourstep_s *ntt128_fourstep_t;
 
-/* log2n1, log2n2 in [1, 13]; q, omega: host {lo, hi}, omega of exact order N = 2^(log2n1 + log2n2);
- * world G a power of two dividing both n1 and n2; 0 <= rank < world. */
+/* log2n1, log2n2 >= 1, log2n1 + log2n2 <= 26; q, omega: host {lo, hi}, omega of exact order
+ * N = 2^(log2n1 + log2n2); world G a power of two <= 8 dividing both n1 and n2; 0 <= rank < world.
+ * Builds the sub-plans and the rank's twiddle-factor tables ([R2][n1] forward, [R1][n2]
+ * inverse: 2 N/G residues) on `device`. */
 ntt128_status ntt128_fourstep_create(ntt128_fourstep_t *out, uint32_t log2n1, uint32_t log2n2, const uint64_t *q,
                                      const uint64_t *omega, uint32_t rank, uint32_t world, int device);
-/* forward, before the exchange: X_g (columns) -> send [G][R1][R2] */
+/* forward, before the exchange: X_g (columns) -> send [G][R1][R2] (pass A; its last pass
+ * stores straight into the blocks) */
 ntt128_status ntt128_fourstep_forward_a(const ntt128_fourstep_t fs, const uint64_t *d_cols, uint64_t *d_send,
                                         ntt128_stream_t stream);
-/* forward, after the exchange: recv [G][R1][R2] -> Y_g (rows) */
+/* forward, after the exchange: recv [G][R1][R2] -> Y_g (rows); d_recv != d_rows */
 ntt128_status ntt128_fourstep_forward_c(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_rows,
                                         ntt128_stream_t stream);
 /* inverse, before the exchange: Y_g (rows) -> send [G][R2][R1] */
 ntt128_status ntt128_fourstep_inverse_a(const ntt128_fourstep_t fs, const uint64_t *d_rows, uint64_t *d_send,
                                         ntt128_stream_t stream);
-/* inverse, after the exchange: recv [G][R2][R1] -> X_g (columns) */
+/* inverse, after the exchange: recv [G][R2][R1] -> X_g (columns); d_recv != d_cols */
 ntt128_status ntt128_fourstep_inverse_c(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_cols,
                                         ntt128_stream_t stream);
-/* Fused exchange: pass A whose twiddle + pack kernel stores block h
- * straight into rank h's receive buffer instead of a local send buffer -- the layout
- * ntt128_fourstep_*_c expects, as if the all-to-all had run.  peers: host array of `world`
- * device pointers, peers[h] = rank h's [G][R1][R2] (forward) / [G][R2][R1] (inverse)
- * receive buffer mapped into this process (peer memory over NVLink/NVSwitch, e.g. torch
- * symmetric memory; peers[rank] is the local one).  The caller orders the writes: a
- * barrier across ranks before the call (every peer is done reading its receive buffer)
- * and after it (every block has landed) before pass C.  world <= 64. */
+/* Fused exchange: pass A whose LAST transform pass stores each output
+ * straight into its destination rank's receive buffer (peer memory over NVLink/NVSwitch)
+ * at the offset the all-to-all would have used -- the layout ntt128_fourstep_*_c expects.
+ * No send buffer and no collective.  peers: host array of `world` device pointers,
+ * peers[h] = rank h's [G][R1][R2] (forward) / [G][R2][R1] (inverse) receive buffer mapped
+ * into this process (e.g. torch symmetric memory; peers[rank] is the local one).  The
+ * caller orders the writes: a barrier across ranks before the call (every peer is done
+ * reading its receive buffer) and after it (every block has landed) before pass C.
+ * Every pointer is validated before anything is enqueued. */
 ntt128_status ntt128_fourstep_forward_a_peers(const ntt128_fourstep_t fs, const uint64_t *d_cols,
                                               const uint64_t *const *peers, ntt128_stream_t stream);
 ntt128_status ntt128_fourstep_inverse_a_peers(const ntt128_fourstep_t fs, const uint64_t *d_rows,

@@ -36,6 +36,7 @@
 #include "../../include/ntt128.h"
 #include "arith128.cuh"
 #include "host128.h"
+#include "ntt128_internal.h"
 
 #ifndef NTT128_EXPERIMENTS
 #define NTT128_EXPERIMENTS 0   // 1: experiment build (environment switches; never the product .so)
@@ -282,6 +283,17 @@ struct PassArgs {
     uint32_t* cnt_out;       // optional [batch]: this pass's completion counters (+1 per CTA)
     uint32_t target;         // cnt_in[poly] value that means "previous pass done" (wrap-safe compare)
     uint32_t pdl_wait;       // 1: griddepcontrol.wait before reading data (first pass of a PDL launch)
+    // Four-step I/O (fourstep.cu; natural [batch][N] when left at the defaults):
+    //  * the pass reads element idx of polynomial p at src[p in_ps + idx in_es] (default N, 1;
+    //    a first pass may read the columns of a received [n][batch] matrix: in_ps 1, in_es batch);
+    //  * fpoly: fin is indexed by polynomial instead of modulus ([batch][f_stride]);
+    //  * r_lb != 0 (the transform's last pass): output k of polynomial p goes to
+    //    rdst[k >> r_lb] + p r_ps + (k mod 2^r_lb) -- the destination rank's block of the
+    //    all-to-all send buffer, or that rank's receive buffer itself (peer memory).
+    uint64_t in_ps, in_es;
+    uint32_t fpoly, r_lb;
+    uint64_t r_ps;
+    uint4* rdst[NTT128_FS_MAX_RANKS];
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
@@ -500,11 +512,12 @@ struct PassOcc {
     static constexpr int RB = PassShape<B, RBMAX>::RB;
     static constexpr int THREADS = (RB == 2 && !SINGLE) ? NTT_OCC_THREADS_RB2 : NTT_OCC_THREADS;
 };
-template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX>
+template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX, bool PM = false>
 __global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T,
                                   (PassOcc<B, RBMAX, SINGLE>::THREADS / (C * PassShape<B, RBMAX>::T)) > 0
                                       ? PassOcc<B, RBMAX, SINGLE>::THREADS / (C * PassShape<B, RBMAX>::T) : 1)
 k_ntt_pass(const PassArgs a) {
+    static_assert(!PM || (FIRST && !SINGLE), "polynomial-major groups: multi-pass first passes only");
     constexpr bool PADL = !SINGLE;
     using S = PassShape<B, RBMAX, C, PADL>;
     constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS, TS = S::TS;
@@ -522,7 +535,16 @@ k_ntt_pass(const PassArgs a) {
     uint64_t gg0 = (uint64_t)blockIdx.x * C;
     // multi-pass CTAs hold groups of one polynomial: visit polynomials in the plan's order
     // (grouped by arithmetic mode) so one code path at a time is hot in the I-cache
-    if (!SINGLE && a.order) gg0 = ((uint64_t)a.order[gg0 >> gbits] << gbits) | (gg0 & gmask);
+    if (!SINGLE && !PM && a.order) gg0 = ((uint64_t)a.order[gg0 >> gbits] << gbits) | (gg0 & gmask);
+    // PM (polynomial-major first pass, four-step pass C over a received matrix whose
+    // polynomials are adjacent in memory): the CTA's C groups are column g0
+    // of the C consecutive polynomials [pc C, pc C + C), CTAs ordered g-major, so a row of
+    // the gather is C adjacent residues (a full 32-byte sector at C = 2, 64 bytes at C = 4)
+    // and consecutive CTAs read consecutive segments.  One modulus (nq == 1).
+    const uint64_t pm_np = PM ? (a.total_groups >> gbits) / C : 1;
+    const uint64_t pm_g0 = PM ? blockIdx.x / pm_np : 0, pm_pc = PM ? blockIdx.x % pm_np : 0;
+    if (PM) gg0 = ((pm_pc * C) << gbits) | pm_g0;
+    auto gg_of = [&](int c) -> uint64_t { return PM ? (((pm_pc * C + c) << gbits) | pm_g0) : gg0 + c; };
     const int tid = threadIdx.x;
 
     // ---------------- load phase: twiddles and data -> shared memory, all copies in flight
@@ -537,7 +559,7 @@ k_ntt_pass(const PassArgs a) {
     const int c_me = tid % C;
     const int u_me = tid / C;
     const int t0 = (RT == 0 || LT == 0) ? u_me : ((u_me >> RT) | ((u_me & ((1 << RT) - 1)) << (LT - RT)));
-    const uint64_t gg_me = gg0 + c_me;
+    const uint64_t gg_me = gg_of(c_me);
     const bool live = gg_me < a.total_groups;
     const uint64_t ggc_me = live ? gg_me : a.total_groups - 1;
     const uint64_t poly_me = ggc_me >> gbits, g_me = ggc_me & gmask;
@@ -602,7 +624,8 @@ k_ntt_pass(const PassArgs a) {
         gstride = (uint32_t)T << lo;
         lbase = t0;
     }
-    const uint4* srcp = a.src + poly_me * N + gbase;
+    const uint4* srcp = a.src + poly_me * a.in_ps + gbase * a.in_es;
+    const uint64_t sstride = (uint64_t)gstride * a.in_es;   // source step per i
     uint4* smc = sm + c_me * GS;
     if (!a.fin && !a.pmul) {
         if (live) {
@@ -611,7 +634,7 @@ k_ntt_pass(const PassArgs a) {
             // writing consecutive 16-byte slots) costs one L1 wavefront per lane
             uint4 v[PER];
 #pragma unroll
-            for (int i = 0; i < PER; i++) v[i] = __ldcg(srcp + (size_t)i * gstride);
+            for (int i = 0; i < PER; i++) v[i] = __ldcg(srcp + (size_t)i * sstride);
 #pragma unroll
             for (int i = 0; i < PER; i++) {
                 const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
@@ -621,14 +644,14 @@ k_ntt_pass(const PassArgs a) {
 #pragma unroll
             for (int i = 0; i < PER; i++) {
                 const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
-                cp_async16(smc + slot<B, PADL, RB>(l), srcp + (size_t)i * gstride);
+                cp_async16(smc + slot<B, PADL, RB>(l), srcp + (size_t)i * sstride);
             }
 #endif
         }
     } else if (live) {
         uint4 stage[PER];
 #pragma unroll
-        for (int i = 0; i < PER; i++) stage[i] = srcp[(size_t)i * gstride];
+        for (int i = 0; i < PER; i++) stage[i] = srcp[(size_t)i * sstride];
         const ModC& M = a.mods[m_me];
         const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
 #pragma unroll
@@ -636,7 +659,7 @@ k_ntt_pass(const PassArgs a) {
             const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
             const uint64_t idx = gbase + (size_t)i * gstride;
             U128 x = u128_from(stage[i]);
-            if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + m_me * a.f_stride + idx)), q, M.qinv0);
+            if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + (a.fpoly ? poly_me : m_me) * a.f_stride + idx)), q, M.qinv0);
             if (a.pmul) x = mont_mul(x, u128_from(__ldg(a.pmul + poly_me * N + idx)), q, M.qinv0);
             smc[slot<B, PADL, RB>(l)] = u128_to(x);
         }
@@ -654,7 +677,7 @@ k_ntt_pass(const PassArgs a) {
     {
         constexpr bool WARPMAP = T <= 32 && (32 % T) == 0;
         const int c = WARPMAP ? tid / T : tid % C, t = WARPMAP ? tid % T : tid / C;
-        const uint64_t gg = gg0 + c;
+        const uint64_t gg = gg_of(c);
         const uint64_t ggc = gg < a.total_groups ? gg : a.total_groups - 1;
         const uint32_t m = a.nq == 1 ? 0 : (uint32_t)(ggc >> gbits);
         uint32_t q[4], qinv0;
@@ -699,7 +722,7 @@ k_ntt_pass(const PassArgs a) {
             for (int i = 0; i < PER; i++) {
                 const int e = tid + i * NT;
                 const int c = e / G, l = e % G;
-                const uint64_t gg = gg0 + c;
+                const uint64_t gg = gg_of(c);
                 if (gg >= a.total_groups) continue;
                 const uint64_t poly = gg >> gbits, g = gg & gmask;
                 const uint64_t idx = ((uint64_t)brev_bits((uint32_t)g, gbits) << B) | (uint64_t)l;
@@ -710,7 +733,10 @@ k_ntt_pass(const PassArgs a) {
                     const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
                     v = u128_to(mont_mul(u128_from(v), u128_from(__ldg(a.fout + m * a.f_stride + idx)), q, M.qinv0));
                 }
-                a.dst[poly * N + idx] = v;
+                if (SINGLE && a.r_lb)   // four-step: straight into the destination rank's block
+                    a.rdst[idx >> a.r_lb][poly * a.r_ps + (idx & ((1ull << a.r_lb) - 1))] = v;
+                else
+                    a.dst[poly * N + idx] = v;
             }
         } else {
             // same (c_me, rows t0 + i T) assignment as the load phase
@@ -742,15 +768,27 @@ k_ntt_pass(const PassArgs a) {
                         outv[i] = u128_to(mont_mul(u128_from(outv[i]),
                                                    u128_from(__ldg(a.fout + m_me * a.f_stride + gbase + (size_t)i * gstride)), q, M.qinv0));
                 }
+                if (!SINGLE && a.r_lb && lo + B == n) {   // four-step: into the destination rank's block
 #pragma unroll
-                for (int i = 0; i < PER; i++) dstp[(size_t)i * gstride] = outv[i];
+                    for (int i = 0; i < PER; i++) {
+                        const uint64_t k = gbase + (size_t)i * gstride;
+                        a.rdst[k >> a.r_lb][poly_me * a.r_ps + (k & ((1ull << a.r_lb) - 1))] = outv[i];
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < PER; i++) dstp[(size_t)i * gstride] = outv[i];
+                }
             }
         }
     }
     if (!SINGLE && a.cnt_out) {
         // all of this CTA's stores happen-before the release (barrier + cumulative release)
         __syncthreads();
-        if (tid == 0) red_release_gpu_add(a.cnt_out + (gg0 >> gbits), 1u);
+        if (PM) {                         // one signal per polynomial of the CTA
+            if (tid < C) red_release_gpu_add(a.cnt_out + (gg_of(tid) >> gbits), 1u);
+        } else if (tid == 0) {
+            red_release_gpu_add(a.cnt_out + (gg0 >> gbits), 1u);
+        }
     }
 #if NTT_TRACE
     if (tid == 0 && !SINGLE && g_trace) {
@@ -1109,11 +1147,11 @@ struct PassCfg {
     size_t smem;
 };
 
-template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE = false, int RBMAX = 3>
+template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE = false, int RBMAX = 3, bool PM = false>
 static PassCfg make_cfg() {
     using S = PassShape<B, RBMAX, C, !SINGLE>;
     PassCfg c;
-    c.fn = k_ntt_pass<B, C, FIRST, SCALE_LAST, SINGLE, RBMAX>;
+    c.fn = k_ntt_pass<B, C, FIRST, SCALE_LAST, SINGLE, RBMAX, PM>;
     c.B = B;
     c.C = C;
     c.threads = C * S::T;
@@ -1210,6 +1248,23 @@ static std::vector<int> nc_pass_bits(int n) {
     for (int i = 0; i < np; i++) b.push_back(n / np + (i < n % np ? 1 : 0));
     return b;
 }
+
+// Four-step pass C reads the columns of a received matrix (element stride = the number of
+// polynomials, polynomials adjacent in memory): groups of adjacent polynomials per CTA.
+//  * single pass: C polynomials per CTA (lanes c = tid % C are adjacent residues); B = 9
+//    (cfg 5's 2^9-point pass C) takes 4 instead of the contiguous-layout 1;
+//  * multi-pass first pass with 9 stages (cfg 5's inverse pass C, 2^17 = 9 + 8): the
+//    polynomial-major kernel (PM, 4 polynomials per CTA); other widths keep their shape.
+#ifndef NTT_FS_C
+#define NTT_FS_C 4
+#endif
+static PassCfg strided_single_cfg(int B, bool scale_last, uint32_t batch) {
+    if (B == 9 && batch % NTT_FS_C == 0)
+        return scale_last ? make_cfg<9, NTT_FS_C, true, true, true>() : make_cfg<9, NTT_FS_C, true, false, true>();
+    return scale_last ? single_cfg_t<true>(B) : single_cfg_t<false>(B);
+}
+static bool strided_pm_first(int B, uint32_t batch) { return B == 9 && batch % NTT_FS_C == 0; }
+static PassCfg strided_pm_cfg() { return make_cfg<9, NTT_FS_C, true, false, false, NTT_RB9, true>(); }
 
 #ifndef NTT_WIDE_STRIDE
 #define NTT_WIDE_STRIDE 17
@@ -1629,6 +1684,7 @@ struct RunOpts {
     bool inverse;
     const uint4* pmul;     // fused point-wise product (polymul inverse)
     bool polymul;          // use the R-compensated inverse tables
+    const Ntt128IO* io = nullptr;   // four-step input / output layouts (fourstep.cu)
 };
 
 static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaStream_t stream);
@@ -1703,19 +1759,21 @@ static ntt128_plan_s::StreamCtr* stream_entry(ntt128_plan_s* p, unsigned long lo
     it->second.tick = ++p->tick;
     return &it->second;
 }
-// Record the end of this call's use of the stream's entry (or pin it under capture).
+static bool is_capturing(cudaStream_t stream) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) return false;
+    return cs != cudaStreamCaptureStatusNone;
+}
+// Record the end of this call's use of the stream's entry.  Under stream capture nothing of
+// the cache is used (cudaStreamGetId would invalidate the capture; counters are bypassed and
+// scratch comes from graph-owned stream-ordered allocations), so there is nothing to record.
 static void stream_touch(ntt128_plan_s* p, cudaStream_t stream) {
+    if (is_capturing(stream)) return;
     unsigned long long sid = 0;
     if (cudaStreamGetId(stream, &sid) != cudaSuccess) return;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(stream, &cs);
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->ctrs.find(sid);
     if (it == p->ctrs.end()) return;
-    if (cs != cudaStreamCaptureStatusNone) {
-        it->second.pinned = true;
-        return;
-    }
     if (!it->second.ev && cudaEventCreateWithFlags(&it->second.ev, cudaEventDisableTiming) != cudaSuccess) {
         it->second.ev = nullptr;
         it->second.pinned = true;   // cannot prove it idle: never evict
@@ -1764,6 +1822,26 @@ static ntt128_status stream_scratch(ntt128_plan_s* p, cudaStream_t stream, size_
     return NTT128_OK;
 }
 
+// Scratch for one call: the stream's cached buffer, or -- under stream capture -- a
+// stream-ordered allocation the caller frees on the same stream after its last use (a
+// graph memory node: the captured graph owns it, so no cache entry is involved).
+struct CallScratch {
+    uint4* ptr = nullptr;
+    bool graph_owned = false;
+};
+static ntt128_status acquire_scratch(ntt128_plan_s* p, cudaStream_t stream, size_t elems, CallScratch* cs) {
+    if (is_capturing(stream)) {
+        if (cudaMallocAsync(&cs->ptr, elems * sizeof(uint4), stream) != cudaSuccess) return NTT128_ERR_OOM;
+        cs->graph_owned = true;
+        return NTT128_OK;
+    }
+    return stream_scratch(p, stream, elems, &cs->ptr);
+}
+static void release_scratch(ntt128_plan_s* p, cudaStream_t stream, const CallScratch& cs) {
+    if (cs.graph_owned) cudaFreeAsync(cs.ptr, stream);
+    else stream_touch(p, stream);
+}
+
 // pass i (of npass, execution order) of an overlapped transform: the first pass waits for
 // the previous grid; pass i > 0 waits on row i - 1 for the previous pass's CTAs per
 // polynomial; every pass but the last signals row i.
@@ -1790,7 +1868,7 @@ static void set_overlap(ntt128_plan_s* p, ntt128_plan_s::StreamCtr* ctr, PassArg
 #define NTT_CLU_MAX_BATCH 512
 #endif
 static bool use_cluster(const ntt128_plan_s* p, const RunOpts& o) {
-    if (switches().no_cluster || p->kind != 0 || o.pmul || p->bits.size() != 1) return false;
+    if (switches().no_cluster || p->kind != 0 || o.pmul || o.io || p->bits.size() != 1) return false;
     return p->log2n >= 8 && p->log2n <= 11 && p->batch <= NTT_CLU_MAX_BATCH;
 }
 template <bool SL>
@@ -1866,6 +1944,18 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
         PassCfg c = pass_cfg(npass, i, B, scale_last, lo, n);
         if (npass == 1 && use_latency_shape(B, p->batch))
             c = scale_last ? single_lat_cfg_t<true>(B) : single_lat_cfg_t<false>(B);
+        bool pm = false;
+        if (i == 0 && o.io && o.io->in_ps == 1) {   // four-step pass C: adjacent polynomials per CTA
+            if (npass == 1) {
+                c = strided_single_cfg(B, scale_last, p->batch);
+            } else if (strided_pm_first(B, p->batch)) {
+                c = strided_pm_cfg();
+                pm = true;
+            }
+            // > 48 KB of dynamic shared memory (set on the plan's device, as plan_create does)
+            if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
+                return NTT128_ERR_CUDA;
+        }
         PassArgs a;
         memset(&a, 0, sizeof(a));
         a.src = i == 0 ? src : dst;
@@ -1886,7 +1976,25 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
             if (!o.inverse && first) a.fin = p->d_f_twist;
             if (o.inverse && last) a.fout = o.polymul ? p->d_f_untwist_r : p->d_f_untwist;
         }
-        const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (uint64_t)c.C);
+        a.in_ps = p->N;
+        a.in_es = 1;
+        if (o.io) {
+            if (first && o.io->in_ps) {
+                a.in_ps = o.io->in_ps;
+                a.in_es = o.io->in_es;
+            }
+            if (first && o.io->fin) {
+                a.fin = o.io->fin;
+                a.fpoly = 1;
+            }
+            if (last && o.io->r_lb) {
+                a.r_lb = o.io->r_lb;
+                a.r_ps = o.io->r_ps;
+                for (int h = 0; h < NTT128_FS_MAX_RANKS; h++) a.rdst[h] = o.io->rdst[h];
+            }
+        }
+        // CTAs that signal each polynomial's counter (a PM CTA signals all of its C polynomials)
+        const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (pm ? 1u : (uint64_t)c.C));
         if (overlap) set_overlap(p, ctr, a, i, npass, prev_ctas_per_poly);
         if (pdl_single) a.pdl_wait = 1u;
         const uint64_t ctas = (a.total_groups + c.C - 1) / c.C;
@@ -1993,12 +2101,12 @@ static ntt128_status transform(const ntt128_plan_t p, const uint64_t* d_in, uint
     if (src == dst && p->bits.size() > 1) {
         // the first pass gathers bit-reversed columns: it cannot run in place
         const size_t bytes = (size_t)p->N * p->batch * sizeof(uint4);
-        uint4* tmp = nullptr;
-        ntt128_status s = stream_scratch(p, stream, (size_t)p->N * p->batch, &tmp);
+        CallScratch cs;
+        ntt128_status s = acquire_scratch(p, stream, (size_t)p->N * p->batch, &cs);
         if (s != NTT128_OK) return s;
-        if (cudaMemcpyAsync(tmp, src, bytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess) return NTT128_ERR_CUDA;
-        s = run_transform(p, tmp, dst, stream, o);
-        stream_touch(p, stream);
+        if (cudaMemcpyAsync(cs.ptr, src, bytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess) s = NTT128_ERR_CUDA;
+        else s = run_transform(p, cs.ptr, dst, stream, o);
+        release_scratch(p, stream, cs);
         return s;
     }
     const ntt128_status s = run_transform(p, src, dst, stream, o);
@@ -2025,9 +2133,10 @@ extern "C" ntt128_status ntt128_polymul(const ntt128_plan_t p, const uint64_t* d
         if (s == NTT128_OK) s = check_range(p, (const uint4*)d_b, stream);
         if (s != NTT128_OK) return s;
     }
-    uint4* fa = nullptr;
-    ntt128_status s = stream_scratch(p, stream, 2 * (size_t)p->N * p->batch, &fa);
+    CallScratch cs;
+    ntt128_status s = acquire_scratch(p, stream, 2 * (size_t)p->N * p->batch, &cs);
     if (s != NTT128_OK) return s;
+    uint4* fa = cs.ptr;
     uint4* fb = fa + (size_t)p->N * p->batch;
     if (!p->nc_bits.empty() && !switches().no_nc) {
         // permutation-free pipeline: no twist / untwist multiplies, spectra stay bit-reversed
@@ -2042,7 +2151,7 @@ extern "C" ntt128_status ntt128_polymul(const ntt128_plan_t p, const uint64_t* d
         RunOpts inv{true, fb, true};
         if (s == NTT128_OK) s = run_transform(p, fa, (uint4*)d_c, stream, inv);
     }
-    stream_touch(p, stream);
+    release_scratch(p, stream, cs);
     return s;
 }
 
@@ -2068,4 +2177,24 @@ extern "C" ntt128_status ntt128_forward_bitrev(const ntt128_plan_t p, const uint
 extern "C" ntt128_status ntt128_inverse_bitrev(const ntt128_plan_t p, const uint64_t* d_in, uint64_t* d_out,
                                                ntt128_stream_t stream) {
     return transform_bitrev(p, d_in, d_out, (cudaStream_t)stream, true);
+}
+
+// Four-step sub-transform with non-natural input / output (ntt128_internal.h).
+ntt128_status ntt128_transform_io(ntt128_plan_t p, const uint4* src, uint4* dst, cudaStream_t stream, bool inverse,
+                                  const Ntt128IO& io) {
+    if (!p || !src || p->kind != 0) return NTT128_ERR_INVALID_ARG;
+    if (io.r_lb) {
+        if (p->bits.size() > 1 && !io.tmp) return NTT128_ERR_INVALID_ARG;
+        for (uint64_t h = 0; h < (p->N >> io.r_lb); h++)
+            if (h >= NTT128_FS_MAX_RANKS || !io.rdst[h]) return NTT128_ERR_INVALID_ARG;
+        if (p->bits.size() > 1) dst = io.tmp;
+        else if (!dst) dst = io.rdst[0];
+    }
+    if (!dst) return NTT128_ERR_INVALID_ARG;
+    if (src == dst && p->bits.size() > 1) return NTT128_ERR_INVALID_ARG;
+    DeviceGuard g(p->device);
+    RunOpts o{inverse, nullptr, false, &io};
+    const ntt128_status s = run_transform(p, src, dst, stream, o);
+    if (p->bits.size() > 1) stream_touch(p, stream);
+    return s;
 }

@@ -1,9 +1,12 @@
 """Distributed four-step NTT of one huge polynomial over G ranks (one process per GPU).
 
 Binding of the ntt128_fourstep_* C ABI (include/ntt128.h, "Distributed four-step") plus
-the host-side exchange: each rank runs its local pass A in the library, the packed
-blocks move with ONE all-to-all of equal splits (torch.distributed, NCCL over
-NVLink/NVSwitch on GPUs), then the local pass C.  No arithmetic happens here.
+the host-side exchange: each rank runs its local pass A in the library (its last pass
+stores every output into the block of its destination rank), the blocks move with ONE
+all-to-all of equal splits (torch.distributed, NCCL over NVLink/NVSwitch on GPUs) -- or,
+with transport="p2p", pass A stores them straight into the peers' receive buffers -- then
+the local pass C (whose first pass gathers the received columns and applies the
+four-step twiddle as it loads).  No arithmetic happens here.
 
 Layouts (N = n1 n2, R1 = n1/G, R2 = n2/G, rank g):
   columns  X_g[r][j2] = x[(g R1 + r) + n1 j2]     (forward input, inverse output)
@@ -37,8 +40,12 @@ _L.ntt128_fourstep_destroy.restype = None
 
 # ----------------------------------------------------------------------------- layouts (host index maps)
 def split(log2n: int) -> tuple[int, int]:
-    """n1 = 2^ceil(log2n/2), n2 = 2^floor(log2n/2) exponents (2^13 x 2^13 for N = 2^26)"""
-    return (log2n + 1) // 2, log2n // 2
+    """(log2 n1, log2 n2): n1 = 2^min(9, floor(log2n / 2)) is the length of pass C's forward
+    transforms (one 9-stage pass), n2 = N / n1 the length of pass A's (2^9 x 2^17 at
+    N = 2^26: pass A two passes 9 + 8, pass C one, the same three passes as the
+    single-GPU plan)"""
+    l1 = min(9, log2n // 2)
+    return l1, log2n - l1
 
 
 def to_columns(x: np.ndarray, n1: int, n2: int, rank: int, world: int) -> np.ndarray:

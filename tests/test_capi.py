@@ -77,7 +77,9 @@ def test_fourstep_validation_host_only(N, params):
     h = C.c_void_p()
     f = N._L.ntt128_fourstep_create
     assert f(C.byref(h), 0, 13, N._pairs([q]), N._pairs([w]), 0, 1, 0) == 1      # log2n1 out of range
-    assert f(C.byref(h), 13, 14, N._pairs([q]), N._pairs([w]), 0, 1, 0) == 1     # log2n2 out of range
+    assert f(C.byref(h), 13, 14, N._pairs([q]), N._pairs([w]), 0, 1, 0) == 1     # log2n1 + log2n2 > 26
+    assert f(C.byref(h), 9, 0, N._pairs([q]), N._pairs([w]), 0, 1, 0) == 1       # log2n2 out of range
+    assert f(C.byref(h), 9, 17, N._pairs([q]), N._pairs([w]), 0, 16, 0) == 1     # world > 8
     assert f(C.byref(h), 13, 13, N._pairs([q]), N._pairs([w]), 0, 3, 0) == 1     # world not a power of two
     assert f(C.byref(h), 13, 13, N._pairs([q]), N._pairs([w]), 2, 2, 0) == 1     # rank >= world
     assert f(C.byref(h), 2, 2, N._pairs([q]), N._pairs([w]), 0, 8, 0) == 1      # world > n1

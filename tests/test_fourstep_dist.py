@@ -34,28 +34,34 @@ class OracleLocal:
         self.q, self.w, self.rank, self.world = q, w, rank, world
         self.R1, self.R2 = self.n1 // world, self.n2 // world
 
-    def _pack(self, z, R, C, row0, w):
-        CG = C // self.world
+    def _blocks(self, z, R, C):
+        """z[R][C] -> send[G][R][C/G]: block h holds the columns [h C/G, (h+1) C/G)"""
+        return np.ascontiguousarray(z.reshape(R, self.world, C // self.world, 2).transpose(1, 0, 2, 3))
+
+    def _twiddle(self, m, row0, w):
+        """m[r][c] * w^((row0 + r) c): the four-step twiddle, applied in pass C"""
+        R, C = m.shape[0], m.shape[1]
         tw = np.stack([synth.from_ints([pow(w, ((row0 + r) * c) % self.N, self.q) for c in range(C)]) for r in range(R)])
-        v = O.vmul(z.reshape(-1, 2), tw.reshape(-1, 2), self.q).reshape(R, C, 2)
-        return np.ascontiguousarray(v.reshape(R, self.world, CG, 2).transpose(1, 0, 2, 3))
+        return O.vmul(np.ascontiguousarray(m).reshape(-1, 2), tw.reshape(-1, 2), self.q).reshape(R, C, 2)
 
     def forward_a(self, cols, send):
-        z = O.ntt(_n(cols), self.q, pow(self.w, self.n1, self.q))
-        send.copy_(_t(self._pack(z, self.R1, self.n2, self.rank * self.R1, self.w)))
+        z = O.ntt(_n(cols), self.q, pow(self.w, self.n1, self.q))          # [R1][n2]
+        send.copy_(_t(self._blocks(z, self.R1, self.n2)))
 
     def forward_c(self, recv, rows):
-        m = _n(recv).reshape(self.n1, self.R2, 2).transpose(1, 0, 2)
-        rows.copy_(_t(O.ntt(np.ascontiguousarray(m), self.q, pow(self.w, self.n2, self.q))))
+        m = _n(recv).reshape(self.n1, self.R2, 2).transpose(1, 0, 2)       # [R2][n1]: row cc = k2 = rank R2 + cc
+        m = self._twiddle(m, self.rank * self.R2, self.w)
+        rows.copy_(_t(O.ntt(m, self.q, pow(self.w, self.n2, self.q))))
         return rows
 
     def inverse_a(self, rows, send):
-        z = O.intt(_n(rows), self.q, pow(self.w, self.n2, self.q))
-        send.copy_(_t(self._pack(z, self.R2, self.n1, self.rank * self.R2, pow(self.w, -1, self.q))))
+        z = O.intt(_n(rows), self.q, pow(self.w, self.n2, self.q))         # [R2][n1]
+        send.copy_(_t(self._blocks(z, self.R2, self.n1)))
 
     def inverse_c(self, recv, cols):
-        m = _n(recv).reshape(self.n2, self.R1, 2).transpose(1, 0, 2)
-        cols.copy_(_t(O.intt(np.ascontiguousarray(m), self.q, pow(self.w, self.n1, self.q))))
+        m = _n(recv).reshape(self.n2, self.R1, 2).transpose(1, 0, 2)       # [R1][n2]: row m = j1 = rank R1 + m
+        m = self._twiddle(m, self.rank * self.R1, pow(self.w, -1, self.q))
+        cols.copy_(_t(O.intt(m, self.q, pow(self.w, self.n1, self.q))))
         return cols
 
 

@@ -129,3 +129,32 @@ def test_three_pass_chain(N, params):
     for y in ys:
         assert np.array_equal(to_host(y), ref)
     assert np.array_equal(to_host(cur), x)
+
+
+def test_graph_capture_in_place_and_polymul(N, params):
+    """in-place multi-pass transforms and polymul captured in a CUDA graph: their scratch is
+    a graph-owned stream-ordered allocation (no per-stream cache lookup under capture)"""
+    import torch
+    mods = params["cfg3"]["moduli"][:4]
+    qs, psis = [m["q"] for m in mods], [m["psi"] for m in mods]
+    ws = [pow(m["omega"], 2, m["q"]) for m in mods]          # order 2^15
+    n, B = 1 << 15, 4
+    x = np.stack([synth.uniform_residues(qs[i], n, synth.stream_seed(3, 0, 800 + i)) for i in range(B)])
+    b = np.stack([synth.uniform_residues(qs[i], n, synth.stream_seed(3, 1, 800 + i)) for i in range(B)])
+    plan = N.Plan(15, qs, ws, batch=B)
+    pn = N.Plan(15, qs, [pow(p, 2, q) for p, q in zip(psis, qs)], batch=B, negacyclic=True)
+    d, da, db, dc = to_dev(x), to_dev(x), to_dev(b), torch.empty_like(to_dev(x))
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.forward(d, out=d)
+        pn.polymul(da, db, out=dc)
+    ref = O.ntt(x, qs, ws)
+    refc = O.negacyclic_polymul(x, b, qs, [pow(p, 2, q) for p, q in zip(psis, qs)])
+    for _ in range(3):
+        d.copy_(to_dev(x))
+        dc.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(d), ref)
+        assert np.array_equal(to_host(dc), refc)

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <vector>
 #include <algorithm>
+#include <cstdlib>
+#include <ctime>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
 
@@ -131,10 +133,19 @@ __global__ void k_mixed(uint64_t* out, uint32_t seed, int iters, long long* cyc)
 typedef void (*kfn)(uint64_t*, uint32_t, int, long long*);
 struct K { const char* name; kfn f; double ops_per_step; const char* unit; };
 
+// Every kernel is launched as exactly one wave (SMs x its measured occupancy), then re-launched
+// back to back for >= 1 s of wall time (sustained clocks); tools/micro/int_peak.py reads the
+// NVML clock samples of each kernel's [t_begin, t_end] window.  ops_per_clk_per_sm is
+// computed from clock64 with the ACTUAL resident blocks per SM (round 1 assumed 8).
+static double now_s() {
+  timespec ts; clock_gettime(CLOCK_REALTIME, &ts); return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
 int main(int argc, char** argv) {
   int dev = 0; CK(cudaSetDevice(dev));
   cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, dev));
   int sms = p.multiProcessorCount;
+  const double min_s = argc > 1 ? atof(argv[1]) : 1.5;
   printf("{\"device\":\"%s\",\"sms\":%d,\"l2_bytes\":%d,\"smem_per_sm\":%zu,\"regs_per_sm\":%d}\n", p.name, sms, p.l2CacheSize, p.sharedMemPerMultiprocessor, p.regsPerMultiprocessor);
   K ks[] = {
     {"imad_wide_u32", k_imad_wide, ILP, "32x32->64 products"},
@@ -144,27 +155,39 @@ int main(int argc, char** argv) {
     {"iadd_cc_chain", k_iadd_cc, 4.0 * ILP, "32-bit adds with carry"},
     {"mixed_wide_lop3", k_mixed, ILP, "IMAD.WIDE (+1 LOP3 each)"},
   };
-  uint64_t* d_out; long long* d_cyc; CK(cudaMalloc(&d_out, 8)); 
-  const int threads = 256; const int blocks = sms * 8; const int iters = 4096;
-  CK(cudaMalloc(&d_cyc, sizeof(long long) * blocks));
+  uint64_t* d_out; long long* d_cyc; CK(cudaMalloc(&d_out, 8));
+  const int threads = 256; const int iters = 4096;
+  CK(cudaMalloc(&d_cyc, sizeof(long long) * sms * 32));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (auto& k : ks) {
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.f, threads, 0));
+    const int blocks = sms * occ;
     for (int w = 0; w < 3; w++) k.f<<<blocks, threads>>>(d_out, 1234u, iters, d_cyc);
     CK(cudaDeviceSynchronize());
-    float best = 1e30f; std::vector<long long> cyc(blocks);
-    for (int r = 0; r < 5; r++) {
-      cudaEventRecord(e0); k.f<<<blocks, threads>>>(d_out, 1234u, iters, d_cyc); cudaEventRecord(e1);
-      CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms);
+    // sustained: back-to-back launches for >= min_s seconds
+    const double t_begin = now_s();
+    long launches = 0; float total_ms = 0.f;
+    while (total_ms < 1e3 * min_s) {
+      cudaEventRecord(e0);
+      for (int r = 0; r < 50; r++) k.f<<<blocks, threads>>>(d_out, 1234u, iters, d_cyc);
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1);
+      total_ms += ms; launches += 50;
     }
+    const double t_end = now_s();
+    std::vector<long long> cyc(blocks);
     CK(cudaMemcpy(cyc.data(), d_cyc, sizeof(long long) * blocks, cudaMemcpyDeviceToHost));
     std::sort(cyc.begin(), cyc.end());
-    double ops = (double)blocks * threads * iters * k.ops_per_step;
-    double rate = ops / (best * 1e-3);
-    // per-SM-per-clock from the median block's clock64 span (8 blocks resident per SM run concurrently)
-    double med_cyc = (double)cyc[blocks / 2];
-    double per_sm_clk = (double)threads * 8 * iters * k.ops_per_step / med_cyc;
-    printf("{\"kernel\":\"%s\",\"unit\":\"%s\",\"ms\":%.4f,\"ops_per_s\":%.4e,\"ops_per_clk_per_sm\":%.2f,\"implied_mhz\":%.0f}\n",
-           k.name, k.unit, best, rate, per_sm_clk, rate / (per_sm_clk * sms) / 1e6);
+    const double ops = (double)launches * blocks * threads * iters * k.ops_per_step;
+    const double rate = ops / (total_ms * 1e-3);
+    // one wave: each SM runs `occ` blocks concurrently over the median block's clock64 span
+    const double med_cyc = (double)cyc[blocks / 2];
+    const double per_sm_clk = (double)occ * threads * iters * k.ops_per_step / med_cyc;
+    printf("{\"kernel\":\"%s\",\"unit\":\"%s\",\"blocks_per_sm\":%d,\"launches\":%ld,\"seconds\":%.3f,\"ops_per_s\":%.4e,"
+           "\"ops_per_clk_per_sm\":%.3f,\"implied_mhz\":%.0f,\"t_begin\":%.3f,\"t_end\":%.3f}\n",
+           k.name, k.unit, occ, launches, total_ms * 1e-3, rate, per_sm_clk, rate / (per_sm_clk * sms) / 1e6, t_begin, t_end);
+    fflush(stdout);
   }
   return 0;
 }
