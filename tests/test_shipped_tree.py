@@ -46,5 +46,5 @@ def test_no_closed_copy_api_names_in_shipped_tree():
 
 def test_no_tracked_micro_binaries():
     out = subprocess.run(["git", "ls-files", "tools/micro"], cwd=ROOT, capture_output=True, text=True).stdout.split()
-    bad = [f for f in out if not (f.endswith(".cu") or f.endswith(".sh"))]
+    bad = [f for f in out if not f.endswith((".cu", ".cuh", ".sh", ".py"))]
     assert not bad, f"tracked executables under tools/micro: {bad}"
