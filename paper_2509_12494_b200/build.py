@@ -50,8 +50,9 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    with open(os.path.join(CSRC, "ptxas_info.txt"), "w") as f:
-        f.write("\n".join(logs))
+    if lib == LIB:   # the product build's register / spill report
+        with open(os.path.join(CSRC, "ptxas_info.txt"), "w") as f:
+            f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
     return lib

@@ -14,7 +14,7 @@
 // NVLink: the exchange is the epilogue of the transform); pass C's FIRST pass gathers the
 // columns of the received [n1][R2] matrix directly (element stride R2) and multiplies the
 // four-step twiddle w^{j1 k2} in as it loads -- one Montgomery product per element from a
-// per-rank factor table [R2][n1] (plan time).  No separate twiddle, pack or transpose
+// per-rank factor table [n1][R2] (plan time, laid out like the received matrix).  No separate twiddle, pack or transpose
 // kernel and no extra HBM round trip: a direction is the same 3 passes as the single-GPU
 // plan (n2 = 2^17 as 9 + 8, n1 = 2^9 as one pass at cfg 5).
 // The inverse swaps the roles: pass A = n1-point inverse NTTs of the rows (x n1^{-1}) into
@@ -45,13 +45,14 @@ struct FsConst {
     uint32_t one_m[4];
 };
 
-// out[r][c] = w^{((row0 + r) c) mod N} (Montgomery form), r < R, c < C, from
+// out[c][r] = w^{((row0 + r) c) mod N} (Montgomery form), r < R, c < C -- laid out like the
+// received matrix pass C reads (input index c major, polynomial r adjacent), from
 // pw[b] = w^{2^b} (Montgomery form): square-and-multiply over the exponent's bits.
 __global__ void k_fs_factors(uint4* out, uint64_t R, uint64_t C, uint64_t row0, uint64_t nmask, const uint4* pw,
                              const FsConst k) {
     const uint64_t total = R * C;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t r = i / C, c = i - r * C;
+        const uint64_t c = i / R, r = i - c * R;
         uint64_t e = ((row0 + r) * c) & nmask;
         U128 v = U128{{k.one_m[0], k.one_m[1], k.one_m[2], k.one_m[3]}};
         for (int b = 0; e; b++, e >>= 1)
@@ -71,8 +72,8 @@ struct ntt128_fourstep_s {
     uint64_t n1, n2, N, R1, R2;
     int device;
     ntt128_plan_t p1 = nullptr, p2 = nullptr;  // n1-point x R2 (root w^{n2}), n2-point x R1 (root w^{n1})
-    uint4* d_ff = nullptr;                     // [R2][n1]: w^{j1 (rank R2 + r)}     (forward pass C)
-    uint4* d_fi = nullptr;                     // [R1][n2]: w^{-(rank R1 + r) k2}    (inverse pass C)
+    uint4* d_ff = nullptr;                     // [n1][R2]: w^{j1 (rank R2 + r)}     (forward pass C)
+    uint4* d_fi = nullptr;                     // [n2][R1]: w^{-(rank R1 + r) k2}    (inverse pass C)
     uint4* d_tmp = nullptr;                    // N/G: pass A's working buffer (multi-pass sub-transforms)
 };
 
@@ -197,7 +198,9 @@ ntt128_status pass_c(const ntt128_fourstep_s* f, ntt128_plan_t plan, bool invers
     Ntt128IO io;
     io.in_ps = 1;
     io.in_es = R_in;
-    io.fin = fac;
+    io.fin = fac;                 // [n_sub][R_in]: same layout as the received matrix
+    io.fin_ps = 1;
+    io.fin_es = R_in;
     (void)f;
     return ntt128_transform_io(plan, (const uint4*)d_recv, (uint4*)d_out, st, inverse, io);
 }

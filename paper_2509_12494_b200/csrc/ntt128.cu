@@ -185,6 +185,32 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Bulk copies (SASS UBLKCP) completing on an mbarrier (NTT_BULK, DESIGN.md §6 "Bulk staging").
+#ifndef NTT_BULK
+#define NTT_BULK 0   // bit 0: twiddle sets by bulk copy; bit 1: first-pass stores by bulk copy
+#endif
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra W;\n\t}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+
 
 // ----------------------------------------------------------------------------- twiddle generation
 // out[m][i] = scale_m * base_m^i (Montgomery form), i < count; pow2[m][k] = base_m^{2^k}
@@ -286,11 +312,12 @@ struct PassArgs {
     // Four-step I/O (fourstep.cu; natural [batch][N] when left at the defaults):
     //  * the pass reads element idx of polynomial p at src[p in_ps + idx in_es] (default N, 1;
     //    a first pass may read the columns of a received [n][batch] matrix: in_ps 1, in_es batch);
-    //  * fpoly: fin is indexed by polynomial instead of modulus ([batch][f_stride]);
+    //  * fpoly: fin is indexed by polynomial instead of modulus, at fin[p f_ps + idx f_es];
     //  * r_lb != 0 (the transform's last pass): output k of polynomial p goes to
     //    rdst[k >> r_lb] + p r_ps + (k mod 2^r_lb) -- the destination rank's block of the
     //    all-to-all send buffer, or that rank's receive buffer itself (peer memory).
     uint64_t in_ps, in_es;
+    uint64_t f_ps, f_es;     // fpoly: factor of (p, idx) at fin[p f_ps + idx f_es]
     uint32_t fpoly, r_lb;
     uint64_t r_ps;
     uint4* rdst[NTT128_FS_MAX_RANKS];
@@ -525,6 +552,7 @@ k_ntt_pass(const PassArgs a) {
     constexpr int NTW = (FIRST && !SINGLE) ? 1 : C;  // twiddle sets: a multi-pass first pass shares one (L = 0)
     extern __shared__ uint4 sm[];
     uint4* tsm = sm + C * GS;                        // [NTW][TS] pass-local twiddles
+    __shared__ __align__(8) uint64_t tw_bar;         // NTT_BULK: twiddle bulk copies
 
     const uint32_t n = a.n, lo = a.lo, gbits = n - B;
     const uint64_t N = 1ull << n;
@@ -569,7 +597,19 @@ k_ntt_pass(const PassArgs a) {
         // (2^sl - 1) + jj for local stage sl), precomputed per pass at plan time; the sets
         // of one CTA (consecutive L, same polynomial) are consecutive runs of the table.
         constexpr int TW_IT = (G - 1 + NT - 1) / NT;
-        if (NTW == 1 || !(FIRST && SINGLE)) {
+        if ((NTT_BULK & 1) && !SINGLE) {
+            // one thread streams the CTA's twiddle sets (contiguous runs of the pass table)
+            // with bulk copies; the other threads wait on the mbarrier after the data phase
+            if (tid == 0) {
+                const uint64_t L0 = FIRST ? 0 : ((gg0 & gmask) & ((1ull << lo) - 1));
+                const uint32_t m0 = a.nq == 1 ? 0 : (uint32_t)((gg0 < a.total_groups ? gg0 : a.total_groups - 1) >> gbits);
+                const uint4* src = a.pt + m0 * a.pt_stride + L0 * (G - 1);
+                mbar_init(&tw_bar, 1);
+                mbar_expect_tx(&tw_bar, NTW * (G - 1) * 16);
+#pragma unroll
+                for (int c = 0; c < NTW; c++) bulk_g2s(tsm + c * TS, src + c * (G - 1), (G - 1) * 16, &tw_bar);
+            }
+        } else if (NTW == 1 || !(FIRST && SINGLE)) {
             const uint64_t L0 = FIRST ? 0 : ((gg0 & gmask) & ((1ull << lo) - 1));
             const uint32_t m0 = a.nq == 1 ? 0 : (uint32_t)((gg0 < a.total_groups ? gg0 : a.total_groups - 1) >> gbits);
             const uint4* src = a.pt + m0 * a.pt_stride + L0 * (G - 1) + tid;
@@ -659,13 +699,14 @@ k_ntt_pass(const PassArgs a) {
             const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
             const uint64_t idx = gbase + (size_t)i * gstride;
             U128 x = u128_from(stage[i]);
-            if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + (a.fpoly ? poly_me : m_me) * a.f_stride + idx)), q, M.qinv0);
+            if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + (a.fpoly ? poly_me * a.f_ps + idx * a.f_es : m_me * a.f_stride + idx))), q, M.qinv0);
             if (a.pmul) x = mont_mul(x, u128_from(__ldg(a.pmul + poly_me * N + idx)), q, M.qinv0);
             smc[slot<B, PADL, RB>(l)] = u128_to(x);
         }
     }
     cp_async_wait_all();
     __syncthreads();
+    if ((NTT_BULK & 1) && !SINGLE) mbar_wait(&tw_bar, 0);
 #if NTT_TRACE
     const uint32_t tr_t1 = gtimer_lo();
 #endif
@@ -711,7 +752,25 @@ k_ntt_pass(const PassArgs a) {
     // ---------------- store phase: shared -> global, coalesced; all smem reads first
     {
         uint4 outv[PER];
-        if (FIRST) {
+        if ((NTT_BULK & 2) && FIRST && !SINGLE && gbits > 0 && !a.fout) {
+            // a group's output is one contiguous row of the working order (G residues at
+            // brev(g) G): its 8-residue chunks (128 B, contiguous in the padded layout) leave
+            // by bulk copies, one per thread; results must be visible to the async proxy first
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            constexpr int CH = G / 8;
+            for (int j = tid; j < C * CH; j += NT) {
+                const int c = j / CH, k = j - c * CH;
+                const uint64_t gg = gg_of(c);
+                if (gg >= a.total_groups) continue;
+                const uint64_t poly = gg >> gbits, g = gg & gmask;
+                uint4* dstp = a.dst + poly * N + ((uint64_t)brev_bits((uint32_t)g, gbits) << B) + 8 * k;
+                bulk_s2g(dstp, sm + c * GS + 9 * k, 128);
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");     // written (the next pass may read)
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        } else if (FIRST) {
             // groups are contiguous rows of the working order: e = tid + i NT -> (c, l), l fastest
 #pragma unroll
             for (int i = 0; i < PER; i++) {
@@ -727,13 +786,26 @@ k_ntt_pass(const PassArgs a) {
                 const uint64_t poly = gg >> gbits, g = gg & gmask;
                 const uint64_t idx = ((uint64_t)brev_bits((uint32_t)g, gbits) << B) | (uint64_t)l;
                 uint4 v = outv[i];
+                if (!SINGLE && gbits == 0 && !a.fout) {
+                    // the whole transform was this pass (four-step sub-transforms of 2^9 run the
+                    // padded multi-pass kernel as their single pass): lazy classes -> canonical
+                    const ModC& M = a.mods[a.nq == 1 ? 0 : (uint32_t)poly];
+                    const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+                    const int mode = mode_of(q);
+                    if (mode == MODE_LAZY) {
+                        const uint32_t q2[4] = {q[0] << 1, (q[1] << 1) | (q[0] >> 31), (q[2] << 1) | (q[1] >> 31),
+                                                (q[3] << 1) | (q[2] >> 31)};
+                        v = u128_to(reduce_2q(u128_from(v), q2));
+                    }
+                    if (mode != MODE_FULL) v = u128_to(reduce_2q(u128_from(v), q));
+                }
                 if (a.fout) {
                     const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
                     const ModC& M = a.mods[m];
                     const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
                     v = u128_to(mont_mul(u128_from(v), u128_from(__ldg(a.fout + m * a.f_stride + idx)), q, M.qinv0));
                 }
-                if (SINGLE && a.r_lb)   // four-step: straight into the destination rank's block
+                if ((SINGLE || gbits == 0) && a.r_lb)   // four-step: straight into the destination rank's block
                     a.rdst[idx >> a.r_lb][poly * a.r_ps + (idx & ((1ull << a.r_lb) - 1))] = v;
                 else
                     a.dst[poly * N + idx] = v;
@@ -1265,6 +1337,7 @@ static PassCfg strided_single_cfg(int B, bool scale_last, uint32_t batch) {
 }
 static bool strided_pm_first(int B, uint32_t batch) { return B == 9 && batch % NTT_FS_C == 0; }
 static PassCfg strided_pm_cfg() { return make_cfg<9, NTT_FS_C, true, false, false, NTT_RB9, true>(); }
+
 
 #ifndef NTT_WIDE_STRIDE
 #define NTT_WIDE_STRIDE 17
@@ -1945,7 +2018,14 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
         if (npass == 1 && use_latency_shape(B, p->batch))
             c = scale_last ? single_lat_cfg_t<true>(B) : single_lat_cfg_t<false>(B);
         bool pm = false;
-        if (i == 0 && o.io && o.io->in_ps == 1) {   // four-step pass C: adjacent polynomials per CTA
+        if (i == 0 && o.io && npass == 1 && B == 9 && o.io->in_ps == 1 && strided_pm_first(B, p->batch)) {
+            // four-step 2^9-point pass C: one polynomial-major pass of the padded multi-pass
+            // kernel (2.0 vs 2.07 ms for the 4-polynomial single-pass kernel at cfg 5)
+            c = strided_pm_cfg();
+            pm = true;
+            if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
+                return NTT128_ERR_CUDA;
+        } else if (i == 0 && o.io && o.io->in_ps == 1) {   // four-step pass C: adjacent polynomials per CTA
             if (npass == 1) {
                 c = strided_single_cfg(B, scale_last, p->batch);
             } else if (strided_pm_first(B, p->batch)) {
@@ -1986,6 +2066,8 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
             if (first && o.io->fin) {
                 a.fin = o.io->fin;
                 a.fpoly = 1;
+                a.f_ps = o.io->fin_ps;
+                a.f_es = o.io->fin_es;
             }
             if (last && o.io->r_lb) {
                 a.r_lb = o.io->r_lb;

@@ -14,14 +14,15 @@
 // Non-natural input / output of one batched cyclic transform (fourstep.cu):
 //  * the first pass reads element idx of polynomial p at src[p in_ps + idx in_es]
 //    (in_ps == 0: the natural [batch][N] layout);
-//  * fin (optional): per-polynomial factors [batch][N] (Montgomery form) multiplied into the
-//    inputs as the first pass loads them;
+//  * fin (optional): per-polynomial factors (Montgomery form), that of input idx of
+//    polynomial p at fin[p fin_ps + idx fin_es], multiplied in as the first pass loads it;
 //  * r_lb != 0: the last pass stores output k of polynomial p at
 //    rdst[k >> r_lb] + p r_ps + (k mod 2^r_lb); a multi-pass transform then works in `tmp`
 //    ([batch][N], natural) until its last pass.
 struct Ntt128IO {
     uint64_t in_ps = 0, in_es = 1;
     const uint4* fin = nullptr;
+    uint64_t fin_ps = 0, fin_es = 1;
     uint32_t r_lb = 0;
     uint64_t r_ps = 0;
     uint4* rdst[NTT128_FS_MAX_RANKS] = {};

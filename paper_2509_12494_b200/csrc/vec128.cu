@@ -87,6 +87,153 @@ __global__ void __launch_bounds__(THREADS) k_vec(uint4* z, const uint4* __restri
     }
 }
 
+// ---- bulk-copy pipeline (DESIGN.md §6 "BLAS"): one producer lane streams chunks of x and y
+// into a ring of shared-memory stages with cp.async.bulk (SASS UBLKCP), completion counted
+// on an mbarrier per stage (expect_tx); consumer warps compute and store z.  HBM reads run
+// from the first cycle at full depth whatever the consumers are doing, so the modular
+// products of chunk i overlap the loads of chunks i+1 .. i+S-1 (the one-wave kernel above
+// issues every thread's loads, then computes: its compute tail is exposed).
+// Shape <consumer warps, residues per stage and operand, stages>: two CTAs per SM.
+template <int CW, int CHUNK, int STAGES>
+struct PipeShape {
+    static constexpr int CWARPS = CW, PCHUNK = CHUNK, PSTAGES = STAGES;
+    static constexpr int THREADS = 32 * (CW + 1);            // warp CW is the producer
+    static constexpr size_t SMEM = (size_t)STAGES * 2 * CHUNK * sizeof(uint4);
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra W;\n\t}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <int OPK>
+__device__ __forceinline__ U128 vec_op1(const U128& a, const U128& b, const VecConst& c) {
+    if (OPK == OP_ADD) return add_mod(a, b, c.q);
+    if (OPK == OP_SUB) return sub_mod(a, b, c.q);
+    if (OPK == OP_MUL) return mont_mul(mont_mul(a, b, c.q, c.qinv0), U128{{c.r2[0], c.r2[1], c.r2[2], c.r2[3]}}, c.q, c.qinv0);
+    if (OPK == OP_MULB) return mul_b(a, b, c.bc);
+    return add_mod(mont_mul(a, U128{{c.a_m[0], c.a_m[1], c.a_m[2], c.a_m[3]}}, c.q, c.qinv0), b, c.q);
+}
+
+template <int OPK, class PS>
+__global__ void __launch_bounds__(PS::THREADS, 2) k_vec_pipe(uint4* z, const uint4* x, const uint4* y, uint64_t n,
+                                                            const VecConst c) {
+    constexpr int PIPE_CWARPS = PS::CWARPS, PIPE_CHUNK = PS::PCHUNK, PIPE_STAGES = PS::PSTAGES;
+    extern __shared__ __align__(128) uint4 ring[];              // [STAGES][2][CHUNK]
+    __shared__ __align__(8) uint64_t full[PIPE_STAGES], empty[PIPE_STAGES];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < PIPE_STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], PIPE_CWARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint64_t nchunks = (n + PIPE_CHUNK - 1) / PIPE_CHUNK;
+    if (warp == PIPE_CWARPS) {                                    // producer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (uint64_t k = blockIdx.x; k < nchunks; k += gridDim.x) {
+                mbar_wait(&empty[s], ph ^ 1);                    // consumers released this stage
+                const uint64_t e0 = k * PIPE_CHUNK;
+                const uint32_t cnt = (uint32_t)(n - e0 < (uint64_t)PIPE_CHUNK ? n - e0 : PIPE_CHUNK);
+                mbar_expect_tx(&full[s], 2 * cnt * 16);
+                bulk_g2s(ring + (2 * s) * PIPE_CHUNK, x + e0, cnt * 16, &full[s]);
+                bulk_g2s(ring + (2 * s + 1) * PIPE_CHUNK, y + e0, cnt * 16, &full[s]);
+                if (++s == PIPE_STAGES) { s = 0; ph ^= 1; }
+            }
+        }
+        return;
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    constexpr int PER = PIPE_CHUNK / (32 * PIPE_CWARPS);        // residues per consumer thread per stage
+    for (uint64_t k = blockIdx.x; k < nchunks; k += gridDim.x) {
+        mbar_wait(&full[s], ph);
+        const uint64_t e0 = k * PIPE_CHUNK;
+        const uint4* xs = ring + (2 * s) * PIPE_CHUNK;
+        const uint4* ys = ring + (2 * s + 1) * PIPE_CHUNK;
+        uint4 xv[PER], yv[PER];
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+            const int i = threadIdx.x + u * 32 * PIPE_CWARPS;
+            xv[u] = xs[i];
+            yv[u] = ys[i];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);                   // the stage may be refilled
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+            const uint64_t i = e0 + threadIdx.x + u * 32 * PIPE_CWARPS;
+            if (i < n) z[i] = u128_to(vec_op1<OPK>(u128_from(xv[u]), u128_from(yv[u]), c));
+        }
+        if (++s == PIPE_STAGES) { s = 0; ph ^= 1; }
+    }
+}
+#ifndef NTT_VEC_PIPE_MASK
+#define NTT_VEC_PIPE_MASK 0   // ops on the pipeline kernel (bit OPK); measured: DESIGN.md §6 "BLAS"
+#endif
+using Pipe0 = PipeShape<8, 512, 6>;
+using Pipe1 = PipeShape<16, 1024, 3>;
+using Pipe2 = PipeShape<16, 512, 6>;
+#ifndef NTT_VEC_PIPE_CFG
+#define NTT_VEC_PIPE_CFG 1
+#endif
+template <int OPK, class PS>
+cudaError_t launch_pipe_s(cudaLaunchConfig_t& pc, uint4* z, const uint4* x, const uint4* y, uint64_t n, const VecConst& c) {
+    static bool attr = false;   // > 48 KB of dynamic shared memory
+    if (!attr) {
+        cudaFuncSetAttribute(k_vec_pipe<OPK, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PS::SMEM);
+        attr = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t nchunks = (n + PS::PCHUNK - 1) / PS::PCHUNK;
+    uint64_t g = (uint64_t)sms * 2;
+    if (g > nchunks) g = nchunks;
+    pc.gridDim = dim3((unsigned)g);
+    pc.blockDim = dim3(PS::THREADS);
+    pc.dynamicSmemBytes = PS::SMEM;
+    return cudaLaunchKernelEx(&pc, k_vec_pipe<OPK, PS>, z, x, y, n, c);
+}
+template <int OPK>
+cudaError_t launch_pipe(cudaLaunchConfig_t& pc, uint4* z, const uint4* x, const uint4* y, uint64_t n, const VecConst& c) {
+#if NTT128_EXPERIMENTS
+    static const int cfg = getenv("NTT128_VEC_PIPE_CFG") ? atoi(getenv("NTT128_VEC_PIPE_CFG")) : NTT_VEC_PIPE_CFG;
+    if (cfg == 0) return launch_pipe_s<OPK, Pipe0>(pc, z, x, y, n, c);
+    if (cfg == 2) return launch_pipe_s<OPK, Pipe2>(pc, z, x, y, n, c);
+    return launch_pipe_s<OPK, Pipe1>(pc, z, x, y, n, c);
+#else
+#if NTT_VEC_PIPE_CFG == 0
+    return launch_pipe_s<OPK, Pipe0>(pc, z, x, y, n, c);
+#elif NTT_VEC_PIPE_CFG == 2
+    return launch_pipe_s<OPK, Pipe2>(pc, z, x, y, n, c);
+#else
+    return launch_pipe_s<OPK, Pipe1>(pc, z, x, y, n, c);
+#endif
+#endif
+}
+
 __global__ void k_vec_check(const uint4* __restrict__ x, const uint4* __restrict__ y, uint64_t n, const VecConst c,
                             int* err) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -169,6 +316,34 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
         cudaFreeAsync(d_err, stream);
         if (cudaStreamSynchronize(stream) != cudaSuccess) return NTT128_ERR_CUDA;
         if (h) return NTT128_ERR_INPUT_RANGE;
+    }
+    // mul and axpy (compute ~70 % of their HBM time) run the bulk-copy pipeline; add / sub
+    // (a handful of ALU ops per element) the one-wave kernel (DESIGN.md §6 "BLAS")
+#if NTT128_EXPERIMENTS
+    static const int pipe_mask = getenv("NTT128_VEC_PIPE") ? atoi(getenv("NTT128_VEC_PIPE")) : NTT_VEC_PIPE_MASK;
+#else
+    constexpr int pipe_mask = NTT_VEC_PIPE_MASK;
+#endif
+    const int opk = (op == OP_MUL && barrett) ? OP_MULB : op;
+    if ((pipe_mask >> opk) & 1) {
+        cudaLaunchConfig_t pc;
+        memset(&pc, 0, sizeof(pc));
+        pc.stream = stream;
+        cudaLaunchAttribute pa[1];
+        pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        pa[0].val.programmaticStreamSerializationAllowed = 1;
+        pc.attrs = pa;
+        pc.numAttrs = 1;
+        cudaError_t e;
+        switch (opk) {
+            case OP_ADD: e = launch_pipe<OP_ADD>(pc, z, x, y, n, c); break;
+            case OP_SUB: e = launch_pipe<OP_SUB>(pc, z, x, y, n, c); break;
+            case OP_MUL: e = launch_pipe<OP_MUL>(pc, z, x, y, n, c); break;
+            case OP_MULB: e = launch_pipe<OP_MULB>(pc, z, x, y, n, c); break;
+            default: e = launch_pipe<OP_AXPY>(pc, z, x, y, n, c); break;
+        }
+        ntt128_count_launch(1);
+        return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NTT128_OK : NTT128_ERR_CUDA;
     }
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
