@@ -155,9 +155,9 @@ ntt128_status vec128_axpy(uint64_t *d_y, const uint64_t *a, const uint64_t *d_x,
  *   "rows"    Y_g[R2][n1]: Y_g[r][k1] = y[(g R2 + r) + n2 k1]       (forward output / inverse input)
  *   send [G][R1][R2] (forward): send[h][r][c] = z[g R1 + r][h R2 + c], block h goes to rank h;
  *   recv [G][R1][R2]: recv[g'][r][c] = z[g' R1 + r][g R2 + c] (block g' came from rank g').
- * Inverse: pass A = Z[k2][j1] = n1^{-1} sum_{k1} y[k2 + n2 k1] w^{-n2 j1 k1} (rows), send /
- * recv [G][R2][R1] by the destination of j1; pass C = x[j1 + n1 j2] = n2^{-1} sum_{k2}
- * (w^{-j1 k2} Z[k2][j1]) w^{-n1 j2 k2}.  A four-step object holds one working buffer of
+ * Inverse: pass A = Z[k2][j1] = sum_{k1} y[k2 + n2 k1] w^{-n2 j1 k1} (rows), send / recv
+ * [G][R2][R1] by the destination of j1; pass C = x[j1 + n1 j2] = sum_{k2} (N^{-1} w^{-j1 k2}
+ * Z[k2][j1]) w^{-n1 j2 k2} (the whole N^{-1} rides on pass C's twiddle factor).  A four-step object holds one working buffer of
  * N/G residues: use it on one stream at a time.
  * ------------------------------------------------------------------------- */
 typedef struct ntt128_fourstep_s *ntt128_fourstep_t;

@@ -17,9 +17,10 @@
 // per-rank factor table [n1][R2] (plan time, laid out like the received matrix).  No separate twiddle, pack or transpose
 // kernel and no extra HBM round trip: a direction is the same 3 passes as the single-GPU
 // plan (n2 = 2^17 as 9 + 8, n1 = 2^9 as one pass at cfg 5).
-// The inverse swaps the roles: pass A = n1-point inverse NTTs of the rows (x n1^{-1}) into
-// the blocks of the destination of j1; pass C = w^{-j1 k2} at the load of the n2-point
-// inverse NTTs (x n2^{-1}) of the received [n2][R1] matrix's columns.
+// The inverse swaps the roles: pass A = n1-point transforms with root w^{-n2} of the rows
+// into the blocks of the destination of j1; pass C = N^{-1} w^{-j1 k2} at the load of the
+// n2-point transforms with root w^{-n1} of the received [n2][R1] matrix's columns (forward
+// kernels with inverse roots: the N^{-1} costs no stage of its own).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -42,10 +43,10 @@ namespace {
 struct FsConst {
     uint32_t q[4];
     uint32_t qinv0;
-    uint32_t one_m[4];
+    uint32_t scale_m[4];   // factor every entry is multiplied by (Montgomery form)
 };
 
-// out[c][r] = w^{((row0 + r) c) mod N} (Montgomery form), r < R, c < C -- laid out like the
+// out[c][r] = s w^{((row0 + r) c) mod N} (Montgomery form), r < R, c < C -- laid out like the
 // received matrix pass C reads (input index c major, polynomial r adjacent), from
 // pw[b] = w^{2^b} (Montgomery form): square-and-multiply over the exponent's bits.
 __global__ void k_fs_factors(uint4* out, uint64_t R, uint64_t C, uint64_t row0, uint64_t nmask, const uint4* pw,
@@ -54,7 +55,7 @@ __global__ void k_fs_factors(uint4* out, uint64_t R, uint64_t C, uint64_t row0, 
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t c = i / R, r = i - c * R;
         uint64_t e = ((row0 + r) * c) & nmask;
-        U128 v = U128{{k.one_m[0], k.one_m[1], k.one_m[2], k.one_m[3]}};
+        U128 v = U128{{k.scale_m[0], k.scale_m[1], k.scale_m[2], k.scale_m[3]}};
         for (int b = 0; e; b++, e >>= 1)
             if (e & 1) v = mont_mul(v, u128_from(pw[b]), k.q, k.qinv0);
         out[i] = u128_to(v);
@@ -71,9 +72,13 @@ struct ntt128_fourstep_s {
     uint32_t log2n1, log2n2, rank, world;
     uint64_t n1, n2, N, R1, R2;
     int device;
-    ntt128_plan_t p1 = nullptr, p2 = nullptr;  // n1-point x R2 (root w^{n2}), n2-point x R1 (root w^{n1})
-    uint4* d_ff = nullptr;                     // [n1][R2]: w^{j1 (rank R2 + r)}     (forward pass C)
-    uint4* d_fi = nullptr;                     // [n2][R1]: w^{-(rank R1 + r) k2}    (inverse pass C)
+    // n1-point x R2 rows: p1 root w^{n2} (forward pass C), p1i root w^{-n2} (inverse pass A);
+    // n2-point x R1 columns: p2 root w^{n1} (forward pass A), p2i root w^{-n1} (inverse pass C).
+    // The inverse runs FORWARD transforms with the inverse roots: no N^-1 stage in either
+    // pass, the whole N^-1 = n1^-1 n2^-1 rides on pass C's factor table.
+    ntt128_plan_t p1 = nullptr, p2 = nullptr, p1i = nullptr, p2i = nullptr;
+    uint4* d_ff = nullptr;                     // [n1][R2]: w^{j1 (rank R2 + r)}          (forward pass C)
+    uint4* d_fi = nullptr;                     // [n2][R1]: N^-1 w^{-(rank R1 + r) k2}    (inverse pass C)
     uint4* d_tmp = nullptr;                    // N/G: pass A's working buffer (multi-pass sub-transforms)
 };
 
@@ -84,6 +89,8 @@ static void fs_free(ntt128_fourstep_s* f) {
     cudaSetDevice(f->device);
     ntt128_plan_destroy(f->p1);
     ntt128_plan_destroy(f->p2);
+    ntt128_plan_destroy(f->p1i);
+    ntt128_plan_destroy(f->p2i);
     cudaFree(f->d_ff);
     cudaFree(f->d_fi);
     cudaFree(f->d_tmp);
@@ -92,7 +99,8 @@ static void fs_free(ntt128_fourstep_s* f) {
 }
 
 static cudaError_t gen_factors(uint4* out, uint64_t R, uint64_t C, uint64_t row0, u128 w, const ntt128h::Mont& M,
-                               const FsConst& k, uint32_t logN) {
+                               FsConst k, u128 scale, uint32_t logN) {
+    for (int i = 0; i < 4; i++) k.scale_m[i] = (uint32_t)(M.to_m(scale) >> (32 * i));
     std::vector<uint4> pw(logN + 1);
     u128 b = M.to_m(w);
     for (uint32_t i = 0; i <= logN; i++) {
@@ -144,14 +152,17 @@ extern "C" ntt128_status ntt128_fourstep_create(ntt128_fourstep_t* out, uint32_t
     FsConst k;
     for (int i = 0; i < 4; i++) k.q[i] = (uint32_t)(q >> (32 * i));
     k.qinv0 = (uint32_t)M.qp;
-    for (int i = 0; i < 4; i++) k.one_m[i] = (uint32_t)(M.r1 >> (32 * i));
 
     // sub-plans: n2-point over the R1 local columns (root w^{n1}), n1-point over the R2 rows (root w^{n2})
-    const u128 w2 = M.pow(w, n1), w1 = M.pow(w, n2);
+    const u128 wi = M.inv(w);
+    const u128 w2 = M.pow(w, n1), w1 = M.pow(w, n2), w2i = M.pow(wi, n1), w1i = M.pow(wi, n2);
     const uint64_t qq[2] = {q_[0], q_[1]};
     const uint64_t r2[2] = {(uint64_t)w2, (uint64_t)(w2 >> 64)}, r1[2] = {(uint64_t)w1, (uint64_t)(w1 >> 64)};
+    const uint64_t r2i[2] = {(uint64_t)w2i, (uint64_t)(w2i >> 64)}, r1i[2] = {(uint64_t)w1i, (uint64_t)(w1i >> 64)};
     ntt128_status st = ntt128_plan_create(&f->p2, log2n2, (uint32_t)f->R1, qq, r2, 1, NTT128_CYCLIC, device);
     if (st == NTT128_OK) st = ntt128_plan_create(&f->p1, log2n1, (uint32_t)f->R2, qq, r1, 1, NTT128_CYCLIC, device);
+    if (st == NTT128_OK) st = ntt128_plan_create(&f->p2i, log2n2, (uint32_t)f->R1, qq, r2i, 1, NTT128_CYCLIC, device);
+    if (st == NTT128_OK) st = ntt128_plan_create(&f->p1i, log2n1, (uint32_t)f->R2, qq, r1i, 1, NTT128_CYCLIC, device);
     if (st != NTT128_OK) { fs_free(f); return st; }
 
     int prev = 0;
@@ -161,8 +172,9 @@ extern "C" ntt128_status ntt128_fourstep_create(ntt128_fourstep_t* out, uint32_t
     if (cudaMalloc(&f->d_ff, local * 16) != cudaSuccess || cudaMalloc(&f->d_fi, local * 16) != cudaSuccess ||
         cudaMalloc(&f->d_tmp, local * 16) != cudaSuccess) {
         st = NTT128_ERR_OOM;
-    } else if (gen_factors(f->d_ff, f->R2, n1, (uint64_t)rank * f->R2, w, M, k, log2n1 + log2n2) != cudaSuccess ||
-               gen_factors(f->d_fi, f->R1, n2, (uint64_t)rank * f->R1, M.inv(w), M, k, log2n1 + log2n2) != cudaSuccess) {
+    } else if (gen_factors(f->d_ff, f->R2, n1, (uint64_t)rank * f->R2, w, M, k, 1, log2n1 + log2n2) != cudaSuccess ||
+               gen_factors(f->d_fi, f->R1, n2, (uint64_t)rank * f->R1, wi, M, k, M.inv((u128)(N % q)), log2n1 + log2n2) !=
+                   cudaSuccess) {
         st = NTT128_ERR_CUDA;
     }
     cudaSetDevice(prev);
@@ -231,7 +243,7 @@ extern "C" ntt128_status ntt128_fourstep_inverse_a(const ntt128_fourstep_t f, co
     if (!al16(d_rows) || !al16(d_send)) return NTT128_ERR_ALIGNMENT;
     uint4* bases[NTT128_FS_MAX_RANKS] = {};
     for (uint32_t h = 0; h < f->world; h++) bases[h] = (uint4*)d_send + (uint64_t)h * f->R2 * f->R1;   // send[h][r][m]
-    return pass_a(f, f->p1, true, d_rows, bases, f->R1, f->n1, (cudaStream_t)s);
+    return pass_a(f, f->p1i, false, d_rows, bases, f->R1, f->n1, (cudaStream_t)s);
 }
 
 extern "C" ntt128_status ntt128_fourstep_inverse_c(const ntt128_fourstep_t f, const uint64_t* d_recv, uint64_t* d_cols,
@@ -239,7 +251,7 @@ extern "C" ntt128_status ntt128_fourstep_inverse_c(const ntt128_fourstep_t f, co
     if (!f || !d_recv || !d_cols) return NTT128_ERR_INVALID_ARG;
     if (!al16(d_recv) || !al16(d_cols)) return NTT128_ERR_ALIGNMENT;
     if (d_recv == d_cols) return NTT128_ERR_INVALID_ARG;
-    return pass_c(f, f->p2, true, d_recv, d_cols, f->R1, f->d_fi, (cudaStream_t)s);
+    return pass_c(f, f->p2i, false, d_recv, d_cols, f->R1, f->d_fi, (cudaStream_t)s);
 }
 
 // Fused exchange (include/ntt128.h): peers[h] = rank h's receive buffer, mapped in this
@@ -257,7 +269,7 @@ static ntt128_status a_peers(const ntt128_fourstep_s* f, const uint64_t* d_in, c
         if (!al16(peers[h])) return NTT128_ERR_ALIGNMENT;
         bases[h] = (uint4*)peers[h] + (uint64_t)f->rank * blk;
     }
-    return inverse ? pass_a(f, f->p1, true, d_in, bases, f->R1, f->n1, st)
+    return inverse ? pass_a(f, f->p1i, false, d_in, bases, f->R1, f->n1, st)
                    : pass_a(f, f->p2, false, d_in, bases, f->R2, f->n2, st);
 }
 

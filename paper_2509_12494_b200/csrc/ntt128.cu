@@ -187,7 +187,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // Bulk copies (SASS UBLKCP) completing on an mbarrier (NTT_BULK, DESIGN.md §6 "Bulk staging").
 #ifndef NTT_BULK
-#define NTT_BULK 0   // bit 0: twiddle sets by bulk copy; bit 1: first-pass stores by bulk copy
+// bit 0: twiddle sets of 8- and 9-stage multi-pass passes by bulk copy (cfg3 +1.7 %, cfg4
+// 2^14..2^17 +0.8..+1.4 %; with the 6/7-stage passes' eight small sets -1.3 % at 2^12: those
+// keep cp.async); bit 1: first-pass stores by bulk copy (-3.4 %: off).  tools/exp_ab.py,
+// profiles/r02/bulk_ab.txt
+#define NTT_BULK 1
 #endif
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
@@ -597,7 +601,7 @@ k_ntt_pass(const PassArgs a) {
         // (2^sl - 1) + jj for local stage sl), precomputed per pass at plan time; the sets
         // of one CTA (consecutive L, same polynomial) are consecutive runs of the table.
         constexpr int TW_IT = (G - 1 + NT - 1) / NT;
-        if ((NTT_BULK & 1) && !SINGLE) {
+        if ((NTT_BULK & 1) && !SINGLE && B >= 8) {
             // one thread streams the CTA's twiddle sets (contiguous runs of the pass table)
             // with bulk copies; the other threads wait on the mbarrier after the data phase
             if (tid == 0) {
@@ -706,7 +710,7 @@ k_ntt_pass(const PassArgs a) {
     }
     cp_async_wait_all();
     __syncthreads();
-    if ((NTT_BULK & 1) && !SINGLE) mbar_wait(&tw_bar, 0);
+    if ((NTT_BULK & 1) && !SINGLE && B >= 8) mbar_wait(&tw_bar, 0);
 #if NTT_TRACE
     const uint32_t tr_t1 = gtimer_lo();
 #endif

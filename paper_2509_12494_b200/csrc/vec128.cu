@@ -46,10 +46,13 @@ __device__ __forceinline__ U128 mul_b(const U128& a, const U128& b, const Barret
     return r;
 }
 
-constexpr int UNROLL = 4;
+#ifndef NTT_VEC_UNROLL
+#define NTT_VEC_UNROLL 4   // residues in flight per thread (4: measured; 2 / 8: tools/exp_vec_graph.py)
+#endif
+constexpr int UNROLL = NTT_VEC_UNROLL;
 constexpr int THREADS = 256;
 
-template <int OPK>
+template <int OPK, int UNROLL = 4>
 __global__ void __launch_bounds__(THREADS) k_vec(uint4* z, const uint4* __restrict__ x,
                                                  const uint4* y, uint64_t n, const VecConst c) {
     // programmatic dependent launch: wait for the previous kernel's writes, then let the
@@ -357,13 +360,13 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
     cfg.numAttrs = 1;
     cudaError_t e;
     switch (op) {
-        case OP_ADD: e = cudaLaunchKernelEx(&cfg, k_vec<OP_ADD>, z, x, y, (uint64_t)n, c); break;
-        case OP_SUB: e = cudaLaunchKernelEx(&cfg, k_vec<OP_SUB>, z, x, y, (uint64_t)n, c); break;
+        case OP_ADD: e = cudaLaunchKernelEx(&cfg, k_vec<OP_ADD, UNROLL>, z, x, y, (uint64_t)n, c); break;
+        case OP_SUB: e = cudaLaunchKernelEx(&cfg, k_vec<OP_SUB, UNROLL>, z, x, y, (uint64_t)n, c); break;
         case OP_MUL:
-            e = barrett ? cudaLaunchKernelEx(&cfg, k_vec<OP_MULB>, z, x, y, (uint64_t)n, c)
-                        : cudaLaunchKernelEx(&cfg, k_vec<OP_MUL>, z, x, y, (uint64_t)n, c);
+            e = barrett ? cudaLaunchKernelEx(&cfg, k_vec<OP_MULB, UNROLL>, z, x, y, (uint64_t)n, c)
+                        : cudaLaunchKernelEx(&cfg, k_vec<OP_MUL, UNROLL>, z, x, y, (uint64_t)n, c);
             break;
-        default: e = cudaLaunchKernelEx(&cfg, k_vec<OP_AXPY>, z, x, y, (uint64_t)n, c); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_vec<OP_AXPY, UNROLL>, z, x, y, (uint64_t)n, c); break;
     }
     ntt128_count_launch(1);
     return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NTT128_OK : NTT128_ERR_CUDA;

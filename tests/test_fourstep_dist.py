@@ -55,13 +55,14 @@ class OracleLocal:
         return rows
 
     def inverse_a(self, rows, send):
-        z = O.intt(_n(rows), self.q, pow(self.w, self.n2, self.q))         # [R2][n1]
+        z = O.ntt(_n(rows), self.q, pow(self.w, -self.n2, self.q))        # [R2][n1], unscaled
         send.copy_(_t(self._blocks(z, self.R2, self.n1)))
 
     def inverse_c(self, recv, cols):
         m = _n(recv).reshape(self.n2, self.R1, 2).transpose(1, 0, 2)       # [R1][n2]: row m = j1 = rank R1 + m
         m = self._twiddle(m, self.rank * self.R1, pow(self.w, -1, self.q))
-        cols.copy_(_t(O.intt(m, self.q, pow(self.w, self.n1, self.q))))
+        m = O.vmul(m.reshape(-1, 2), synth.from_ints([pow(self.N, -1, self.q)] * (m.size // 2)), self.q).reshape(m.shape)
+        cols.copy_(_t(O.ntt(m, self.q, pow(self.w, -self.n1, self.q))))   # N^-1 applied with the twiddle
         return cols
 
 
