@@ -265,7 +265,9 @@ def run_gpu(args):
     n = 1 << logn
     NSETS = 4
     qs, ws, psis, sets = cfg3_inputs(P, rank, NSETS)
-    plan = N.Plan(logn, qs, ws, batch=B)
+    # NTT128_FLAG_CHAIN: consecutive transforms on the stream overlap polynomial by polynomial
+    # (include/ntt128.h; DESIGN.md §6 "Chained calls") -- same work, same results
+    plan = N.Plan(logn, qs, ws, batch=B, chain=True)
     X = [to_dev(x) for x in sets]
     Y = [torch.empty_like(x) for x in X]
     Z = [torch.empty_like(x) for x in X]
@@ -356,7 +358,9 @@ def run_gpu(args):
                                    "124-128-bit primes (BASELINE.json configs[2])",
                        "N": n, "batch_per_gpu": B, "parallelism": f"batch-shard x{world} (no collective)",
                        "l2": "inputs rotate over 4 disjoint buffer sets (768 MiB footprint > 126 MB L2)",
-                       "passes": npasses},
+                       "passes": npasses,
+                       "chain": "NTT128_FLAG_CHAIN: each transform's first pass starts on a polynomial once the "
+                                "previous call finished it (per-polynomial counters) instead of after the whole grid"},
             "ntt_per_s": value / bfly_per_transform,
             "ns_per_butterfly": 1e9 / value,
             "fwd_ms": fwd_ms, "inv_ms": inv_ms,
@@ -492,7 +496,7 @@ def run_rows(args, P, pk, stream, rank, world):
     mods = P["cfg3"]["moduli"]
     qs, psis = [hexint(m["q"]) for m in mods], [hexint(m["psi"]) for m in mods]
     n3 = 1 << 16
-    pn = N.Plan(16, qs, psis, batch=64, negacyclic=True)
+    pn = N.Plan(16, qs, psis, batch=64, negacyclic=True, chain=True)
     a = to_dev(np.stack([synth.uniform_residues(qs[i], n3, synth.stream_seed(3, 0, i)) for i in range(64)]))
     b = to_dev(np.stack([synth.uniform_residues(qs[i], n3, synth.stream_seed(3, 1, i)) for i in range(64)]))
     c = torch.empty_like(a)

@@ -63,6 +63,18 @@ typedef enum {
 #define NTT128_CYCLIC 0u            /* root = omega of exact order N; y_k = sum_j x_j omega^{jk} (Eq. ntt) */
 #define NTT128_NEGACYCLIC 1u        /* root = psi of exact order 2N; y_k = sum_j x_j psi^{j(2k+1)}, the evaluation at psi^{2k+1} */
 #define NTT128_FLAG_CHECK_INPUT 0x100u /* validate inputs < q on every call (synchronises the stream) */
+/* Chained calls (DESIGN.md §6 "Chained calls"): consecutive transforms of this plan on one
+ * stream overlap polynomial by polynomial -- the first pass of a call starts on polynomial p
+ * once the previous call's last pass has finished p, instead of waiting for the previous
+ * call's whole grid (the passes inside one call already overlap this way).  The library
+ * applies it only when the previous library call on the stream was this plan's own transform
+ * (forward, inverse, polymul, bitrev) and each buffer of the new call is either one of the
+ * previous call's buffers (same base pointer) or disjoint from all of them; otherwise the
+ * call waits for the whole previous grid.  Contract: between two such calls the caller
+ * enqueues on that stream no kernel launched with programmatic stream serialization (PDL)
+ * that touches their buffers, other than this library's own calls (plain kernels, copies
+ * and memsets are ordered as usual).  Results are identical with or without the flag. */
+#define NTT128_FLAG_CHAIN 0x200u
 
 /* opaque; its tables are immutable after create; safe to share across streams and threads
  * (per-stream pass-overlap counters and scratch are cached inside, at most 8 streams: a
@@ -78,6 +90,7 @@ typedef struct ntt128_plan_s *ntt128_plan_t;
  *   n_moduli:  1 (all polynomials share q) or batch (polynomial b uses modulus b, the
  *              RNS case of BASELINE cfg 3)
  *   flags:     NTT128_CYCLIC or NTT128_NEGACYCLIC, optionally | NTT128_FLAG_CHECK_INPUT
+ *              and / or | NTT128_FLAG_CHAIN
  *   device:    CUDA device ordinal that owns the plan tables
  * Validates primality (Miller-Rabin), divisibility and the root's exact order, then
  * builds per-modulus Montgomery constants and twiddle tables on the device

@@ -21,6 +21,8 @@
 //  * Stage 0 has twiddle 1 for every butterfly and skips the multiply.
 //  * Negacyclic: twist x_j psi^j fused into the first pass's load, untwist
 //    N^{-1} psi^{-j} fused into the last pass's store (reading c9).
+#include <cuda.h>            // CUtensorMap (types only: the encoder comes from the driver entry point)
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -124,6 +126,7 @@ using ntt128h::u128;
 
 // ----------------------------------------------------------------------------- common
 static std::atomic<uint64_t> g_launches{0};
+static std::atomic<int> g_chain_plans{0};   // live plans with NTT128_FLAG_CHAIN (chained calls, below)
 extern "C" uint64_t ntt128_launch_count(void) { return g_launches.load(); }
 void ntt128_count_launch(uint64_t k) { g_launches += k; }
 
@@ -214,6 +217,14 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
                  : "memory");
 }
+// Tensor (TMA) tile loads, SASS UTMALDG: one instruction moves a whole pass tile (DESIGN.md
+// §6 "TMA staging"); the box lands in shared memory in box order, completing on `bar`.
+__device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3, int c4,
+                                          uint64_t* bar) {
+    asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                 ::"r"(smem_u32(dst)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)) : "memory");
+}
 
 
 // ----------------------------------------------------------------------------- twiddle generation
@@ -295,6 +306,9 @@ __global__ void k_gather_nc_tw(uint4* out, uint64_t out_stride, const uint4* psi
 
 // ----------------------------------------------------------------------------- pass kernel
 struct PassArgs {
+    // TMA kernels (k_ntt_pass<..., TMA>): the data tile's tensor map over src, encoded per
+    // launch by the host (tma_map_*); unused otherwise.  First member: 64-byte aligned.
+    CUtensorMap tm;
     const uint4* src;      // [batch][N]
     uint4* dst;            // [batch][N]
     const uint4* pmul;     // optional point-wise multiplicand, same layout as src (Montgomery product)
@@ -543,20 +557,34 @@ struct PassOcc {
     static constexpr int RB = PassShape<B, RBMAX>::RB;
     static constexpr int THREADS = (RB == 2 && !SINGLE) ? NTT_OCC_THREADS_RB2 : NTT_OCC_THREADS;
 };
-template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX, bool PM = false>
+// TMA (later passes of 7-, 8- and 9-stage multi-pass plans, one group per CTA, DESIGN.md §6
+// "TMA staging"): thread 0 moves the CTA's whole data tile with ONE tensor load (UTMALDG)
+// and its twiddle set with one bulk copy (UBLKCP), both completing on mbarriers in shared
+// memory; no thread issues a per-element copy.  The box {2 u64, 9 rows j from -1, 2^B/8
+// chunks m} over the [poly][H][m][j][L] view (r = 8 m + j) lands as exactly the padded
+// layout, slot 1 + l + l/8, the j = -1 rows being out of bounds (zero-filled, never read).
+// First passes keep per-thread cp.async: their rows are the bit-reversed gather, which no
+// affine box maps onto the padded layout.
+template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE, int RBMAX, bool PM = false, bool TMA = false>
 __global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T,
                                   (PassOcc<B, RBMAX, SINGLE>::THREADS / (C * PassShape<B, RBMAX>::T)) > 0
                                       ? PassOcc<B, RBMAX, SINGLE>::THREADS / (C * PassShape<B, RBMAX>::T) : 1)
-k_ntt_pass(const PassArgs a) {
+k_ntt_pass(const __grid_constant__ PassArgs a) {
     static_assert(!PM || (FIRST && !SINGLE), "polynomial-major groups: multi-pass first passes only");
+    static_assert(!TMA || (C == 1 && !SINGLE && !PM && !FIRST && B >= 7 && B <= 9), "TMA: later passes, one group per CTA");
     constexpr bool PADL = !SINGLE;
     using S = PassShape<B, RBMAX, C, PADL>;
     constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS, TS = S::TS;
     constexpr int NT = C * T;
     constexpr int NTW = (FIRST && !SINGLE) ? 1 : C;  // twiddle sets: a multi-pass first pass shares one (L = 0)
-    extern __shared__ uint4 sm[];
-    uint4* tsm = sm + C * GS;                        // [NTW][TS] pass-local twiddles
-    __shared__ __align__(8) uint64_t tw_bar;         // NTT_BULK: twiddle bulk copies
+    constexpr int DOFF = TMA ? 1 : 0;                // TMA: slot 0 takes the box's first pad row
+    extern __shared__ __align__(128) uint4 sm[];     // tensor-copy destinations: 128-byte aligned
+    uint4* const dsm = sm + DOFF;                    // [C][GS] data tiles
+    uint4* tsm = dsm + C * GS;                       // [NTW][TS] pass-local twiddles
+    __shared__ __align__(8) uint64_t tw_bar_s;       // NTT_BULK: twiddle bulk copies (non-TMA kernels)
+    // TMA kernels keep their barriers in dynamic shared memory: [0] twiddles, [1] data tile
+    uint64_t* const bars = reinterpret_cast<uint64_t*>(tsm + NTW * TS);
+    uint64_t* const twb = TMA ? bars : &tw_bar_s;
 
     const uint32_t n = a.n, lo = a.lo, gbits = n - B;
     const uint64_t N = 1ull << n;
@@ -601,17 +629,18 @@ k_ntt_pass(const PassArgs a) {
         // (2^sl - 1) + jj for local stage sl), precomputed per pass at plan time; the sets
         // of one CTA (consecutive L, same polynomial) are consecutive runs of the table.
         constexpr int TW_IT = (G - 1 + NT - 1) / NT;
-        if ((NTT_BULK & 1) && !SINGLE && B >= 8) {
+        if (TMA || ((NTT_BULK & 1) && !SINGLE && B >= 8)) {
             // one thread streams the CTA's twiddle sets (contiguous runs of the pass table)
             // with bulk copies; the other threads wait on the mbarrier after the data phase
             if (tid == 0) {
                 const uint64_t L0 = FIRST ? 0 : ((gg0 & gmask) & ((1ull << lo) - 1));
                 const uint32_t m0 = a.nq == 1 ? 0 : (uint32_t)((gg0 < a.total_groups ? gg0 : a.total_groups - 1) >> gbits);
                 const uint4* src = a.pt + m0 * a.pt_stride + L0 * (G - 1);
-                mbar_init(&tw_bar, 1);
-                mbar_expect_tx(&tw_bar, NTW * (G - 1) * 16);
+                mbar_init(twb, 1);
+                if (TMA) mbar_init(bars + 1, 1);
+                mbar_expect_tx(twb, NTW * (G - 1) * 16);
 #pragma unroll
-                for (int c = 0; c < NTW; c++) bulk_g2s(tsm + c * TS, src + c * (G - 1), (G - 1) * 16, &tw_bar);
+                for (int c = 0; c < NTW; c++) bulk_g2s(tsm + c * TS, src + c * (G - 1), (G - 1) * 16, twb);
             }
         } else if (NTW == 1 || !(FIRST && SINGLE)) {
             const uint64_t L0 = FIRST ? 0 : ((gg0 & gmask) & ((1ull << lo) - 1));
@@ -647,8 +676,18 @@ k_ntt_pass(const PassArgs a) {
                 const uint32_t* cp = a.cnt_in + (gg0 >> gbits);
                 while ((int32_t)(ld_acquire_gpu(cp) - a.target) < 0) __nanosleep(128);
             }
-            __syncthreads();
+            if (!TMA) __syncthreads();
         }
+        if (TMA && tid == 0) {
+            // the producers' generic-proxy stores (acquired above) before our async-proxy reads
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            // group (H, L): rows r = 8 m + j at stride 2^lo, box j from -1 (pad)
+            const uint64_t poly = gg0 >> gbits, g = gg0 & gmask;
+            const uint64_t H = g >> lo, L = g & ((1ull << lo) - 1);
+            mbar_expect_tx(bars + 1, 9 * (G / 8) * 16);
+            tma_load5(sm, &a.tm, (int)(2 * L), -1, 0, (int)H, (int)poly, bars + 1);
+        }
+        if (TMA) __syncthreads();   // mbarrier initialisation visible before anyone waits
         // our predecessors are complete (or their output for this polynomial is): the next
         // pass may be scheduled onto SMs as this grid drains
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -670,8 +709,10 @@ k_ntt_pass(const PassArgs a) {
     }
     const uint4* srcp = a.src + poly_me * a.in_ps + gbase * a.in_es;
     const uint64_t sstride = (uint64_t)gstride * a.in_es;   // source step per i
-    uint4* smc = sm + c_me * GS;
-    if (!a.fin && !a.pmul) {
+    uint4* smc = dsm + c_me * GS;
+    if (TMA) {
+        // the tile is in flight (thread 0's tensor load)
+    } else if (!a.fin && !a.pmul) {
         if (live) {
 #if NTT_LDG_DATA
             // registers, then conflict-free STS: cp.async into the padded layout (lanes not
@@ -692,7 +733,7 @@ k_ntt_pass(const PassArgs a) {
             }
 #endif
         }
-    } else if (live) {
+    } else if (FIRST && live) {   // load-side factors (twist, four-step, point-wise): first passes only
         uint4 stage[PER];
 #pragma unroll
         for (int i = 0; i < PER; i++) stage[i] = srcp[(size_t)i * sstride];
@@ -708,9 +749,14 @@ k_ntt_pass(const PassArgs a) {
             smc[slot<B, PADL, RB>(l)] = u128_to(x);
         }
     }
-    cp_async_wait_all();
-    __syncthreads();
-    if ((NTT_BULK & 1) && !SINGLE && B >= 8) mbar_wait(&tw_bar, 0);
+    if (TMA) {
+        mbar_wait(bars + 1, 0);   // data tile
+        mbar_wait(bars, 0);       // twiddle set
+    } else {
+        cp_async_wait_all();
+        __syncthreads();
+        if ((NTT_BULK & 1) && !SINGLE && B >= 8) mbar_wait(twb, 0);
+    }
 #if NTT_TRACE
     const uint32_t tr_t1 = gtimer_lo();
 #endif
@@ -736,7 +782,7 @@ k_ntt_pass(const PassArgs a) {
                 nf = U128{{src[0], src[1], src[2], src[3]}};
             }
         }
-        uint4* gsm = sm + c * GS;
+        uint4* gsm = dsm + c * GS;
         const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
         const int mode = SINGLE ? MODE_FULL : mode_of(q);   // uniform per CTA: its groups share the polynomial
@@ -769,7 +815,7 @@ k_ntt_pass(const PassArgs a) {
                 if (gg >= a.total_groups) continue;
                 const uint64_t poly = gg >> gbits, g = gg & gmask;
                 uint4* dstp = a.dst + poly * N + ((uint64_t)brev_bits((uint32_t)g, gbits) << B) + 8 * k;
-                bulk_s2g(dstp, sm + c * GS + 9 * k, 128);
+                bulk_s2g(dstp, dsm + c * GS + 9 * k, 128);
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");     // written (the next pass may read)
@@ -779,7 +825,7 @@ k_ntt_pass(const PassArgs a) {
 #pragma unroll
             for (int i = 0; i < PER; i++) {
                 const int e = tid + i * NT;
-                outv[i] = sm[(e / G) * GS + slot<B, PADL, RB>(e % G)];
+                outv[i] = dsm[(e / G) * GS + slot<B, PADL, RB>(e % G)];
             }
 #pragma unroll
             for (int i = 0; i < PER; i++) {
@@ -1221,18 +1267,22 @@ struct PassCfg {
     PassKernel fn;
     int B, C, threads;
     size_t smem;
+    bool tma = false;     // k_ntt_pass<..., TMA>: the launch must carry the data tile's tensor map
+    bool first = false;
 };
 
-template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE = false, int RBMAX = 3, bool PM = false>
+template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE = false, int RBMAX = 3, bool PM = false, bool TMA = false>
 static PassCfg make_cfg() {
     using S = PassShape<B, RBMAX, C, !SINGLE>;
     PassCfg c;
-    c.fn = k_ntt_pass<B, C, FIRST, SCALE_LAST, SINGLE, RBMAX, PM>;
+    c.fn = k_ntt_pass<B, C, FIRST, SCALE_LAST, SINGLE, RBMAX, PM, TMA>;
     c.B = B;
     c.C = C;
     c.threads = C * S::T;
+    c.tma = TMA;
+    c.first = FIRST;
     const size_t ntw = (size_t)((FIRST && !SINGLE) ? 1 : C) * S::TS;
-    c.smem = ((size_t)C * S::GS + ntw) * sizeof(uint4);
+    c.smem = ((size_t)C * S::GS + ntw + (TMA ? 2 : 0)) * sizeof(uint4);   // TMA: + the pad slot, + two mbarriers
     return c;
 }
 
@@ -1280,14 +1330,32 @@ static bool use_latency_shape(int B, uint32_t batch) {
 // `wide`: rows of the pass are >= 2^NTT_WIDE_STRIDE elements apart; a one-group CTA then
 // reads 16-byte pieces of rows megabytes apart, so 8- and 9-stage passes take 4 adjacent
 // groups per CTA (64-byte row segments; N = 2^26: 12.1 -> 10.3 ms, tools/exp_large.py).
+// `tma`: the pass may take the TMA kernel (natural-layout input, no load-side factor);
+// one-group CTAs (7-, 8-, 9-stage passes, not wide) then load their tile by tensor copy.
+#ifndef NTT_TMA
+#define NTT_TMA 1
+#endif
+template <int B, bool FIRST, bool SL, int RB>
+static PassCfg tma_cfg() {
+    if constexpr (FIRST) return make_cfg<B, 1, FIRST, SL, false, RB>();
+    else return make_cfg<B, 1, FIRST, SL, false, RB, false, true>();
+}
 template <bool FIRST, bool SL>
-static PassCfg multi_cfg_t(int B, bool wide) {
+static PassCfg multi_cfg_t(int B, bool wide, bool tma) {
+    tma = tma && NTT_TMA && !FIRST;
     switch (B) {
         case 5: return make_cfg<5, NTT_C5, FIRST, SL>();
         case 6: return make_cfg<6, NTT_C6, FIRST, SL, false, NTT_RB6>();
-        case 7: return make_cfg<7, NTT_C7, FIRST, SL, false, NTT_RB7>();
-        case 8: return wide ? make_cfg<8, 4, FIRST, SL, false, NTT_RB8>() : make_cfg<8, NTT_C8, FIRST, SL, false, NTT_RB8>();
-        default: return wide ? make_cfg<9, 4, FIRST, SL, false, NTT_RB9>() : make_cfg<9, NTT_C9, FIRST, SL, false, NTT_RB9>();
+        case 7: return (tma && NTT_C7 == 1) ? tma_cfg<7, FIRST, SL, NTT_RB7>()
+                                            : make_cfg<7, NTT_C7, FIRST, SL, false, NTT_RB7>();
+        case 8:
+            if (wide) return make_cfg<8, 4, FIRST, SL, false, NTT_RB8>();
+            return (tma && NTT_C8 == 1) ? tma_cfg<8, FIRST, SL, NTT_RB8>()
+                                        : make_cfg<8, NTT_C8, FIRST, SL, false, NTT_RB8>();
+        default:
+            if (wide) return make_cfg<9, 4, FIRST, SL, false, NTT_RB9>();
+            return (tma && NTT_C9 == 1) ? tma_cfg<9, FIRST, SL, NTT_RB9>()
+                                        : make_cfg<9, NTT_C9, FIRST, SL, false, NTT_RB9>();
     }
 }
 // Permutation-free negacyclic passes (B in [5, 8], warp-owned groups).
@@ -1347,12 +1415,52 @@ static PassCfg strided_pm_cfg() { return make_cfg<9, NTT_FS_C, true, false, fals
 #define NTT_WIDE_STRIDE 17
 #endif
 // lo = index bits below the pass (0 for the first pass); n = log2 N
-static PassCfg pass_cfg(size_t npass, size_t i, int B, bool scale_last, int lo = 0, int n = 0) {
+static PassCfg pass_cfg(size_t npass, size_t i, int B, bool scale_last, int lo = 0, int n = 0, bool tma = true) {
     if (npass == 1) return scale_last ? single_cfg_t<true>(B) : single_cfg_t<false>(B);
     const bool wide = (i == 0 ? n - B : lo) >= NTT_WIDE_STRIDE;   // row stride of the pass, log2 elements
-    if (i == 0) return multi_cfg_t<true, false>(B, wide);
-    if (i + 1 == npass && scale_last) return multi_cfg_t<false, true>(B, wide);
-    return multi_cfg_t<false, false>(B, wide);
+    if (i == 0) return multi_cfg_t<true, false>(B, wide, tma);
+    if (i + 1 == npass && scale_last) return multi_cfg_t<false, true>(B, wide, tma);
+    return multi_cfg_t<false, false>(B, wide, tma);
+}
+
+// Tensor map of a TMA pass's data tiles over a.src ([batch][N] residues, natural layout),
+// encoded per launch (the map holds the buffer's address) through the driver's
+// cuTensorMapEncodeTiled, reached via the runtime's entry-point query (no libcuda link).
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return (PFN_cuTensorMapEncodeTiled_v12000)f;
+    }();
+    return fn;
+}
+static bool tma_encode(PassArgs& a, bool first, int n, int B, int lo, uint32_t batch) {
+    const PFN_cuTensorMapEncodeTiled_v12000 enc = tma_encoder();
+    if (!enc) return false;
+    const cuuint64_t N = 1ull << n;
+    void* base = const_cast<uint4*>(a.src);
+    CUresult r;
+    if (first) {
+        // [poly][r (2^B rows, as r_lo < 256 and r_hi)][g][2 u64]: box = column g, 128B swizzle
+        const int gb = n - B;
+        const cuuint32_t rl = B > 8 ? 256u : (1u << B), rh = (1u << B) / rl;
+        const cuuint64_t dims[4] = {2ull << gb, rl, rh, batch};
+        const cuuint64_t strides[3] = {16ull << gb, (16ull << gb) * rl, 16 * N};
+        const cuuint32_t box[4] = {2, rl, rh, 1}, es[4] = {1, 1, 1, 1};
+        r = enc(&a.tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        // [poly][H][m][j][L][2 u64], r = 8 m + j: box {2, 9 (j from -1), 2^B / 8, 1, 1}
+        const cuuint64_t dims[5] = {2ull << lo, 8, 1ull << (B - 3), 1ull << (n - lo - B), batch};
+        const cuuint64_t strides[4] = {16ull << lo, 16ull << (lo + 3), 16ull << (lo + B), 16 * N};
+        const cuuint32_t box[5] = {2, 9, 1u << (B - 3), 1, 1}, es[5] = {1, 1, 1, 1, 1};
+        r = enc(&a.tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    return r == CUDA_SUCCESS;
 }
 
 // ----------------------------------------------------------------------------- plan
@@ -1383,14 +1491,20 @@ struct ntt128_plan_s {
     // every pass enqueued so far on the stream has signalled (a pass adds its CTAs per
     // polynomial), so in-stream order makes the targets exact without a reset, for any mix
     // of pass structures, and different streams never share a set.
-    static constexpr int MAX_ROWS = 3;                 // passes - 1 of the deepest schedule (4 passes)
+    static constexpr int MAX_ROWS = 4;                 // passes of the deepest schedule (the last row: chained calls)
     // At most MAX_STREAMS entries are cached: a further stream evicts the least recently used
     // entry once the event recorded after that entry's last use has completed (entries used
     // under stream capture are pinned: a captured graph keeps referring to them).
     static constexpr int MAX_STREAMS = 8;
     struct StreamCtr {
         uint32_t* d = nullptr;                          // [MAX_ROWS][batch]
-        uint32_t expected[MAX_ROWS] = {0, 0, 0};
+        uint32_t expected[MAX_ROWS] = {0, 0, 0, 0};
+        // NTT128_FLAG_CHAIN: the last counter-signalling call of this plan on the stream --
+        // its last pass's row and target, its buffers, and its library generation
+        int last_row = -1;
+        uint32_t last_target = 0;
+        const void* last_bufs[3] = {nullptr, nullptr, nullptr};
+        uint64_t gen = 0;
         uint4* scratch = nullptr;                       // polymul spectra [2][batch][N] / in-place copy [batch][N]
         size_t scratch_elems = 0;
         cudaEvent_t ev = nullptr;                       // recorded after the last enqueue that used the entry
@@ -1404,6 +1518,7 @@ struct ntt128_plan_s {
 
 static void plan_free(ntt128_plan_s* p) {
     if (!p) return;
+    if (p->flags & NTT128_FLAG_CHAIN) g_chain_plans--;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(p->device);
@@ -1524,7 +1639,7 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
     *out = nullptr;
     if (log2n < 1 || log2n > 26 || batch == 0) return NTT128_ERR_INVALID_ARG;
     if (n_moduli != 1 && n_moduli != batch) return NTT128_ERR_INVALID_ARG;
-    if (flags & ~(NTT128_NEGACYCLIC | NTT128_FLAG_CHECK_INPUT)) return NTT128_ERR_INVALID_ARG;
+    if (flags & ~(NTT128_NEGACYCLIC | NTT128_FLAG_CHECK_INPUT | NTT128_FLAG_CHAIN)) return NTT128_ERR_INVALID_ARG;
     const uint32_t kind = flags & NTT128_NEGACYCLIC;
     const uint64_t N = 1ull << log2n;
 
@@ -1557,6 +1672,7 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
     p->batch = batch;
     p->nq = n_moduli;
     p->flags = flags;
+    if (flags & NTT128_FLAG_CHAIN) g_chain_plans++;   // plan_free undoes it
     p->kind = kind;
     p->device = device;
     p->N = N;
@@ -1624,9 +1740,12 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
             for (int sl = 0; sl < 2; sl++) {
                 int lo_i = 0;
                 for (size_t k = 0; k < i; k++) lo_i += p->bits[k];
-                PassCfg c = pass_cfg(p->bits.size(), i, p->bits[i], sl == 1, lo_i, (int)log2n);
-                if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
-                    st = NTT128_ERR_CUDA;
+                for (int tma = 0; tma < 2; tma++) {   // the TMA kernel and its cp.async fallback
+                    const PassCfg ct = pass_cfg(p->bits.size(), i, p->bits[i], sl == 1, lo_i, (int)log2n, tma == 1);
+                    if (cudaFuncSetAttribute(ct.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess)
+                        st = NTT128_ERR_CUDA;
+                }
+                PassCfg c;
                 if (p->bits.size() == 1 && use_latency_shape(p->bits[i], batch)) {
                     c = sl ? single_lat_cfg_t<true>(p->bits[i]) : single_lat_cfg_t<false>(p->bits[i]);
                     if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
@@ -1762,6 +1881,9 @@ struct RunOpts {
     const uint4* pmul;     // fused point-wise product (polymul inverse)
     bool polymul;          // use the R-compensated inverse tables
     const Ntt128IO* io = nullptr;   // four-step input / output layouts (fourstep.cu)
+    // NTT128_FLAG_CHAIN: the stream's library generation before this API call and the one
+    // it took (ntt128_stream_gen); 0 when unknown (stream capture)
+    uint64_t gen_prev = 0, gen_new = 0;
 };
 
 static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaStream_t stream);
@@ -1919,6 +2041,74 @@ static void release_scratch(ntt128_plan_s* p, cudaStream_t stream, const CallScr
     else stream_touch(p, stream);
 }
 
+// ---------------------------------------------------------------- chained calls
+// NTT128_FLAG_CHAIN (include/ntt128.h, DESIGN.md §6 "Chained calls"): the first pass of a
+// transform waits, per polynomial, on the previous call's last-pass counters instead of on
+// the whole previous grid (griddepcontrol.wait) -- so the tail of one transform overlaps the
+// start of the next, as consecutive passes of one transform already do.  Allowed only when
+// (a) the previous library call on the stream was this plan's own counter-signalling
+// transform (library-wide per-stream generation, ntt128_stream_gen) and (b) every buffer
+// of this call either is a buffer of that call (same base) or is disjoint from all of them
+// -- every pass touches only its own polynomial's [N] slice of each buffer, so the
+// per-polynomial order then covers every read-after-write, write-after-read and
+// write-after-write pair between the two calls.  Otherwise the first pass waits for the
+// whole previous grid, as without the flag.
+static std::mutex g_gen_mu;
+static std::unordered_map<unsigned long long, uint64_t> g_gen;   // stream id -> generation
+static uint64_t g_gen_next = 0;
+// Every public entry point that enqueues device work calls this once per call (it is a no-op
+// unless a chained plan exists).  Returns the stream's generation before the call in *prev
+// and the call's own in *now (unique across streams; 0 / 0 under stream capture).
+void ntt128_stream_gen(cudaStream_t stream, uint64_t* prev, uint64_t* now) {
+    *prev = *now = 0;
+    if (g_chain_plans.load(std::memory_order_relaxed) == 0) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    unsigned long long sid = 0;
+    if (cudaStreamGetId(stream, &sid) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(g_gen_mu);
+    if (g_gen.size() > 4096) g_gen.clear();        // generations stay unique: a cleared stream never matches
+    uint64_t& g = g_gen[sid];
+    *prev = g;
+    g = *now = ++g_gen_next;
+}
+static bool chain_bufs_ok(const ntt128_plan_s* p, const ntt128_plan_s::StreamCtr* c, const void* const cur[3]) {
+    const uintptr_t bytes = (uintptr_t)p->N * p->batch * sizeof(uint4);
+    for (int i = 0; i < 3; i++) {
+        if (!cur[i]) continue;
+        for (int j = 0; j < 3; j++) {
+            const uintptr_t a = (uintptr_t)cur[i], b = (uintptr_t)c->last_bufs[j];
+            if (!b || a == b || a + bytes <= b || b + bytes <= a) continue;
+            return false;                          // partial overlap: polynomials would not line up
+        }
+    }
+    return true;
+}
+// Decide whether this call's first pass may wait on the previous call's counters (the
+// caller holds p->mu through `ctr`); `cur` are the call's buffers.
+static bool chain_wait(const ntt128_plan_s* p, const ntt128_plan_s::StreamCtr* ctr, const RunOpts& o,
+                       const void* const cur[3]) {
+    if (!(p->flags & NTT128_FLAG_CHAIN) || o.gen_new == 0 || ctr->last_row < 0) return false;
+    if (ctr->gen != o.gen_prev && ctr->gen != o.gen_new) return false;   // other library work in between
+    return chain_bufs_ok(p, ctr, cur);
+}
+static void chain_first(const ntt128_plan_s* p, const ntt128_plan_s::StreamCtr* ctr, PassArgs& a) {
+    a.pdl_wait = 0u;
+    a.cnt_in = ctr->d + (size_t)ctr->last_row * p->batch;
+    a.target = ctr->last_target;
+}
+// the last pass of a chained plan's transform signals row npass - 1; record the call
+static void chain_last(ntt128_plan_s* p, ntt128_plan_s::StreamCtr* ctr, PassArgs& a, size_t npass,
+                       uint32_t ctas_per_poly, const RunOpts& o, const void* const cur[3]) {
+    const int row = (int)npass - 1;
+    a.cnt_out = ctr->d + (size_t)row * p->batch;
+    ctr->expected[row] += ctas_per_poly;
+    ctr->last_row = row;
+    ctr->last_target = ctr->expected[row];
+    for (int j = 0; j < 3; j++) ctr->last_bufs[j] = cur[j];
+    ctr->gen = o.gen_new;
+}
+
 // pass i (of npass, execution order) of an overlapped transform: the first pass waits for
 // the previous grid; pass i > 0 waits on row i - 1 for the previous pass's CTAs per
 // polynomial; every pass but the last signals row i.
@@ -2014,6 +2204,10 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
     // a single-pass transform is one programmatic dependent launch (no counters): its
     // launch and twiddle prologue overlap the previous kernel's tail, also under capture
     const bool pdl_single = npass == 1 && !switches().no_pdl;
+    const void* const bufs[3] = {src, dst, o.pmul};
+    const bool chain = overlap && (p->flags & NTT128_FLAG_CHAIN) && !o.io && !switches().pdl_nocnt;
+    const bool wait_prev = chain && chain_wait(p, ctr, o, bufs);
+    if (ctr && (p->flags & NTT128_FLAG_CHAIN) && !chain) ctr->last_row = -1;   // not signalling: no successor may chain
     int lo = 0;
     uint32_t prev_ctas_per_poly = 0;
     for (size_t i = 0; i < npass; i++) {
@@ -2079,9 +2273,14 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
                 for (int h = 0; h < NTT128_FS_MAX_RANKS; h++) a.rdst[h] = o.io->rdst[h];
             }
         }
+        if (c.tma && (a.fin || a.pmul || a.in_ps != p->N || a.in_es != 1 ||
+                      !tma_encode(a, c.first, n, B, lo, p->batch)))
+            c = pass_cfg(npass, i, B, scale_last, lo, n, false);   // per-thread cp.async tiles
         // CTAs that signal each polynomial's counter (a PM CTA signals all of its C polynomials)
         const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (pm ? 1u : (uint64_t)c.C));
         if (overlap) set_overlap(p, ctr, a, i, npass, prev_ctas_per_poly);
+        if (i == 0 && wait_prev) chain_first(p, ctr, a);
+        if (chain && last) chain_last(p, ctr, a, npass, ctas_per_poly, o, bufs);
         if (pdl_single) a.pdl_wait = 1u;
         const uint64_t ctas = (a.total_groups + c.C - 1) / c.C;
         if (launch_pass(c, a, ctas, stream, overlap || pdl_single) != cudaSuccess) return NTT128_ERR_CUDA;
@@ -2097,7 +2296,7 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
 // out, N^-1 in the last stage; `pmul` fuses the point-wise product into the inverse's
 // first load (its R^-1 is cancelled by the R-scaled last-stage table).
 static ntt128_status run_transform_nc(ntt128_plan_s* p, const uint4* src, uint4* dst, cudaStream_t stream,
-                                      bool inverse, const uint4* pmul) {
+                                      bool inverse, const uint4* pmul, const RunOpts& go) {
     const int n = (int)p->log2n;
     const size_t npass = p->nc_bits.size();
     bool overlap = false;
@@ -2108,6 +2307,9 @@ static ntt128_status run_transform_nc(ntt128_plan_s* p, const uint4* src, uint4*
         ntt128_status st = stream_counters(p, stream, lk, &ctr);
         if (st != NTT128_OK) return st;
     }
+    const void* const bufs[3] = {src, dst, pmul};
+    const bool chain = overlap && (p->flags & NTT128_FLAG_CHAIN) && !switches().pdl_nocnt;
+    const bool wait_prev = chain && chain_wait(p, ctr, go, bufs);
     std::vector<int> los(npass);
     for (size_t k = 0, lo = 0; k < npass; k++) { los[k] = (int)lo; lo += p->nc_bits[k]; }
     uint32_t prev_ctas_per_poly = 0;
@@ -2132,6 +2334,8 @@ static ntt128_status run_transform_nc(ntt128_plan_s* p, const uint4* src, uint4*
         a.ninv_r = pmul ? 1 : 0;
         const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (uint64_t)c.C);
         if (overlap) set_overlap(p, ctr, a, i, npass, prev_ctas_per_poly);
+        if (i == 0 && wait_prev) chain_first(p, ctr, a);
+        if (chain && i + 1 == npass) chain_last(p, ctr, a, npass, ctas_per_poly, go, bufs);
         const uint64_t ctas = (a.total_groups + c.C - 1) / c.C;
         if (launch_pass(c, a, ctas, stream, overlap) != cudaSuccess) return NTT128_ERR_CUDA;
         ntt128_count_launch(1);
@@ -2184,6 +2388,7 @@ static ntt128_status transform(const ntt128_plan_t p, const uint64_t* d_in, uint
         if (s != NTT128_OK) return s;
     }
     RunOpts o{inverse, nullptr, false};
+    ntt128_stream_gen(stream, &o.gen_prev, &o.gen_new);
     if (src == dst && p->bits.size() > 1) {
         // the first pass gathers bit-reversed columns: it cannot run in place
         const size_t bytes = (size_t)p->N * p->batch * sizeof(uint4);
@@ -2224,17 +2429,19 @@ extern "C" ntt128_status ntt128_polymul(const ntt128_plan_t p, const uint64_t* d
     if (s != NTT128_OK) return s;
     uint4* fa = cs.ptr;
     uint4* fb = fa + (size_t)p->N * p->batch;
+    RunOpts go{false, nullptr, false};
+    ntt128_stream_gen(stream, &go.gen_prev, &go.gen_new);   // one API call: its transforms chain among themselves
     if (!p->nc_bits.empty() && !switches().no_nc) {
         // permutation-free pipeline: no twist / untwist multiplies, spectra stay bit-reversed
-        s = run_transform_nc(p, (const uint4*)d_a, fa, stream, false, nullptr);
-        if (s == NTT128_OK) s = run_transform_nc(p, (const uint4*)d_b, fb, stream, false, nullptr);
-        if (s == NTT128_OK) s = run_transform_nc(p, fa, (uint4*)d_c, stream, true, fb);
+        s = run_transform_nc(p, (const uint4*)d_a, fa, stream, false, nullptr, go);
+        if (s == NTT128_OK) s = run_transform_nc(p, (const uint4*)d_b, fb, stream, false, nullptr, go);
+        if (s == NTT128_OK) s = run_transform_nc(p, fa, (uint4*)d_c, stream, true, fb, go);
     } else {
-        RunOpts fwd{false, nullptr, false};
+        RunOpts fwd{false, nullptr, false, nullptr, go.gen_prev, go.gen_new};
         s = run_transform(p, (const uint4*)d_a, fa, stream, fwd);
         if (s == NTT128_OK) s = run_transform(p, (const uint4*)d_b, fb, stream, fwd);
         // inverse with the point-wise Montgomery product fused into its first pass's load
-        RunOpts inv{true, fb, true};
+        RunOpts inv{true, fb, true, nullptr, go.gen_prev, go.gen_new};
         if (s == NTT128_OK) s = run_transform(p, fa, (uint4*)d_c, stream, inv);
     }
     release_scratch(p, stream, cs);
@@ -2252,7 +2459,9 @@ static ntt128_status transform_bitrev(const ntt128_plan_t p, const uint64_t* d_i
         ntt128_status s = check_range(p, (const uint4*)d_in, stream);
         if (s != NTT128_OK) return s;
     }
-    const ntt128_status s = run_transform_nc(p, (const uint4*)d_in, (uint4*)d_out, stream, inverse, nullptr);
+    RunOpts go{inverse, nullptr, false};
+    ntt128_stream_gen(stream, &go.gen_prev, &go.gen_new);
+    const ntt128_status s = run_transform_nc(p, (const uint4*)d_in, (uint4*)d_out, stream, inverse, nullptr, go);
     stream_touch(p, stream);
     return s;
 }
@@ -2280,6 +2489,7 @@ ntt128_status ntt128_transform_io(ntt128_plan_t p, const uint4* src, uint4* dst,
     if (src == dst && p->bits.size() > 1) return NTT128_ERR_INVALID_ARG;
     DeviceGuard g(p->device);
     RunOpts o{inverse, nullptr, false, &io};
+    ntt128_stream_gen(stream, &o.gen_prev, &o.gen_new);
     const ntt128_status s = run_transform(p, src, dst, stream, o);
     if (p->bits.size() > 1) stream_touch(p, stream);
     return s;

@@ -29,5 +29,9 @@ struct Ntt128IO {
     uint4* tmp = nullptr;
 };
 
+// NTT128_FLAG_CHAIN bookkeeping (ntt128.cu): every public entry point that enqueues device
+// work takes its stream's next library generation (no-op while no chained plan exists).
+void ntt128_stream_gen(cudaStream_t stream, uint64_t* prev, uint64_t* now);
+
 ntt128_status ntt128_transform_io(ntt128_plan_t p, const uint4* src, uint4* dst, cudaStream_t stream, bool inverse,
                                   const Ntt128IO& io);

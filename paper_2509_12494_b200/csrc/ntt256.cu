@@ -21,6 +21,7 @@
 
 #include "../../include/ntt128.h"
 #include "arith256_gen.cuh"
+#include "ntt128_internal.h"
 
 void ntt128_count_launch(uint64_t k);
 
@@ -557,9 +558,13 @@ static ntt128_status transform256(const ntt256_plan_t p, const uint64_t* d_in, u
     return r;
 }
 extern "C" ntt128_status ntt256_forward(const ntt256_plan_t p, const uint64_t* d_in, uint64_t* d_out, ntt128_stream_t s) {
+    uint64_t g0, g1;
+    ntt128_stream_gen((cudaStream_t)s, &g0, &g1);   // NTT128_FLAG_CHAIN: other library work on the stream
     return transform256(p, d_in, d_out, s, false);
 }
 extern "C" ntt128_status ntt256_inverse(const ntt256_plan_t p, const uint64_t* d_in, uint64_t* d_out, ntt128_stream_t s) {
+    uint64_t g0, g1;
+    ntt128_stream_gen((cudaStream_t)s, &g0, &g1);
     return transform256(p, d_in, d_out, s, true);
 }
 
@@ -571,6 +576,8 @@ extern "C" ntt128_status vec256_mul(uint64_t* d_z, const uint64_t* d_x, const ui
     if (n == 0) return NTT128_OK;
     if (!d_z || !d_x || !d_y) return NTT128_ERR_INVALID_ARG;
     if (((uintptr_t)d_z | (uintptr_t)d_x | (uintptr_t)d_y) & 15u) return NTT128_ERR_ALIGNMENT;
+    uint64_t g0, g1;
+    ntt128_stream_gen((cudaStream_t)s, &g0, &g1);
     const ModC256 M = make_modc(q, 1);
     unsigned g = (unsigned)((n + 255) / 256);
     if (g > 148 * 8) g = 148 * 8;

@@ -3,7 +3,7 @@
 //
 // HBM-bound (48 bytes per element at ~6.5 TB/s vs <= 2 Montgomery products per
 // element): a grid-stride loop over 16-byte elements, each thread
-// keeping UNROLL independent elements in flight for memory-level parallelism.
+// keeping UNROLL independent elements in flight (vec_unroll below).
 // vec128_mul is a general product: mont(mont(x, y), R^2) = x y mod q.
 // axpy uses the host-converted Montgomery scalar a R mod q: mont(x, aR) = a x.
 #include <cuda_runtime.h>
@@ -16,6 +16,7 @@
 #include "arith128.cuh"
 #include "barrett128.cuh"
 #include "host128.h"
+#include "ntt128_internal.h"
 
 #ifndef NTT128_EXPERIMENTS
 #define NTT128_EXPERIMENTS 0   // 1: experiment build (environment switches; never the product .so)
@@ -46,11 +47,25 @@ __device__ __forceinline__ U128 mul_b(const U128& a, const U128& b, const Barret
     return r;
 }
 
-#ifndef NTT_VEC_UNROLL
-#define NTT_VEC_UNROLL 4   // residues in flight per thread (4: measured; 2 / 8: tools/exp_vec_graph.py)
+// Residues per thread and resident-CTA cap (tools/exp_vec_graph.py sweeps, profiles/r02/vec_sweep.txt):
+// many small CTAs over several waves beat one wave of 4-residue threads -- a CTA that finishes
+// is replaced by one whose loads then overlap its neighbours' products.  mul keeps 2 residues
+// per thread (its 43-product Barrett needs the in-flight loads), add / sub / axpy take 1.
+#ifndef NTT_VEC_UNROLL_MUL
+#define NTT_VEC_UNROLL_MUL 2
 #endif
-constexpr int UNROLL = NTT_VEC_UNROLL;
-constexpr int THREADS = 256;
+#ifndef NTT_VEC_UNROLL
+#define NTT_VEC_UNROLL 1
+#endif
+#ifndef NTT_VEC_CTAS_PER_SM
+#define NTT_VEC_CTAS_PER_SM 16
+#endif
+template <int OPK>
+constexpr int vec_unroll() { return (OPK == OP_MUL || OPK == OP_MULB) ? NTT_VEC_UNROLL_MUL : NTT_VEC_UNROLL; }
+#ifndef NTT_VEC_THREADS
+#define NTT_VEC_THREADS 256
+#endif
+constexpr int THREADS = NTT_VEC_THREADS;
 
 template <int OPK, int UNROLL = 4>
 __global__ void __launch_bounds__(THREADS) k_vec(uint4* z, const uint4* __restrict__ x,
@@ -248,17 +263,17 @@ void words(u128 v, uint32_t w[4]) {
     for (int i = 0; i < 4; i++) w[i] = (uint32_t)(v >> (32 * i));
 }
 
-int grid_for(uint64_t n) {
+int grid_for(uint64_t n, int unroll) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    uint64_t want = (n + (uint64_t)THREADS * UNROLL - 1) / ((uint64_t)THREADS * UNROLL);
+    uint64_t want = (n + (uint64_t)THREADS * unroll - 1) / ((uint64_t)THREADS * unroll);
 #if NTT128_EXPERIMENTS
-    static const int per_sm = getenv("NTT128_VEC_CTAS_PER_SM") ? atoi(getenv("NTT128_VEC_CTAS_PER_SM")) : 8;
+    static const int per_sm = getenv("NTT128_VEC_CTAS_PER_SM") ? atoi(getenv("NTT128_VEC_CTAS_PER_SM")) : NTT_VEC_CTAS_PER_SM;
 #else
-    constexpr int per_sm = 8;
+    constexpr int per_sm = NTT_VEC_CTAS_PER_SM;
 #endif
-    uint64_t cap = (uint64_t)sms * per_sm;  // resident 256-thread CTAs per SM
+    uint64_t cap = (uint64_t)sms * per_sm;  // CTAs per SM over the launch (several waves)
     if (want > cap) want = cap;
     return want < 1 ? 1 : (int)want;
 }
@@ -272,6 +287,8 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
     if (n == 0) return NTT128_OK;
     if (!d_z || !d_x || !d_y) return NTT128_ERR_INVALID_ARG;
     if (((uintptr_t)d_z | (uintptr_t)d_x | (uintptr_t)d_y) & 15u) return NTT128_ERR_ALIGNMENT;
+    uint64_t g0, g1;
+    ntt128_stream_gen(stream, &g0, &g1);   // NTT128_FLAG_CHAIN: other library work on the stream
     ntt128h::Mont M(q);
     VecConst c;
     words(q, c.q);
@@ -307,7 +324,8 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
     const uint4* x = (const uint4*)d_x;
     const uint4* y = (const uint4*)d_y;
     uint4* z = (uint4*)d_z;
-    const int grid = grid_for(n);
+    const int opk_ = (op == OP_MUL && (q >> 127) != 0) ? OP_MULB : op;
+    const int grid = grid_for(n, (opk_ == OP_MUL || opk_ == OP_MULB) ? NTT_VEC_UNROLL_MUL : NTT_VEC_UNROLL);
     if (flags & NTT128_FLAG_CHECK_INPUT) {
         int* d_err = nullptr;
         int h = 0;
@@ -360,13 +378,13 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
     cfg.numAttrs = 1;
     cudaError_t e;
     switch (op) {
-        case OP_ADD: e = cudaLaunchKernelEx(&cfg, k_vec<OP_ADD, UNROLL>, z, x, y, (uint64_t)n, c); break;
-        case OP_SUB: e = cudaLaunchKernelEx(&cfg, k_vec<OP_SUB, UNROLL>, z, x, y, (uint64_t)n, c); break;
+        case OP_ADD: e = cudaLaunchKernelEx(&cfg, k_vec<OP_ADD, vec_unroll<OP_ADD>()>, z, x, y, (uint64_t)n, c); break;
+        case OP_SUB: e = cudaLaunchKernelEx(&cfg, k_vec<OP_SUB, vec_unroll<OP_SUB>()>, z, x, y, (uint64_t)n, c); break;
         case OP_MUL:
-            e = barrett ? cudaLaunchKernelEx(&cfg, k_vec<OP_MULB, UNROLL>, z, x, y, (uint64_t)n, c)
-                        : cudaLaunchKernelEx(&cfg, k_vec<OP_MUL, UNROLL>, z, x, y, (uint64_t)n, c);
+            e = barrett ? cudaLaunchKernelEx(&cfg, k_vec<OP_MULB, vec_unroll<OP_MULB>()>, z, x, y, (uint64_t)n, c)
+                        : cudaLaunchKernelEx(&cfg, k_vec<OP_MUL, vec_unroll<OP_MUL>()>, z, x, y, (uint64_t)n, c);
             break;
-        default: e = cudaLaunchKernelEx(&cfg, k_vec<OP_AXPY, UNROLL>, z, x, y, (uint64_t)n, c); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_vec<OP_AXPY, vec_unroll<OP_AXPY>()>, z, x, y, (uint64_t)n, c); break;
     }
     ntt128_count_launch(1);
     return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? NTT128_OK : NTT128_ERR_CUDA;

@@ -60,7 +60,7 @@ _L.ntt128_status_string.restype = ctypes.c_char_p
 _L.ntt128_launch_count.argtypes = []
 _L.ntt128_launch_count.restype = ctypes.c_uint64
 
-CYCLIC, NEGACYCLIC, FLAG_CHECK_INPUT = 0, 1, 0x100
+CYCLIC, NEGACYCLIC, FLAG_CHECK_INPUT, FLAG_CHAIN = 0, 1, 0x100, 0x200   # include/ntt128.h
 OK = 0
 _ARG_ERRORS = {1, 2, 3, 4, 5, 6, 7}
 
@@ -129,11 +129,12 @@ class Plan:
     """Batched 128-bit NTT plan (ntt128_plan_create).
 
     log2n: 1..26; q, root: int (shared) or a sequence of `batch` ints (one prime per
-    polynomial, the RNS case); negacyclic: root is psi of order 2N.
+    polynomial, the RNS case); negacyclic: root is psi of order 2N; chain: NTT128_FLAG_CHAIN
+    (consecutive calls on a stream overlap polynomial by polynomial; include/ntt128.h).
     """
 
     def __init__(self, log2n: int, q, root, batch: int = 1, negacyclic: bool = False, check_input: bool = False,
-                 device: int | None = None):
+                 device: int | None = None, chain: bool = False):
         qs = list(q) if isinstance(q, (list, tuple)) else [q]
         rs = list(root) if isinstance(root, (list, tuple)) else [root]
         if len(qs) != len(rs):
@@ -142,7 +143,8 @@ class Plan:
         self.negacyclic = bool(negacyclic)
         self.device = torch.cuda.current_device() if device is None else int(device)
         self.q = [int(v) for v in qs]
-        flags = (NEGACYCLIC if negacyclic else CYCLIC) | (FLAG_CHECK_INPUT if check_input else 0)
+        flags = ((NEGACYCLIC if negacyclic else CYCLIC) | (FLAG_CHECK_INPUT if check_input else 0)
+                 | (FLAG_CHAIN if chain else 0))
         h = _vp()
         self._h = None
         _check(_L.ntt128_plan_create(ctypes.byref(h), self.log2n, self.batch, _pairs(qs), _pairs(rs), len(qs), flags,
