@@ -267,6 +267,58 @@ __device__ __forceinline__ U128 sub_add_nored(const U128& u, const U128& t, cons
     return s;
 }
 
+// u 2^-s mod q, 1 <= s <= 31 (the inverse transform's N^-1 = 2^-n on the last stage's u
+// branch, DESIGN.md §5 "N^-1 by one short digit"): a single s-bit Montgomery digit,
+// m = u_0 (-q^-1) mod 2^s, so u + m q = 0 mod 2^s, and T = (u + m q) / 2^s = u 2^-s (mod q)
+// with T < q + u / 2^s.  4 low + 4 high 32x32 products and 4 funnel shifts instead of a
+// 36-product Montgomery multiplication by N^-1 R.  t[4] is T's bit 128 (T < 2^129).
+__device__ __forceinline__ void shr_core(const U128& u, uint32_t s, const uint32_t q[4], uint32_t qinv0, uint32_t t[5]) {
+    const uint32_t m = (u.w[0] * qinv0) & ((1u << s) - 1u);
+    uint32_t x0, x1, x2, x3, x4;
+    asm("mad.lo.cc.u32  %0, %5, %6, %10;\n\t"
+        "madc.lo.cc.u32 %1, %5, %7, %11;\n\t"
+        "madc.lo.cc.u32 %2, %5, %8, %12;\n\t"
+        "madc.lo.cc.u32 %3, %5, %9, %13;\n\t"
+        "addc.u32       %4, 0, 0;\n\t"
+        "mad.hi.cc.u32  %1, %5, %6, %1;\n\t"
+        "madc.hi.cc.u32 %2, %5, %7, %2;\n\t"
+        "madc.hi.cc.u32 %3, %5, %8, %3;\n\t"
+        "madc.hi.u32    %4, %5, %9, %4;"
+        : "=&r"(x0), "=&r"(x1), "=&r"(x2), "=&r"(x3), "=&r"(x4)
+        : "r"(m), "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]), "r"(u.w[0]), "r"(u.w[1]), "r"(u.w[2]), "r"(u.w[3]));
+    t[0] = __funnelshift_r(x0, x1, s);
+    t[1] = __funnelshift_r(x1, x2, s);
+    t[2] = __funnelshift_r(x2, x3, s);
+    t[3] = __funnelshift_r(x3, x4, s);
+    t[4] = x4 >> s;
+}
+// canonical u 2^-s mod q for u < q (T < q + q / 2^s < 2q: one conditional subtraction)
+__device__ __forceinline__ U128 shr_mod(const U128& u, uint32_t s, const uint32_t q[4], uint32_t qinv0) {
+    uint32_t t[5];
+    shr_core(u, s, q, qinv0, t);
+    uint32_t d0, d1, d2, d3, bw;
+    asm("sub.cc.u32  %0, %5, %10;\n\t"
+        "subc.cc.u32 %1, %6, %11;\n\t"
+        "subc.cc.u32 %2, %7, %12;\n\t"
+        "subc.cc.u32 %3, %8, %13;\n\t"
+        "subc.u32    %4, %9, 0;"
+        : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(d3), "=r"(bw)
+        : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]));
+    U128 r;
+    r.w[0] = (t[0] & bw) | (d0 & ~bw);
+    r.w[1] = (t[1] & bw) | (d1 & ~bw);
+    r.w[2] = (t[2] & bw) | (d2 & ~bw);
+    r.w[3] = (t[3] & bw) | (d3 & ~bw);
+    return r;
+}
+// lazy u 2^-s mod q in [0, 2q): u < 4q with q < 2^126 and s >= 2, or u < 2q with q < 2^127
+// (T < q + u / 2^s <= 2q < 2^128: no fifth word)
+__device__ __forceinline__ U128 shr_mod_lazy(const U128& u, uint32_t s, const uint32_t q[4], uint32_t qinv0) {
+    uint32_t t[5];
+    shr_core(u, s, q, qinv0, t);
+    return U128{{t[0], t[1], t[2], t[3]}};
+}
+
 // a < q check (for NTT128_FLAG_CHECK_INPUT): borrow out of a - q
 __device__ __forceinline__ bool lt_q(const U128& a, const uint32_t q[4]) {
     uint32_t bw;

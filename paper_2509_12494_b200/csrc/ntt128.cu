@@ -413,21 +413,26 @@ __device__ __forceinline__ int mode_of(const uint32_t q[4]) {
 
 // One radix-2 CT butterfly (u, v) -> (u + w v, u - w v) in the given mode.  In the last
 // stage of a scaled inverse u is multiplied by nf = N^-1 (Montgomery form) too.
+#ifndef NTT_SHIFT_SCALE
+#define NTT_SHIFT_SCALE 1     // 0: N^-1 always by the Montgomery product (A/B experiment)
+#endif
+// sh != 0 (a plain inverse, N = 2^sh): u N^-1 = u 2^-sh by one short digit (shr_mod, 8 word
+// products) instead of the Montgomery product by nf (36); polymul's N^-1 R keeps nf.
 template <int MODE, bool SCALE_U>
 __device__ __forceinline__ void bfly(U128& u, U128& v, const U128& w, const uint32_t q[4], const uint32_t q2[4],
-                                     uint32_t qinv0, const U128& nf) {
+                                     uint32_t qinv0, const U128& nf, uint32_t sh = 0) {
     if (MODE == MODE_FULL) {
-        const U128 us = SCALE_U ? mont_mul(u, nf, q, qinv0) : u;
+        const U128 us = SCALE_U ? (sh ? shr_mod(u, sh, q, qinv0) : mont_mul(u, nf, q, qinv0)) : u;
         const U128 t = mont_mul(v, w, q, qinv0);
         u = add_mod(us, t, q);
         v = sub_mod(us, t, q);
     } else if (MODE == MODE_HALF) {   // u, v in [0, 2q): t in [0, 2q); results mod 2q
-        const U128 us = SCALE_U ? mont_mul_lazy(u, nf, q, qinv0) : u;
+        const U128 us = SCALE_U ? (sh ? shr_mod_lazy(u, sh, q, qinv0) : mont_mul_lazy(u, nf, q, qinv0)) : u;
         const U128 t = mont_mul_lazy(v, w, q, qinv0);
         u = add_mod(us, t, q2);
         v = sub_mod(us, t, q2);
     } else {                          // Harvey: u, v in [0, 4q); u' = u mod 2q; u' + t, u' - t + 2q
-        const U128 us = SCALE_U ? mont_mul_lazy(u, nf, q, qinv0) : reduce_2q(u, q2);
+        const U128 us = SCALE_U ? (sh ? shr_mod_lazy(u, sh, q, qinv0) : mont_mul_lazy(u, nf, q, qinv0)) : reduce_2q(u, q2);
         const U128 t = mont_mul_lazy(v, w, q, qinv0);
         u = add_nored(us, t);
         v = sub_add_nored(us, t, q2);
@@ -475,7 +480,7 @@ __device__ __forceinline__ void bfly_tw1(U128& u, U128& v, const uint32_t q[4], 
 template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL, bool R0>
 __device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4* tws, const int t, const uint32_t lo,
                                            const uint32_t n, const uint32_t q[4], const uint32_t q2[4],
-                                           const uint32_t qinv0, const U128& nf) {
+                                           const uint32_t qinv0, const U128& nf, const uint32_t sh) {
     using S = PassShape<B, RBMAX, C, PADL>;
     constexpr int RB = S::RB, E = S::E;
     const int slo = R0 ? 0 : rd * RB;
@@ -510,7 +515,7 @@ __device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4
             const int k1 = k0 | (1 << bit);
             const int j = kk & ((1 << bit) - 1);
             if (R0 && j == 0 && !last) bfly_tw1<MODE>(x[k0], x[k1], q, q2);
-            else if (last) bfly<MODE, true>(x[k0], x[k1], tw[j], q, q2, qinv0, nf);
+            else if (last) bfly<MODE, true>(x[k0], x[k1], tw[j], q, q2, qinv0, nf, sh);
             else bfly<MODE, false>(x[k0], x[k1], tw[j], q, q2, qinv0, nf);
         }
     }
@@ -521,7 +526,7 @@ __device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4
 
 template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool WARPSYNC, bool PADL>
 __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
-                                            const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
+                                            const uint32_t q[4], const uint32_t qinv0, const U128 nf, const uint32_t sh) {
     uint32_t q2[4] = {0, 0, 0, 0};
     if (MODE != MODE_FULL) {
         q2[0] = q[0] << 1;
@@ -532,12 +537,12 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
     using S = PassShape<B, RBMAX, C, PADL>;
     constexpr int rd0 = FIRST ? 1 : 0;
     if (FIRST)
-        round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, true>(0, gsm, tws, t, lo, n, q, q2, qinv0, nf);
+        round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, true>(0, gsm, tws, t, lo, n, q, q2, qinv0, nf, sh);
     if (S::RB == 2 && PADL && NTT_RB2_UNROLL) {
         // radix-4 rounds: unrolled, so every window and XOR-swizzle offset is a constant
 #pragma unroll
         for (int rd = rd0; rd < S::ROUNDS; rd++)
-            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf);
+            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf, sh);
     } else {
 #if NTT_UNROLL_ROUNDS
 #pragma unroll
@@ -545,7 +550,7 @@ __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const 
 #pragma unroll 1
 #endif
         for (int rd = rd0; rd < S::ROUNDS; rd++)
-            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf);
+            round_body<B, C, FIRST, SCALE_LAST, RBMAX, MODE, WARPSYNC, PADL, false>(rd, gsm, tws, t, lo, n, q, q2, qinv0, nf, sh);
     }
 }
 
@@ -786,16 +791,17 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
         const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
         const int mode = SINGLE ? MODE_FULL : mode_of(q);   // uniform per CTA: its groups share the polynomial
+        const uint32_t sh = (NTT_SHIFT_SCALE && SCALE_LAST && !a.ninv_r && n >= 2) ? n : 0u;   // plain inverse: N^-1 by shifting
 #if NTT_COMPUTE_REPEAT != 1
 #pragma unroll 1
         for (int rep = 0; rep < NTT_COMPUTE_REPEAT; rep++)
 #endif
         if (mode == MODE_LAZY)
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
         else if (mode == MODE_HALF)
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_HALF, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_HALF, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
         else
-            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_FULL, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf);
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_FULL, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
         if (WARPMAP) __syncthreads();   // the store phase reads every group
     }
 
@@ -937,21 +943,21 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
 // (u + v reduced by 2q, u - v + 2q fed to the lazy product, which accepts < 4q).
 template <int MODE, bool SCALE_U>
 __device__ __forceinline__ void gs_bfly(U128& u, U128& v, const U128& w, const uint32_t q[4], const uint32_t q2[4],
-                                        uint32_t qinv0, const U128& nf) {
+                                        uint32_t qinv0, const U128& nf, uint32_t sh = 0) {
     if (MODE == MODE_FULL) {
         const U128 s = add_mod(u, v, q);
         const U128 d = sub_mod(u, v, q);
-        u = SCALE_U ? mont_mul(s, nf, q, qinv0) : s;
+        u = SCALE_U ? (sh ? shr_mod(s, sh, q, qinv0) : mont_mul(s, nf, q, qinv0)) : s;
         v = mont_mul(d, w, q, qinv0);
     } else if (MODE == MODE_HALF) {
         const U128 s = add_mod(u, v, q2);
         const U128 d = sub_mod(u, v, q2);
-        u = SCALE_U ? mont_mul_lazy(s, nf, q, qinv0) : s;
+        u = SCALE_U ? (sh ? shr_mod_lazy(s, sh, q, qinv0) : mont_mul_lazy(s, nf, q, qinv0)) : s;
         v = mont_mul_lazy(d, w, q, qinv0);
     } else {
         const U128 s = add_nored(u, v);                 // < 4q
         const U128 d = sub_add_nored(u, v, q2);         // in (0, 4q)
-        u = SCALE_U ? mont_mul_lazy(s, nf, q, qinv0) : reduce_2q(s, q2);
+        u = SCALE_U ? (sh ? shr_mod_lazy(s, sh, q, qinv0) : mont_mul_lazy(s, nf, q, qinv0)) : reduce_2q(s, q2);
         v = mont_mul_lazy(d, w, q, qinv0);
     }
 }
@@ -960,7 +966,7 @@ __device__ __forceinline__ void gs_bfly(U128& u, U128& v, const U128& w, const u
 // (forward, each window's stages from its top bit) or bottom-up (inverse).
 template <int B, int C, bool INV, bool SCALE_LAST, int RBMAX, int MODE>
 __device__ __forceinline__ void nc_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
-                                          const uint32_t q[4], const uint32_t qinv0, const U128 nf) {
+                                          const uint32_t q[4], const uint32_t qinv0, const U128 nf, const uint32_t sh) {
     uint32_t q2[4] = {0, 0, 0, 0};
     if (MODE != MODE_FULL) {
         q2[0] = q[0] << 1;
@@ -1002,7 +1008,7 @@ __device__ __forceinline__ void nc_rounds(uint4* gsm, const uint4* tws, const in
                 const int k1 = k0 | (1 << bit);
                 const U128& wv = tw[k0 >> (bit + 1)];
                 if (!INV) bfly<MODE, false>(x[k0], x[k1], wv, q, q2, qinv0, nf);
-                else if (last) gs_bfly<MODE, true>(x[k0], x[k1], wv, q, q2, qinv0, nf);
+                else if (last) gs_bfly<MODE, true>(x[k0], x[k1], wv, q, q2, qinv0, nf, sh);
                 else gs_bfly<MODE, false>(x[k0], x[k1], wv, q, q2, qinv0, nf);
             }
         }
@@ -1098,9 +1104,10 @@ k_nc_pass(const PassArgs a) {
         uint4* gsm = sm + c * GS;
         const uint4* tws = tsm + (shared_set ? 0 : c) * TS;
         const int mode = mode_of(q);
-        if (mode == MODE_LAZY) nc_rounds<B, C, INV, SCALE_LAST, RBMAX, MODE_LAZY>(gsm, tws, t, lo, n, q, qinv0, nf);
-        else if (mode == MODE_HALF) nc_rounds<B, C, INV, SCALE_LAST, RBMAX, MODE_HALF>(gsm, tws, t, lo, n, q, qinv0, nf);
-        else nc_rounds<B, C, INV, SCALE_LAST, RBMAX, MODE_FULL>(gsm, tws, t, lo, n, q, qinv0, nf);
+        const uint32_t sh = (NTT_SHIFT_SCALE && SCALE_LAST && !a.ninv_r && n >= 2) ? n : 0u;   // plain inverse: N^-1 by shifting
+        if (mode == MODE_LAZY) nc_rounds<B, C, INV, SCALE_LAST, RBMAX, MODE_LAZY>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
+        else if (mode == MODE_HALF) nc_rounds<B, C, INV, SCALE_LAST, RBMAX, MODE_HALF>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
+        else nc_rounds<B, C, INV, SCALE_LAST, RBMAX, MODE_FULL>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
         __syncthreads();
     }
     {
@@ -1244,7 +1251,7 @@ __global__ void __launch_bounds__(1 << (LB - CLU_LOG - 1)) k_ntt_cluster(const P
             const int k0 = ((bb >> sp) << (sp + 1)) | (bb & ((1 << sp) - 1)), k1 = k0 | (1 << sp);
             u = u128_from(gb[k0]);
             v = u128_from(gb[k1]);
-            if (SCALE_LAST && LM + sp == LB - 1) bfly<MODE_FULL, true>(u, v, tw[LM + sp], q, q2, qinv0, nf);
+            if (SCALE_LAST && LM + sp == LB - 1) bfly<MODE_FULL, true>(u, v, tw[LM + sp], q, q2, qinv0, nf, (NTT_SHIFT_SCALE && !a.ninv_r) ? LB : 0u);
             else bfly<MODE_FULL, false>(u, v, tw[LM + sp], q, q2, qinv0, nf);
             if (sp + 1 < CLU_LOG) {
                 gb[k0] = u128_to(u);
