@@ -12,7 +12,8 @@ KEYS = ['gpu__time_duration.sum', 'smsp__issue_active.avg.pct_of_peak_sustained_
 
 
 def main(path, nlaunch=4):
-    out = subprocess.run(['ncu', '-i', path, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+    # a .ncu-rep, or its raw page already exported (ncu -i ... --page raw --csv > x.csv)
+    out = open(path).read() if path.endswith('.csv') else subprocess.run(['ncu', '-i', path, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
     hdr, units = r[0], r[1]
     for row in r[2:2 + nlaunch]:

@@ -7,7 +7,8 @@ import sys
 
 
 def main(rep, out, tag):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # a .ncu-rep, or its raw page already exported (ncu -i ... --page raw --csv > x.csv)
+    txt = open(rep).read() if rep.endswith('.csv') else subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(txt.splitlines()))
     hdr, units = r[0], r[1]
     rows = []
