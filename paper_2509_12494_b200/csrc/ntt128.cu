@@ -305,10 +305,28 @@ __global__ void k_gather_nc_tw(uint4* out, uint64_t out_stride, const uint4* psi
 }
 
 // ----------------------------------------------------------------------------- pass kernel
+// Per-modulus constants of one launch as KERNEL PARAMETERS (multi-pass kernels, DESIGN.md §5
+// "Moduli in uniform registers"): indexed by a block-uniform polynomial index they load with
+// LDCU into uniform registers, so every q-word operand of the Montgomery products and the
+// mod-q adds is a uniform register -- no vector registers or vector register-file reads for
+// q, 2q, q' (register-only butterfly rate +7.7 % LAZY, +2.6 % FULL, tools/micro/bfly_uniform.cu).
+// A launch carries at most NTT_QMAX moduli: RNS plans with more polynomials launch each pass
+// in chunks of NTT_QMAX polynomials.
+#ifndef NTT_QMAX
+#define NTT_QMAX 64
+#endif
+struct QPar {
+    uint32_t q[4];
+    uint32_t qinv0, pad[3];
+    uint32_t ninv_m[4];   // N^-1 R mod q
+    uint32_t ninv_rm[4];  // N^-1 R^2 mod q
+};
 struct PassArgs {
     // TMA kernels (k_ntt_pass<..., TMA>): the data tile's tensor map over src, encoded per
     // launch by the host (tma_map_*); unused otherwise.  First member: 64-byte aligned.
     CUtensorMap tm;
+    QPar qp[NTT_QMAX];     // multi-pass kernels: the launch's moduli (qp[0] when nq == 1)
+    uint16_t ord[NTT_QMAX];// multi-pass kernels, nq > 1: CTA polynomial slot -> polynomial (grouped by class)
     const uint4* src;      // [batch][N]
     uint4* dst;            // [batch][N]
     const uint4* pmul;     // optional point-wise multiplicand, same layout as src (Montgomery product)
@@ -316,7 +334,6 @@ struct PassArgs {
     const uint4* fin;      // optional [nq][f_stride]: factor applied at load, by natural input index
     const uint4* fout;     // optional [nq][f_stride]: factor applied at store, by natural output index
     const ModC* mods;      // [nq]
-    const uint32_t* order; // optional [batch]: polynomial processed by CTA slot (lazy-path polynomials first)
     uint64_t pt_stride, f_stride;
     uint64_t total_groups; // batch << (n - B)
     uint32_t n, lo, nq;
@@ -600,7 +617,8 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
     uint64_t gg0 = (uint64_t)blockIdx.x * C;
     // multi-pass CTAs hold groups of one polynomial: visit polynomials in the plan's order
     // (grouped by arithmetic mode) so one code path at a time is hot in the I-cache
-    if (!SINGLE && !PM && a.order) gg0 = ((uint64_t)a.order[gg0 >> gbits] << gbits) | (gg0 & gmask);
+    // (a kernel-parameter table: the polynomial index stays block-uniform, in uniform registers)
+    if (!SINGLE && !PM && a.nq > 1) gg0 = ((uint64_t)a.ord[gg0 >> gbits] << gbits) | (gg0 & gmask);
     // PM (polynomial-major first pass, four-step pass C over a received matrix whose
     // polynomials are adjacent in memory): the CTA's C groups are column g0
     // of the C consecutive polynomials [pc C, pc C + C), CTAs ordered g-major, so a row of
@@ -775,11 +793,20 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
         const int c = WARPMAP ? tid / T : tid % C, t = WARPMAP ? tid % T : tid / C;
         const uint64_t gg = gg_of(c);
         const uint64_t ggc = gg < a.total_groups ? gg : a.total_groups - 1;
-        const uint32_t m = a.nq == 1 ? 0 : (uint32_t)(ggc >> gbits);
         uint32_t q[4], qinv0;
         U128 nf;
-        {
+        if (SINGLE) {   // one-pass CTAs may hold several moduli (lanes differ): the device table
+            const uint32_t m = a.nq == 1 ? 0 : (uint32_t)(ggc >> gbits);
             const ModC& M = a.mods[m];
+            q[0] = M.q[0]; q[1] = M.q[1]; q[2] = M.q[2]; q[3] = M.q[3];
+            qinv0 = M.qinv0;
+            if (SCALE_LAST) {
+                const uint32_t* src = a.ninv_r ? M.ninv_rm : M.ninv_m;
+                nf = U128{{src[0], src[1], src[2], src[3]}};
+            }
+        } else {        // multi-pass: the CTA's groups share one polynomial (PM: nq == 1) -- uniform
+            const uint32_t m = a.nq == 1 ? 0 : (uint32_t)(gg0 >> gbits);
+            const QPar& M = a.qp[m];
             q[0] = M.q[0]; q[1] = M.q[1]; q[2] = M.q[2]; q[3] = M.q[3];
             qinv0 = M.qinv0;
             if (SCALE_LAST) {
@@ -845,7 +872,7 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
                 if (!SINGLE && gbits == 0 && !a.fout) {
                     // the whole transform was this pass (four-step sub-transforms of 2^9 run the
                     // padded multi-pass kernel as their single pass): lazy classes -> canonical
-                    const ModC& M = a.mods[a.nq == 1 ? 0 : (uint32_t)poly];
+                    const QPar& M = a.qp[a.nq == 1 ? 0 : (uint32_t)poly];
                     const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
                     const int mode = mode_of(q);
                     if (mode == MODE_LAZY) {
@@ -872,7 +899,7 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
             for (int i = 0; i < PER; i++) outv[i] = smc[slot<B, PADL, RB>(lbase + (i << LT))];
             if (!SINGLE && lo + B == n && !a.fout) {
                 // lazy classes leave the last pass in [0, 4q) / [0, 2q): canonicalize
-                const ModC& M = a.mods[m_me];
+                const QPar& M = a.qp[a.nq == 1 ? 0 : (uint32_t)(gg0 >> gbits)];
                 const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
                 const int mode = mode_of(q);
                 if (mode == MODE_LAZY) {
@@ -1022,7 +1049,7 @@ template <int B, int C, bool INV, bool SCALE_LAST, int RBMAX>
 __global__ void __launch_bounds__(C * PassShape<B, RBMAX>::T,
                                   (PassOcc<B, RBMAX, false>::THREADS / (C * PassShape<B, RBMAX>::T)) > 0
                                       ? PassOcc<B, RBMAX, false>::THREADS / (C * PassShape<B, RBMAX>::T) : 1)
-k_nc_pass(const PassArgs a) {
+k_nc_pass(const __grid_constant__ PassArgs a) {
     using S = PassShape<B, RBMAX, C, true>;
     constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS, TS = S::TS;
     constexpr int NT = C * T;
@@ -1034,7 +1061,7 @@ k_nc_pass(const PassArgs a) {
     const uint64_t N = 1ull << n;
     const uint64_t gmask = (1ull << gbits) - 1;
     uint64_t gg0 = (uint64_t)blockIdx.x * C;
-    if (a.order) gg0 = ((uint64_t)a.order[gg0 >> gbits] << gbits) | (gg0 & gmask);
+    if (a.nq > 1) gg0 = ((uint64_t)a.ord[gg0 >> gbits] << gbits) | (gg0 & gmask);   // kernel-parameter table: uniform
     const int tid = threadIdx.x;
     constexpr int LT = B - RB;
     const int c_me = tid % C, t0 = tid / C;
@@ -1095,7 +1122,7 @@ k_nc_pass(const PassArgs a) {
         uint32_t q[4], qinv0;
         U128 nf;
         {
-            const ModC& M = a.mods[m_me];
+            const QPar& M = a.qp[m_me];   // kernel parameters, block-uniform index: uniform registers
             q[0] = M.q[0]; q[1] = M.q[1]; q[2] = M.q[2]; q[3] = M.q[3];
             qinv0 = M.qinv0;
             const uint32_t* src = a.ninv_r ? M.ninv_rm : M.ninv_m;
@@ -1117,7 +1144,7 @@ k_nc_pass(const PassArgs a) {
         // the transform's last pass returns canonical values (lazy classes are in [0, 4q) / [0, 2q))
         const bool last_pass = INV ? (lo + B == n) : (lo == 0);
         if (last_pass) {
-            const ModC& M = a.mods[m_me];
+            const QPar& M = a.qp[m_me];
             const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
             const int mode = mode_of(q);
             if (mode == MODE_LAZY && !INV) {
@@ -1276,6 +1303,7 @@ struct PassCfg {
     size_t smem;
     bool tma = false;     // k_ntt_pass<..., TMA>: the launch must carry the data tile's tensor map
     bool first = false;
+    bool single = false;  // one-pass kernel (several moduli per CTA: the device table, not QPar)
 };
 
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE = false, int RBMAX = 3, bool PM = false, bool TMA = false>
@@ -1288,6 +1316,7 @@ static PassCfg make_cfg() {
     c.threads = C * S::T;
     c.tma = TMA;
     c.first = FIRST;
+    c.single = SINGLE;
     const size_t ntw = (size_t)((FIRST && !SINGLE) ? 1 : C) * S::TS;
     c.smem = ((size_t)C * S::GS + ntw + (TMA ? 2 : 0)) * sizeof(uint4);   // TMA: + the pad slot, + two mbarriers
     return c;
@@ -1491,7 +1520,9 @@ struct ntt128_plan_s {
     std::vector<int> nc_bits;
     std::vector<uint4*> d_nc_fwd, d_nc_inv, d_nc_inv_r;
     std::vector<uint64_t> nc_stride;
-    uint32_t* d_order = nullptr;                         // [batch] CTA-slot -> polynomial (nq == batch)
+    // multi-pass launches carry their moduli as kernel parameters (QPar, <= NTT_QMAX per launch):
+    std::vector<QPar> qpar;                              // [nq] host copy of the per-modulus constants
+    std::vector<uint32_t> order;                         // [batch] polynomials grouped by class (nq == batch)
     std::vector<uint64_t> pt_stride;
     // Pass-overlap completion counters, one set per stream (keyed by cudaStreamGetId):
     // counters only grow; the host keeps, per counter row, the value the row reaches once
@@ -1537,7 +1568,6 @@ static void plan_free(ntt128_plan_s* p) {
     cudaFree(p->d_f_twist);
     cudaFree(p->d_f_untwist);
     cudaFree(p->d_f_untwist_r);
-    cudaFree(p->d_order);
     for (auto& kv : p->ctrs) {
         cudaFree(kv.second.d);
         cudaFree(kv.second.scratch);
@@ -1763,16 +1793,25 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
     }
     // polynomial order for multi-pass launches, grouped by arithmetic mode (q < 2^126,
     // q < 2^127, the rest) so one code path at a time is hot in the instruction cache
-    if (st == NTT128_OK && n_moduli > 1 && p->bits.size() > 1) {
-        std::vector<uint32_t> order;
+    if (st == NTT128_OK && n_moduli > 1) {
         for (int cls = 0; cls < 3; cls++)
             for (uint32_t m = 0; m < n_moduli; m++) {
                 const int c = (qs[m] >> 126) == 0 ? 0 : ((qs[m] >> 127) == 0 ? 1 : 2);
-                if (c == cls) order.push_back(m);
+                if (c == cls) p->order.push_back(m);
             }
-        if (cudaMalloc(&p->d_order, order.size() * sizeof(uint32_t)) != cudaSuccess) st = NTT128_ERR_OOM;
-        else if (cudaMemcpy(p->d_order, order.data(), order.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess)
-            st = NTT128_ERR_CUDA;
+    }
+    if (st == NTT128_OK) {
+        p->qpar.resize(n_moduli);
+        for (uint32_t m = 0; m < n_moduli; m++) {
+            QPar& d = p->qpar[m];
+            memset(&d, 0, sizeof(d));
+            for (int i = 0; i < 4; i++) {
+                d.q[i] = mc[m].q[i];
+                d.ninv_m[i] = mc[m].ninv_m[i];
+                d.ninv_rm[i] = mc[m].ninv_rm[i];
+            }
+            d.qinv0 = mc[m].qinv0;
+        }
     }
     // per-pass twiddle tables in consumption order (gathered from the power tables)
     if (st == NTT128_OK) {
@@ -1938,6 +1977,51 @@ static cudaError_t launch_pass(const PassCfg& c, const PassArgs& a, uint64_t cta
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, c.fn, a);
+}
+
+// Launch one pass with its moduli as kernel parameters (QPar table).  Multi-pass
+// kernels of an RNS plan with more than NTT_QMAX polynomials run as chunks of NTT_QMAX
+// polynomials, each a launch over its own slice of every per-polynomial array (data,
+// point-wise operand, completion counters) and per-modulus table (pass twiddles, factors,
+// device constants).  TMA passes encode the chunk's tensor map; `alt` is the same pass
+// without TMA, taken if the encode fails.
+static ntt128_status launch_pass_q(const ntt128_plan_s* p, const PassCfg& c, const PassCfg& alt, const PassArgs& a0,
+                                   int B, int lo, cudaStream_t stream, bool pdl) {
+    const int n = (int)a0.n;
+    const uint32_t nq = p->nq, batch = p->batch;
+    const bool chunked = !c.single && nq > 1 && batch > NTT_QMAX;
+    const uint32_t step = chunked ? NTT_QMAX : batch;
+    for (uint32_t b0 = 0; b0 < batch; b0 += step) {
+        const uint32_t nb = batch - b0 < step ? batch - b0 : step;
+        PassArgs a = a0;
+        if (nq == 1) {
+            a.qp[0] = p->qpar[0];
+        } else if (!c.single) {
+            a.nq = nb;
+            for (uint32_t i = 0; i < nb; i++) a.qp[i] = p->qpar[b0 + i];
+            uint32_t k = 0;
+            for (uint32_t m : p->order)
+                if (m >= b0 && m < b0 + nb) a.ord[k++] = (uint16_t)(m - b0);
+        }
+        if (b0) {   // chunked (nq == batch, natural layout: no four-step I/O)
+            a.src += (uint64_t)b0 * p->N;
+            a.dst += (uint64_t)b0 * p->N;
+            if (a.pmul) a.pmul += (uint64_t)b0 * p->N;
+            a.pt += (uint64_t)b0 * a.pt_stride;
+            a.mods += b0;
+            if (a.fin) a.fin += (uint64_t)b0 * a.f_stride;
+            if (a.fout) a.fout += (uint64_t)b0 * a.f_stride;
+            if (a.cnt_in) a.cnt_in += b0;
+            if (a.cnt_out) a.cnt_out += b0;
+        }
+        if (chunked) a.total_groups = (uint64_t)nb << (n - B);
+        const PassCfg* cc = &c;
+        if (c.tma && !tma_encode(a, c.first, n, B, lo, chunked ? nb : batch)) cc = &alt;   // per-thread cp.async tiles
+        const uint64_t ctas = (a.total_groups + cc->C - 1) / cc->C;
+        if (launch_pass(*cc, a, ctas, stream, pdl) != cudaSuccess) return NTT128_ERR_CUDA;
+        ntt128_count_launch(1);
+    }
+    return NTT128_OK;
 }
 
 // The stream's cache entry (created on first use; `lk` must hold p->mu).  Creating an entry
@@ -2246,7 +2330,6 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
         a.src = i == 0 ? src : dst;
         a.dst = dst;
         a.mods = p->d_mods;
-        a.order = p->d_order;
         a.pt_stride = p->pt_stride[i];
         a.f_stride = p->N;
         a.total_groups = (uint64_t)p->batch << (n - B);
@@ -2280,18 +2363,19 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
                 for (int h = 0; h < NTT128_FS_MAX_RANKS; h++) a.rdst[h] = o.io->rdst[h];
             }
         }
-        if (c.tma && (a.fin || a.pmul || a.in_ps != p->N || a.in_es != 1 ||
-                      !tma_encode(a, c.first, n, B, lo, p->batch)))
-            c = pass_cfg(npass, i, B, scale_last, lo, n, false);   // per-thread cp.async tiles
+        PassCfg alt = c;
+        if (c.tma) {
+            alt = pass_cfg(npass, i, B, scale_last, lo, n, false);
+            if (a.fin || a.pmul || a.in_ps != p->N || a.in_es != 1) c = alt;   // TMA passes read natural tiles only
+        }
         // CTAs that signal each polynomial's counter (a PM CTA signals all of its C polynomials)
         const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (pm ? 1u : (uint64_t)c.C));
         if (overlap) set_overlap(p, ctr, a, i, npass, prev_ctas_per_poly);
         if (i == 0 && wait_prev) chain_first(p, ctr, a);
         if (chain && last) chain_last(p, ctr, a, npass, ctas_per_poly, o, bufs);
         if (pdl_single) a.pdl_wait = 1u;
-        const uint64_t ctas = (a.total_groups + c.C - 1) / c.C;
-        if (launch_pass(c, a, ctas, stream, overlap || pdl_single) != cudaSuccess) return NTT128_ERR_CUDA;
-        ntt128_count_launch(1);
+        const ntt128_status ls = launch_pass_q(p, c, alt, a, B, lo, stream, overlap || pdl_single);
+        if (ls != NTT128_OK) return ls;
         lo += B;
         prev_ctas_per_poly = ctas_per_poly;
     }
@@ -2330,7 +2414,6 @@ static ntt128_status run_transform_nc(ntt128_plan_s* p, const uint4* src, uint4*
         a.src = i == 0 ? src : dst;
         a.dst = dst;
         a.mods = p->d_mods;
-        a.order = p->d_order;
         a.pt_stride = p->nc_stride[k];
         a.total_groups = (uint64_t)p->batch << (n - B);
         a.n = (uint32_t)n;
@@ -2343,9 +2426,8 @@ static ntt128_status run_transform_nc(ntt128_plan_s* p, const uint4* src, uint4*
         if (overlap) set_overlap(p, ctr, a, i, npass, prev_ctas_per_poly);
         if (i == 0 && wait_prev) chain_first(p, ctr, a);
         if (chain && i + 1 == npass) chain_last(p, ctr, a, npass, ctas_per_poly, go, bufs);
-        const uint64_t ctas = (a.total_groups + c.C - 1) / c.C;
-        if (launch_pass(c, a, ctas, stream, overlap) != cudaSuccess) return NTT128_ERR_CUDA;
-        ntt128_count_launch(1);
+        const ntt128_status ls = launch_pass_q(p, c, c, a, B, los[k], stream, overlap);
+        if (ls != NTT128_OK) return ls;
         prev_ctas_per_poly = ctas_per_poly;
     }
     return NTT128_OK;

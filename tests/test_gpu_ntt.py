@@ -236,6 +236,35 @@ def test_rns_many_primes_small_sizes(N, params, logn):
     assert np.array_equal(c, O.negacyclic_polymul(x, b, qs, psis))
 
 
+@pytest.mark.parametrize("logn,B", [(13, 80), (16, 136), (11, 72)])
+def test_rns_more_primes_than_one_launch(N, params, logn, B):
+    """more RNS polynomials than one launch's kernel-parameter moduli table (NTT_QMAX = 64):
+    multi-pass passes run as chunks of 64 polynomials, each with its own slice
+    of data, counters, twiddle tables and moduli; the moduli cycle through the 64 cfg3 primes
+    in a shifted order so every chunk mixes all three classes.  Cyclic forward / inverse,
+    negacyclic (natural and bit-reversed pipelines) and polymul against the oracle on
+    polynomials of every chunk, round trips on all."""
+    mods = params["cfg3"]["moduli"]
+    idx = [(7 * i + 3) % 64 for i in range(B)]
+    qs = [mods[k]["q"] for k in idx]
+    ws = [sub_root(mods[k], logn) for k in idx]
+    psis = [sub_root(mods[k], logn, negacyclic=True) for k in idx]
+    n = 1 << logn
+    x = np.stack([synth.uniform_residues(qs[i], n, 3000 * logn + i) for i in range(B)])
+    sel = sorted({0, 1, 63, 64, 65, B - 1} | ({127, 128} if B > 128 else set()))
+    plan = N.Plan(logn, qs, ws, batch=B)
+    y = to_host(plan.forward(to_dev(x)))
+    assert np.array_equal(y[sel], O.ntt(x[sel], [qs[i] for i in sel], [ws[i] for i in sel]))
+    assert np.array_equal(to_host(plan.inverse(to_dev(y))), x)
+    pn = N.Plan(logn, qs, psis, batch=B, negacyclic=True)
+    yn = to_host(pn.forward(to_dev(x)))
+    assert np.array_equal(yn[sel], O.negacyclic_ntt(x[sel], [qs[i] for i in sel], [psis[i] for i in sel]))
+    assert np.array_equal(to_host(pn.inverse(to_dev(yn))), x)
+    b = np.stack([synth.uniform_residues(qs[i], n, 4000 * logn + i) for i in range(B)])
+    c = to_host(pn.polymul(to_dev(x), to_dev(b)))
+    assert np.array_equal(c[sel], O.negacyclic_polymul(x[sel], b[sel], [qs[i] for i in sel], [psis[i] for i in sel]))
+
+
 @pytest.mark.parametrize("logn", [8, 9, 10, 11])
 def test_cluster_latency_path(N, params, logn):
     """up to 512 polynomials at N = 2^8 .. 2^11 run on 8-CTA clusters (distributed shared
