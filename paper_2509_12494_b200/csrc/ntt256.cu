@@ -115,6 +115,9 @@ inline uint4 h_lo4(const H256& v) { return make_uint4((uint32_t)v.w[0], (uint32_
 inline uint4 h_hi4(const H256& v) { return make_uint4((uint32_t)v.w[2], (uint32_t)(v.w[2] >> 32), (uint32_t)v.w[3], (uint32_t)(v.w[3] >> 32)); }
 
 // ----------------------------------------------------------------------------- device helpers
+#ifndef NTT256_SHIFT_SCALE
+#define NTT256_SHIFT_SCALE 1   // 0: the inverse's N^-1 on u by a Montgomery product (A/B)
+#endif
 struct ModC256 {
     uint32_t q[8];
     uint32_t qinv0;
@@ -137,6 +140,38 @@ __device__ __forceinline__ E256 mmul(const E256& a, const E256& b, const ModC256
     return r;
 }
 __device__ __forceinline__ uint32_t brev_n(uint32_t x, int bits) { return bits == 0 ? 0u : (__brev(x) >> (32 - bits)); }
+// u 2^-s mod q (1 <= s <= 31, u < q): one s-bit Montgomery digit, as shr_mod in arith128.cuh --
+// m = u_0 (-q^-1) mod 2^s, T = (u + m q) / 2^s < q + u / 2^s < 2q, one conditional subtraction
+// (T may reach bit 256: ninth word).  The inverse's last stage: u N^-1 = u 2^-n.
+__device__ __forceinline__ E256 shr256(const E256& u, uint32_t s, const ModC256& M) {
+    const uint32_t m = (u.w[0] * M.qinv0) & ((1u << s) - 1u);
+    uint32_t x[9];
+    uint64_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const uint64_t t = (uint64_t)m * M.q[i] + u.w[i] + c;   // < 2^64
+        x[i] = (uint32_t)t;
+        c = t >> 32;
+    }
+    x[8] = (uint32_t)c;
+    uint32_t t[9];
+#pragma unroll
+    for (int i = 0; i < 8; i++) t[i] = __funnelshift_r(x[i], x[i + 1], s);
+    t[8] = x[8] >> s;
+    uint32_t d[8];
+    int64_t bw = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const int64_t v = (int64_t)t[i] - (int64_t)M.q[i] + bw;
+        d[i] = (uint32_t)v;
+        bw = v >> 32;                                            // 0 or -1
+    }
+    const bool ge = ((int64_t)t[8] + bw) >= 0;                   // T >= q
+    E256 r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.w[i] = ge ? d[i] : t[i];
+    return r;
+}
 
 // out[m][i] = scale_m base_m^i (Montgomery form), i < count: product over the set bits of i
 __global__ void k_pow256(uint4* out, uint64_t stride, uint64_t count, const uint4* pow2, int K, const uint4* scale,
@@ -175,6 +210,7 @@ __global__ void k_gather256(uint4* out, uint64_t out_stride, const uint4* T, con
 }
 
 struct Pass256Args {
+    ModC256 mc0;              // nq == 1: the modulus as a kernel parameter (uniform registers in the rounds)
     const uint4* src;
     uint4* dst;
     const uint4* pt;          // [nq][pt_stride] 32-byte twiddles
@@ -199,7 +235,7 @@ struct Shape256 {
 
 template <int B, bool FIRST, bool SCALE_LAST>
 __global__ void __launch_bounds__(Shape256<B>::C * Shape256<B>::T)
-k_ntt256_pass(const Pass256Args a) {
+k_ntt256_pass(const __grid_constant__ Pass256Args a) {
     using S = Shape256<B>;
     constexpr int G = S::G, RB = S::RB, E = S::E, T = S::T, C = S::C, GP = S::GP;
     constexpr int ROUNDS = (B + RB - 1) / RB;
@@ -244,48 +280,54 @@ k_ntt256_pass(const Pass256Args a) {
         ghi[slot256(l)] = p[1];
     }
     __syncthreads();
-    const ModC256& M = a.mods[m];
-#pragma unroll 1
-    for (int rd = 0; rd < ROUNDS; rd++) {
-        const int slo = rd * RB;
-        const int w = (slo + RB <= B) ? slo : B - RB;
-        const int tlo = t & ((1 << w) - 1);
-        const int l0 = ((t >> w) << (w + RB)) | tlo;
-        E256 x[E];
-#pragma unroll
-        for (int k = 0; k < E; k++) {
-            const int s = slot256(l0 | (k << w));
-            x[k] = e_from(glo[s], ghi[s]);
-        }
-#pragma unroll
-        for (int bit = 0; bit < RB; bit++) {
-            const int sl = w + bit;
-            if (sl < slo) continue;
-            const bool last = SCALE_LAST && lo + sl == n - 1;
-            const bool trivial = FIRST && sl == 0 && !last;
-#pragma unroll
-            for (int kk = 0; kk < E / 2; kk++) {
-                const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
-                const int k1 = k0 | (1 << bit);
-                E256 v = x[k1], u = x[k0];
-                if (!trivial) {
-                    const int ti = (1 << sl) - 1 + tlo + ((kk & ((1 << bit) - 1)) << w);
-                    v = mmul(v, e_from(twl[ti], twh[ti]), M);
-                    if (last) u = mmul(u, E256{{M.ninv_m[0], M.ninv_m[1], M.ninv_m[2], M.ninv_m[3], M.ninv_m[4],
-                                                M.ninv_m[5], M.ninv_m[6], M.ninv_m[7]}}, M);
-                }
-                add_mod256(u.w, v.w, M.q, x[k0].w);
-                sub_mod256(u.w, v.w, M.q, x[k1].w);
+    // the rounds, instantiated once per source of the modulus: a kernel parameter (nq == 1:
+    // uniform registers, UR operands in the products) or the device table (lanes may differ)
+    auto rounds = [&](const ModC256& M) {
+    #pragma unroll 1
+        for (int rd = 0; rd < ROUNDS; rd++) {
+            const int slo = rd * RB;
+            const int w = (slo + RB <= B) ? slo : B - RB;
+            const int tlo = t & ((1 << w) - 1);
+            const int l0 = ((t >> w) << (w + RB)) | tlo;
+            E256 x[E];
+    #pragma unroll
+            for (int k = 0; k < E; k++) {
+                const int s = slot256(l0 | (k << w));
+                x[k] = e_from(glo[s], ghi[s]);
             }
+    #pragma unroll
+            for (int bit = 0; bit < RB; bit++) {
+                const int sl = w + bit;
+                if (sl < slo) continue;
+                const bool last = SCALE_LAST && lo + sl == n - 1;
+                const bool trivial = FIRST && sl == 0 && !last;
+    #pragma unroll
+                for (int kk = 0; kk < E / 2; kk++) {
+                    const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
+                    const int k1 = k0 | (1 << bit);
+                    E256 v = x[k1], u = x[k0];
+                    if (!trivial) {
+                        const int ti = (1 << sl) - 1 + tlo + ((kk & ((1 << bit) - 1)) << w);
+                        v = mmul(v, e_from(twl[ti], twh[ti]), M);
+                        if (last) u = (NTT256_SHIFT_SCALE && n >= 1) ? shr256(u, n, M)
+                                                                   : mmul(u, E256{{M.ninv_m[0], M.ninv_m[1], M.ninv_m[2], M.ninv_m[3], M.ninv_m[4],
+                                                                                    M.ninv_m[5], M.ninv_m[6], M.ninv_m[7]}}, M);
+                    }
+                    add_mod256(u.w, v.w, M.q, x[k0].w);
+                    sub_mod256(u.w, v.w, M.q, x[k1].w);
+                }
+            }
+    #pragma unroll
+            for (int k = 0; k < E; k++) {
+                const int s = slot256(l0 | (k << w));
+                glo[s] = e_lo(x[k]);
+                ghi[s] = e_hi(x[k]);
+            }
+            __syncthreads();
         }
-#pragma unroll
-        for (int k = 0; k < E; k++) {
-            const int s = slot256(l0 | (k << w));
-            glo[s] = e_lo(x[k]);
-            ghi[s] = e_hi(x[k]);
-        }
-        __syncthreads();
-    }
+    };
+    if (a.nq == 1) rounds(a.mc0);
+    else rounds(a.mods[m]);
     if (!live) return;
     // store: the first pass writes the group as contiguous rows (natural order within it)
     if (FIRST) {
@@ -366,6 +408,7 @@ struct ntt256_plan_s {
     uint64_t N;
     std::vector<int> bits;
     ModC256* d_mods = nullptr;
+    ModC256 mc0;                        // host copy of modulus 0 (nq == 1 launches carry it as a parameter)
     std::vector<uint4*> d_fwd, d_inv;   // per pass [nq][stride] 32-byte twiddles
     std::vector<uint64_t> stride;
 };
@@ -459,6 +502,7 @@ extern "C" ntt128_status ntt256_plan_create(ntt256_plan_t* out, uint32_t log2n, 
     ntt128_status st = NTT128_OK;
     std::vector<ModC256> mc;
     for (auto& q : qs) mc.push_back(make_modc(q, N));
+    p->mc0 = mc[0];
     if (cudaMalloc(&p->d_mods, n_moduli * sizeof(ModC256)) != cudaSuccess) st = NTT128_ERR_OOM;
     else if (cudaMemcpy(p->d_mods, mc.data(), n_moduli * sizeof(ModC256), cudaMemcpyHostToDevice) != cudaSuccess)
         st = NTT128_ERR_CUDA;
@@ -521,6 +565,7 @@ static ntt128_status run256(ntt256_plan_s* p, const uint4* src, uint4* dst, cuda
         a.dst = dst;
         a.pt = inverse ? p->d_inv[i] : p->d_fwd[i];
         a.mods = p->d_mods;
+        a.mc0 = p->mc0;
         a.pt_stride = p->stride[i];
         a.total_groups = (uint64_t)p->batch << (n - B);
         a.n = (uint32_t)n;
