@@ -760,16 +760,26 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
         uint4 stage[PER];
 #pragma unroll
         for (int i = 0; i < PER; i++) stage[i] = srcp[(size_t)i * sstride];
-        const ModC& M = a.mods[m_me];
-        const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+        // multi-pass: the modulus from the kernel parameters (block-uniform: one polynomial per
+        // CTA, or nq == 1 for the polynomial-major four-step CTAs); one-pass: the device table
+        auto factors = [&](const uint32_t* qs, uint32_t qinv0) {
+            const uint32_t q[4] = {qs[0], qs[1], qs[2], qs[3]};
 #pragma unroll
-        for (int i = 0; i < PER; i++) {
-            const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
-            const uint64_t idx = gbase + (size_t)i * gstride;
-            U128 x = u128_from(stage[i]);
-            if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + (a.fpoly ? poly_me * a.f_ps + idx * a.f_es : m_me * a.f_stride + idx))), q, M.qinv0);
-            if (a.pmul) x = mont_mul(x, u128_from(__ldg(a.pmul + poly_me * N + idx)), q, M.qinv0);
-            smc[slot<B, PADL, RB>(l)] = u128_to(x);
+            for (int i = 0; i < PER; i++) {
+                const int l = FIRST ? (lbase | (int)(brev_bits((uint32_t)i, RB))) : (lbase + (i << LT));
+                const uint64_t idx = gbase + (size_t)i * gstride;
+                U128 x = u128_from(stage[i]);
+                if (a.fin) x = mont_mul(x, u128_from(__ldg(a.fin + (a.fpoly ? poly_me * a.f_ps + idx * a.f_es : m_me * a.f_stride + idx))), q, qinv0);
+                if (a.pmul) x = mont_mul(x, u128_from(__ldg(a.pmul + poly_me * N + idx)), q, qinv0);
+                smc[slot<B, PADL, RB>(l)] = u128_to(x);
+            }
+        };
+        if (SINGLE) {
+            const ModC& M = a.mods[m_me];
+            factors(M.q, M.qinv0);
+        } else {
+            const QPar& M = a.qp[a.nq == 1 ? 0 : (uint32_t)(gg0 >> gbits)];
+            factors(M.q, M.qinv0);
         }
     }
     if (TMA) {
@@ -915,8 +925,8 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
             }
             if (live) {
                 uint4* dstp = a.dst + poly_me * N + gbase;
-                if (a.fout) {
-                    const ModC& M = a.mods[m_me];
+                if (a.fout) {   // !FIRST: a multi-pass kernel -- block-uniform modulus index
+                    const QPar& M = a.qp[a.nq == 1 ? 0 : (uint32_t)(gg0 >> gbits)];
                     const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
 #pragma unroll
                     for (int i = 0; i < PER; i++)
@@ -1109,7 +1119,7 @@ k_nc_pass(const __grid_constant__ PassArgs a) {
         const uint4* pm = a.pmul + poly * N + gbase;
 #pragma unroll
         for (int i = 0; i < PER; i++) { va[i] = __ldcg(srcp + (size_t)i * gstride); vb[i] = __ldcg(pm + (size_t)i * gstride); }
-        const ModC& M = a.mods[m_me];
+        const QPar& M = a.qp[m_me];   // kernel parameters, block-uniform index
         const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
 #pragma unroll
         for (int i = 0; i < PER; i++)
