@@ -1,7 +1,7 @@
 # round 2 evidence: smoke, default bench, reference arm, ncu launch list + full captures (cfg3 pass kernels, cfg5 four-step),
 # exported to CSV/text on the box (the .ncu-rep files exceed gpurun's 64 MiB return limit)
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/r2g; mkdir -p $O
+O=gpurun_out/${TAG:-r2g}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > $O/smi.csv 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log; tail -2 $O/smoke.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
@@ -16,3 +16,4 @@ python tools/exp_fourstep_prof.py > $O/fs_plain.log 2>&1 && timeout 900 ncu --se
 ncu -i /tmp/prof_fs.ncu-rep --page raw --csv > $O/prof_fs_raw.csv 2>&1
 ncu -i /tmp/prof_fs.ncu-rep --page details --csv > $O/prof_fs_details.csv 2>&1
 ls -la $O; du -sh $O
+timeout 2400 python -m pytest tests -m gpu -q --durations=5 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -4 $O/pytest_gpu.log
