@@ -79,6 +79,9 @@
 #ifndef NTT_OCC_THREADS
 #define NTT_OCC_THREADS 768   // resident threads per SM the radix-8 pass kernels are register-budgeted for
 #endif
+#ifndef NTT_CARVEOUT
+#define NTT_CARVEOUT -1       // >= 0: cudaFuncAttributePreferredSharedMemoryCarveout of the multi-pass kernels (experiment)
+#endif
 #ifndef NTT_OCC_THREADS_RB2
 #define NTT_OCC_THREADS_RB2 1024   // ... and the radix-4 multi-pass kernels
 #endif
@@ -1791,6 +1794,8 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
                     const PassCfg ct = pass_cfg(p->bits.size(), i, p->bits[i], sl == 1, lo_i, (int)log2n, tma == 1);
                     if (cudaFuncSetAttribute(ct.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess)
                         st = NTT128_ERR_CUDA;
+                    if (NTT_CARVEOUT >= 0)   // experiment: shared-memory carveout of the pass kernels
+                        cudaFuncSetAttribute(ct.fn, cudaFuncAttributePreferredSharedMemoryCarveout, NTT_CARVEOUT);
                 }
                 PassCfg c;
                 if (p->bits.size() == 1 && use_latency_shape(p->bits[i], batch)) {
