@@ -348,6 +348,8 @@ def run_gpu(args):
 
     rows = run_rows(args, P, pk, stream, rank, world) if args.rows else None
     cpu = cpu_baseline(P) if (rank == 0 and args.cpu_baseline) else None
+    if cpu is not None and args.rows:
+        cpu["rows"] = oracle_rows(P)
     if rank == 0:
         out = {
             "metric": "128-bit NTT butterflies/sec (N=2^16, fwd+inv, 64 RNS primes)",
@@ -573,17 +575,19 @@ def run_cfg5_fourstep(args, P, rank, world):
     (columns layout), timing = max over ranks.  Two transports: "nccl" (pass A stores into
     the send blocks, one NCCL all-to-all per direction) and "p2p" (pass A's
     last pass stores each block straight into its destination rank's symmetric-memory
-    receive buffer); a transport the box cannot provide is reported as *_unavailable."""
+    receive buffer); a transport the box cannot provide is reported as *_unavailable.  Third
+    row "_natural": the natural block layout (rank g holds x[g N/G, (g+1) N/G) in and y's
+    slice out; pack + unpack and two more all-to-alls per direction)."""
     import torch
     from paper_2509_12494_b200 import fourstep as FS
     import synth
     e = P["cfg5"]
     q, w = hexint(e["q"]), hexint(e["omega"])
     out = {"cfg5_fourstep_gpus": world, "cfg5_fourstep_split": list(FS.split(26))}
-    for transport in ("nccl", "p2p"):
-        tag = "cfg5_fourstep" if transport == "nccl" else "cfg5_fourstep_p2p"
+    for transport, layout in (("nccl", "transposed"), ("p2p", "transposed"), ("nccl", "natural")):
+        tag = {"nccl": "cfg5_fourstep", "p2p": "cfg5_fourstep_p2p"}[transport] + ("_natural" if layout == "natural" else "")
         try:
-            fs = FS.FourStep(26, q, w, rank, world, None, transport=transport)
+            fs = FS.FourStep(26, q, w, rank, world, None, transport=transport, layout=layout)
             ok = 1.0
         except Exception as ex:                      # e.g. no peer mappings on this box
             fs, ok = None, 0.0
@@ -593,18 +597,22 @@ def run_cfg5_fourstep(args, P, rank, world):
             continue
         L = fs.local
         cols = to_dev(synth.uniform_residues(q, L.R1 * L.n2, synth.stream_seed(5, 0, 100 + rank)).reshape(L.R1, L.n2, 2))
-        rows = torch.empty((L.R2, L.n1, 2), dtype=cols.dtype, device=cols.device)
+        if layout == "natural":   # this rank's contiguous slice of x (and of y)
+            cols = cols.reshape(L.R1 * L.n2, 2)
+            rows = torch.empty_like(cols)
+        else:
+            rows = torch.empty((L.R2, L.n1, 2), dtype=cols.dtype, device=cols.device)
         back = torch.empty_like(cols)
         for _ in range(2):
             fs.forward(cols, out=rows)
             fs.inverse(rows, out=back)
         torch.cuda.synchronize()
-        assert torch.equal(back, cols), f"cfg5 four-step ({transport}) round trip mismatch"
+        assert torch.equal(back, cols), f"cfg5 four-step ({transport}, {layout}) round trip mismatch"
         ms = timed_rank(lambda i: (fs.forward(cols, out=rows), fs.inverse(rows, out=back)), 5, world)
         bfly = 2 * (1 << 25) * 26
         out[f"{tag}_fwd_inv_ms"] = ms
         out[f"{tag}_butterflies_per_s"] = bfly / (ms * 1e-3)
-        if transport == "nccl":
+        if transport == "nccl" and layout == "transposed":
             out["cfg5_fourstep_a2a_bytes_per_rank_per_direction"] = 16 * L.R1 * L.R2 * (world - 1)
         del fs, cols, rows, back
         torch.cuda.empty_cache()
@@ -629,6 +637,41 @@ def cpu_baseline(P, npolys: int = 16):
     bfly = 2 * npolys * (n // 2) * P["cfg3"]["logn"]
     return {"value": bfly / dt, "unit": "butterflies/s", "cores": O.num_threads(), "kind": "oracle",
             "sample": f"forward+inverse of {npolys} of the 64 cfg3 polynomials (N=2^16), {dt:.2f} s wall"}
+
+
+def oracle_rows(P, cfg4_coeffs: int = 1 << 20):
+    """The oracle beside the other rows (SURVEY.md §8(d) "Oracle timing"), bounded: cfg1 and
+    cfg2 in full, cfg4 on `cfg4_coeffs` coefficients per size (2^20 instead of the survey's
+    2^23, to keep the default run within minutes), rates per second (extrapolation-free)."""
+    from oracle import oracle as O
+    import synth
+    rows = {"cores": O.num_threads()}
+    e = P["cfg1"]
+    q, w = hexint(e["q"]), hexint(e["omega"])
+    x = synth.uniform_residues(q, 1024, synth.stream_seed(1, 0, 0))
+    t0 = time.perf_counter()
+    for _ in range(20):
+        assert np.array_equal(O.intt(O.ntt(x, q, w), q, w), x)
+    rows["cfg1_n1024_fwd_inv_us"] = (time.perf_counter() - t0) / 20 * 1e6
+    q2, a2, n2 = hexint(P["cfg2"]["q"]), hexint(P["cfg2"]["a"]), P["cfg2"]["n"]
+    xv = synth.uniform_residues(q2, n2, synth.stream_seed(2, 0, 0))
+    yv = synth.uniform_residues(q2, n2, synth.stream_seed(2, 1, 0))
+    for name, fn in (("add", lambda: O.vadd(xv, yv, q2)), ("sub", lambda: O.vsub(xv, yv, q2)),
+                     ("mul", lambda: O.vmul(xv, yv, q2)), ("axpy", lambda: O.axpy(a2, xv, yv, q2))):
+        t0 = time.perf_counter()
+        fn()
+        rows[f"cfg2_{name}_elem_per_s"] = n2 / (time.perf_counter() - t0)
+    for logn in range(10, 18):
+        e = P["cfg4"][str(logn)]
+        q, w = hexint(e["q"]), hexint(e["omega"])
+        B = max(1, cfg4_coeffs >> logn)
+        x = synth.uniform_residues(q, B << logn, synth.stream_seed(4, 0, logn)).reshape(B, 1 << logn, 2)
+        t0 = time.perf_counter()
+        assert np.array_equal(O.intt(O.ntt(x, q, w), q, w), x)
+        rows[f"cfg4_logn{logn}_butterflies_per_s"] = 2 * B * (1 << (logn - 1)) * logn / (time.perf_counter() - t0)
+    rows["sample"] = (f"cfg1 x20, cfg2 full (n=2^20), cfg4 {cfg4_coeffs} coefficients per size; cfg5 not timed "
+                      "(the oracle's 2^26 radix-2 transform takes minutes)")
+    return rows
 
 
 def run_reference(args):

@@ -176,7 +176,8 @@ ntt128_status vec128_axpy(uint64_t *d_y, const uint64_t *a, const uint64_t *d_x,
 typedef struct ntt128_fourstep_s *ntt128_fourstep_t;
 
 /* log2n1, log2n2 >= 1, log2n1 + log2n2 <= 26; q, omega: host {lo, hi}, omega of exact order
- * N = 2^(log2n1 + log2n2); world G a power of two <= 8 dividing both n1 and n2; 0 <= rank < world.
+ * N = 2^(log2n1 + log2n2); world G a power of two <= 8 with 2 G <= n1 and 2 G <= n2 when
+ * G > 1 (exchange blocks at least 2 residues wide); 0 <= rank < world.
  * Builds the sub-plans and the rank's twiddle-factor tables ([R2][n1] forward, [R1][n2]
  * inverse: 2 N/G residues) on `device`. */
 ntt128_status ntt128_fourstep_create(ntt128_fourstep_t *out, uint32_t log2n1, uint32_t log2n2, const uint64_t *q,
@@ -207,6 +208,38 @@ ntt128_status ntt128_fourstep_forward_a_peers(const ntt128_fourstep_t fs, const 
                                               const uint64_t *const *peers, ntt128_stream_t stream);
 ntt128_status ntt128_fourstep_inverse_a_peers(const ntt128_fourstep_t fs, const uint64_t *d_rows,
                                               const uint64_t *const *peers, ntt128_stream_t stream);
+/* Natural block layout ("rank g holds a contiguous N/G slice", a mode
+ * costing one more exchange at each end).  Rank g holds x[g N/G + i] and, after the
+ * forward, y[g N/G + i], i < N/G.  A direction is: pack -> exchange -> *_a_nat ->
+ * exchange -> *_c_nat -> exchange -> unpack, every exchange an all-to-all of equal
+ * blocks (block h -> rank h).  Same arithmetic as the transposed layouts above; pack and
+ * unpack are data movement only (one HBM read + write of the slice each).
+ *   forward_pack:   x slice [R2][G][R1] (j2 = g R2 + a, j1 = h R1 + r) -> send [G][R2][R1]
+ *   forward_a_nat:  recv [G][R2][R1] (= [n2][R1], X_g[r][j2] = recv[j2 R1 + r]) -> send [G][R1][R2]
+ *   forward_c_nat:  recv [G][R1][R2] (as forward_c) -> send [G][R2][R1], block h = k1 in [h R1, (h+1) R1)
+ *   forward_unpack: recv [G][R2][R1] (= [n2][R1]) -> y slice [R1][n2] (k1 = g R1 + b)
+ *   inverse_pack:   y slice [R1][G][R2] -> send [G][R1][R2]
+ *   inverse_a_nat:  recv [G][R1][R2] (= [n1][R2], Y_g[r][k1] = recv[k1 R2 + r]) -> send [G][R2][R1]
+ *   inverse_c_nat:  recv [G][R2][R1] (as inverse_c) -> send [G][R1][R2], block h = j2 in [h R2, (h+1) R2)
+ *   inverse_unpack: recv [G][R1][R2] (= [n1][R2]) -> x slice [R2][n1]
+ * Input and output must not alias (NTT128_ERR_INVALID_ARG); 16-byte aligned device
+ * buffers of N/G residues each; the *_nat passes use the object's working buffer. */
+ntt128_status ntt128_fourstep_forward_pack(const ntt128_fourstep_t fs, const uint64_t *d_nat, uint64_t *d_send,
+                                           ntt128_stream_t stream);
+ntt128_status ntt128_fourstep_forward_a_nat(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_send,
+                                            ntt128_stream_t stream);
+ntt128_status ntt128_fourstep_forward_c_nat(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_send,
+                                            ntt128_stream_t stream);
+ntt128_status ntt128_fourstep_forward_unpack(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_nat,
+                                             ntt128_stream_t stream);
+ntt128_status ntt128_fourstep_inverse_pack(const ntt128_fourstep_t fs, const uint64_t *d_nat, uint64_t *d_send,
+                                           ntt128_stream_t stream);
+ntt128_status ntt128_fourstep_inverse_a_nat(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_send,
+                                            ntt128_stream_t stream);
+ntt128_status ntt128_fourstep_inverse_c_nat(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_send,
+                                            ntt128_stream_t stream);
+ntt128_status ntt128_fourstep_inverse_unpack(const ntt128_fourstep_t fs, const uint64_t *d_recv, uint64_t *d_nat,
+                                             ntt128_stream_t stream);
 void ntt128_fourstep_destroy(ntt128_fourstep_t fs);
 
 /* ---------------------------------------------------------------------------

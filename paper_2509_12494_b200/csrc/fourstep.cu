@@ -66,6 +66,36 @@ inline uint4 to4(u128 v) {
     return make_uint4((uint32_t)v, (uint32_t)(v >> 32), (uint32_t)(v >> 64), (uint32_t)(v >> 96));
 }
 
+// ---- natural block layout (SURVEY.md §8(e) "natural block layout ... +2 all-to-alls"):
+// pure data movement around the exchanges, no arithmetic.
+// Pack before an exchange: out[g][a][r] = in[a][g][r] (in [A][G][R], out [G][A][R]); runs of R
+// residues are contiguous on both sides, so a warp moves 512 contiguous bytes per access.
+__global__ void k_fs_pack(uint4* __restrict__ out, const uint4* __restrict__ in, uint64_t A, uint32_t G, uint64_t R) {
+    const uint64_t total = A * G * R, AR = A * R;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = i / AR, rem = i - g * AR, a = rem / R, r = rem - a * R;
+        out[i] = __ldcs(in + (a * G + g) * R + r);   // streamed: each residue is read once
+    }
+}
+
+// Unpack after an exchange: out[k][m] = in[m][k] (in [M][K], out [K][M]), 32 x 32 tiles of
+// 16-byte residues through shared memory (row pitch 33: conflict-free column reads).
+constexpr int FS_TT = 32;
+__global__ void __launch_bounds__(FS_TT * 8) k_fs_transpose(uint4* __restrict__ out, const uint4* __restrict__ in,
+                                                            uint64_t M, uint64_t K) {
+    __shared__ uint4 tile[FS_TT][FS_TT + 1];
+    const uint64_t tiles_k = (K + FS_TT - 1) / FS_TT;
+    const uint64_t m0 = (blockIdx.x / tiles_k) * FS_TT, k0 = (blockIdx.x % tiles_k) * FS_TT;
+    const int tx = threadIdx.x % FS_TT, ty = threadIdx.x / FS_TT;   // 8 rows of 32 lanes
+#pragma unroll
+    for (int j = ty; j < FS_TT; j += 8)
+        if (m0 + j < M && k0 + tx < K) tile[j][tx] = __ldcs(in + (m0 + j) * K + k0 + tx);
+    __syncthreads();
+#pragma unroll
+    for (int j = ty; j < FS_TT; j += 8)
+        if (k0 + j < K && m0 + tx < M) out[(k0 + j) * M + m0 + tx] = tile[tx][j];
+}
+
 }  // namespace
 
 struct ntt128_fourstep_s {
@@ -128,7 +158,9 @@ extern "C" ntt128_status ntt128_fourstep_create(ntt128_fourstep_t* out, uint32_t
     if (log2n1 < 1 || log2n2 < 1 || log2n1 + log2n2 > 26) return NTT128_ERR_INVALID_ARG;
     if (world == 0 || (world & (world - 1)) || rank >= world || world > NTT128_FS_MAX_RANKS) return NTT128_ERR_INVALID_ARG;
     const uint64_t n1 = 1ull << log2n1, n2 = 1ull << log2n2, N = n1 * n2;
-    if (world > n1 || world > n2) return NTT128_ERR_INVALID_ARG;
+    // every exchange block is at least 2 residues wide (a transform's destination-block
+    // store keys on log2 of the block width, which must be >= 1)
+    if (world > 1 && (2 * world > n1 || 2 * world > n2)) return NTT128_ERR_INVALID_ARG;
     const u128 q = ntt128h::make(q_[0], q_[1]), w = ntt128h::make(omega_[0], omega_[1]);
     if ((q & 1) == 0 || q < 3) return NTT128_ERR_MODULUS;
     if (!ntt128h::is_probable_prime(q)) return NTT128_ERR_NOT_PRIME;
@@ -271,6 +303,144 @@ static ntt128_status a_peers(const ntt128_fourstep_s* f, const uint64_t* d_in, c
     }
     return inverse ? pass_a(f, f->p1i, false, d_in, bases, f->R1, f->n1, st)
                    : pass_a(f, f->p2, false, d_in, bases, f->R2, f->n2, st);
+}
+
+// ---------------------------------------------------------------- natural block layout
+// (include/ntt128.h "Natural block layout").  Rank g holds x[g N/G + i], i < N/G: viewed as
+// [R2][n1] (j2 = g R2 + a) for the input, [R1][n2] (k1 = g R1 + b) for the output.  Each
+// direction is pack -> exchange -> pass A (reading the received matrix's columns) ->
+// exchange -> pass C (last pass into the blocks of the natural owners) -> exchange ->
+// unpack: the transposed layouts' one exchange plus one at each end.
+namespace {
+
+ntt128_status launch_pack(const ntt128_fourstep_s* f, const uint64_t* d_in, uint64_t* d_out, uint64_t A, uint64_t R,
+                          cudaStream_t st) {
+    if (!f || !d_in || !d_out) return NTT128_ERR_INVALID_ARG;
+    if (!al16(d_in) || !al16(d_out)) return NTT128_ERR_ALIGNMENT;
+    if (d_in == d_out) return NTT128_ERR_INVALID_ARG;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(f->device);
+    const uint64_t total = A * f->world * R;
+    const uint64_t blocks = (total + 255) / 256 < 148ull * 16 ? (total + 255) / 256 : 148ull * 16;
+    k_fs_pack<<<(unsigned)blocks, 256, 0, st>>>((uint4*)d_out, (const uint4*)d_in, A, f->world, R);
+    ntt128_count_launch(1);
+    const cudaError_t e = cudaGetLastError();
+    cudaSetDevice(prev);
+    return e == cudaSuccess ? NTT128_OK : NTT128_ERR_CUDA;
+}
+
+ntt128_status launch_unpack(const ntt128_fourstep_s* f, const uint64_t* d_in, uint64_t* d_out, uint64_t M, uint64_t K,
+                            cudaStream_t st) {
+    if (!f || !d_in || !d_out) return NTT128_ERR_INVALID_ARG;
+    if (!al16(d_in) || !al16(d_out)) return NTT128_ERR_ALIGNMENT;
+    if (d_in == d_out) return NTT128_ERR_INVALID_ARG;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(f->device);
+    const uint64_t tiles = ((M + FS_TT - 1) / FS_TT) * ((K + FS_TT - 1) / FS_TT);
+    k_fs_transpose<<<(unsigned)tiles, FS_TT * 8, 0, st>>>((uint4*)d_out, (const uint4*)d_in, M, K);
+    ntt128_count_launch(1);
+    const cudaError_t e = cudaGetLastError();
+    cudaSetDevice(prev);
+    return e == cudaSuccess ? NTT128_OK : NTT128_ERR_CUDA;
+}
+
+// pass A over the columns of a received [n_sub][R] matrix (element stride R), last pass into
+// the send blocks [G][R][n_sub/G]
+ntt128_status pass_a_nat(const ntt128_fourstep_s* f, ntt128_plan_t plan, const uint64_t* d_recv, uint64_t* d_send,
+                         uint64_t R, uint64_t n_sub, cudaStream_t st) {
+    if (!f || !d_recv || !d_send) return NTT128_ERR_INVALID_ARG;
+    if (!al16(d_recv) || !al16(d_send)) return NTT128_ERR_ALIGNMENT;
+    if (d_recv == d_send) return NTT128_ERR_INVALID_ARG;
+    Ntt128IO io;
+    io.tmp = f->d_tmp;
+    io.in_ps = 1;
+    io.in_es = R;
+    uint32_t lb = 0;
+    while ((1ull << lb) < n_sub / f->world) lb++;
+    io.r_lb = lb;
+    io.r_ps = n_sub / f->world;
+    for (uint32_t h = 0; h < f->world; h++) io.rdst[h] = (uint4*)d_send + (uint64_t)h * R * (n_sub / f->world);
+    if (f->world == 1) io.r_lb = 0;   // one rank: the block is the whole output row
+    return ntt128_transform_io(plan, (const uint4*)d_recv, f->world == 1 ? (uint4*)d_send : nullptr, st, false, io);
+}
+
+// pass C (four-step factor at the load, as ntt128_fourstep_*_c) whose last pass stores output
+// k of local polynomial p into block k / (n_out/G) of the send buffer [G][R][n_out/G] --
+// the natural owner of k
+ntt128_status pass_c_nat(const ntt128_fourstep_s* f, ntt128_plan_t plan, const uint64_t* d_recv, uint64_t* d_send,
+                         uint64_t R_in, const uint4* fac, uint64_t R, uint64_t n_out, cudaStream_t st) {
+    if (!f || !d_recv || !d_send) return NTT128_ERR_INVALID_ARG;
+    if (!al16(d_recv) || !al16(d_send)) return NTT128_ERR_ALIGNMENT;
+    if (d_recv == d_send) return NTT128_ERR_INVALID_ARG;
+    Ntt128IO io;
+    io.tmp = f->d_tmp;
+    io.in_ps = 1;
+    io.in_es = R_in;
+    io.fin = fac;
+    io.fin_ps = 1;
+    io.fin_es = R_in;
+    if (f->world > 1) {
+        uint32_t lb = 0;
+        while ((1ull << lb) < n_out / f->world) lb++;
+        io.r_lb = lb;
+        io.r_ps = n_out / f->world;
+        for (uint32_t h = 0; h < f->world; h++) io.rdst[h] = (uint4*)d_send + (uint64_t)h * R * (n_out / f->world);
+    }
+    return ntt128_transform_io(plan, (const uint4*)d_recv, f->world > 1 ? nullptr : (uint4*)d_send, st, false, io);
+}
+
+}  // namespace
+
+extern "C" ntt128_status ntt128_fourstep_forward_pack(const ntt128_fourstep_t f, const uint64_t* d_nat, uint64_t* d_send,
+                                                      ntt128_stream_t s) {
+    // x slice [R2][G][R1] -> send [G][R2][R1]: block g = the columns j1 rank g transforms
+    return f ? launch_pack(f, d_nat, d_send, f->R2, f->R1, (cudaStream_t)s) : NTT128_ERR_INVALID_ARG;
+}
+
+extern "C" ntt128_status ntt128_fourstep_forward_a_nat(const ntt128_fourstep_t f, const uint64_t* d_recv, uint64_t* d_send,
+                                                       ntt128_stream_t s) {
+    // recv [G][R2][R1] = [n2][R1]: X_g[r][j2] = recv[j2 R1 + r] -> send [G][R1][R2] (as forward_a)
+    return f ? pass_a_nat(f, f->p2, d_recv, d_send, f->R1, f->n2, (cudaStream_t)s) : NTT128_ERR_INVALID_ARG;
+}
+
+extern "C" ntt128_status ntt128_fourstep_forward_c_nat(const ntt128_fourstep_t f, const uint64_t* d_recv, uint64_t* d_send,
+                                                       ntt128_stream_t s) {
+    // recv [G][R1][R2] (as forward_c) -> send [G][R2][R1]: block h = the k1 in [h R1, (h+1) R1)
+    return f ? pass_c_nat(f, f->p1, d_recv, d_send, f->R2, f->d_ff, f->R2, f->n1, (cudaStream_t)s)
+             : NTT128_ERR_INVALID_ARG;
+}
+
+extern "C" ntt128_status ntt128_fourstep_forward_unpack(const ntt128_fourstep_t f, const uint64_t* d_recv, uint64_t* d_nat,
+                                                        ntt128_stream_t s) {
+    // recv [G][R2][R1] = [n2][R1] (k2, k1 - g R1) -> y slice [R1][n2]
+    return f ? launch_unpack(f, d_recv, d_nat, f->n2, f->R1, (cudaStream_t)s) : NTT128_ERR_INVALID_ARG;
+}
+
+extern "C" ntt128_status ntt128_fourstep_inverse_pack(const ntt128_fourstep_t f, const uint64_t* d_nat, uint64_t* d_send,
+                                                      ntt128_stream_t s) {
+    // y slice [R1][G][R2] -> send [G][R1][R2]: block g = the k2 rank g holds in the rows layout
+    return f ? launch_pack(f, d_nat, d_send, f->R1, f->R2, (cudaStream_t)s) : NTT128_ERR_INVALID_ARG;
+}
+
+extern "C" ntt128_status ntt128_fourstep_inverse_a_nat(const ntt128_fourstep_t f, const uint64_t* d_recv, uint64_t* d_send,
+                                                       ntt128_stream_t s) {
+    // recv [G][R1][R2] = [n1][R2]: Y_g[r][k1] = recv[k1 R2 + r] -> send [G][R2][R1] (as inverse_a)
+    return f ? pass_a_nat(f, f->p1i, d_recv, d_send, f->R2, f->n1, (cudaStream_t)s) : NTT128_ERR_INVALID_ARG;
+}
+
+extern "C" ntt128_status ntt128_fourstep_inverse_c_nat(const ntt128_fourstep_t f, const uint64_t* d_recv, uint64_t* d_send,
+                                                       ntt128_stream_t s) {
+    // recv [G][R2][R1] (as inverse_c) -> send [G][R1][R2]: block h = the j2 in [h R2, (h+1) R2)
+    return f ? pass_c_nat(f, f->p2i, d_recv, d_send, f->R1, f->d_fi, f->R1, f->n2, (cudaStream_t)s)
+             : NTT128_ERR_INVALID_ARG;
+}
+
+extern "C" ntt128_status ntt128_fourstep_inverse_unpack(const ntt128_fourstep_t f, const uint64_t* d_recv, uint64_t* d_nat,
+                                                        ntt128_stream_t s) {
+    // recv [G][R1][R2] = [n1][R2] (j1, j2 - g R2) -> x slice [R2][n1]
+    return f ? launch_unpack(f, d_recv, d_nat, f->n1, f->R2, (cudaStream_t)s) : NTT128_ERR_INVALID_ARG;
 }
 
 extern "C" ntt128_status ntt128_fourstep_forward_a_peers(const ntt128_fourstep_t f, const uint64_t* d_cols,

@@ -28,7 +28,9 @@ _L.ntt128_fourstep_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_uint32, ctyp
                                       ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int]
 _L.ntt128_fourstep_create.restype = ctypes.c_int
 for _name in ("ntt128_fourstep_forward_a", "ntt128_fourstep_forward_c", "ntt128_fourstep_inverse_a",
-              "ntt128_fourstep_inverse_c"):
+              "ntt128_fourstep_inverse_c", "ntt128_fourstep_forward_pack", "ntt128_fourstep_forward_a_nat",
+              "ntt128_fourstep_forward_c_nat", "ntt128_fourstep_forward_unpack", "ntt128_fourstep_inverse_pack",
+              "ntt128_fourstep_inverse_a_nat", "ntt128_fourstep_inverse_c_nat", "ntt128_fourstep_inverse_unpack"):
     getattr(_L, _name).argtypes = [_vp, _vp, _vp, _vp]
     getattr(_L, _name).restype = ctypes.c_int
 for _name in ("ntt128_fourstep_forward_a_peers", "ntt128_fourstep_inverse_a_peers"):
@@ -108,6 +110,32 @@ class FourStepLocal:
     def inverse_c(self, recv, cols):
         return self._call("ntt128_fourstep_inverse_c", recv, cols)
 
+    # natural block layout (include/ntt128.h "Natural block layout"): rank g holds the
+    # contiguous slice [g N/G, (g+1) N/G) of x (forward input) and of y (forward output)
+    def forward_pack(self, nat, send):
+        return self._call("ntt128_fourstep_forward_pack", nat, send)
+
+    def forward_a_nat(self, recv, send):
+        return self._call("ntt128_fourstep_forward_a_nat", recv, send)
+
+    def forward_c_nat(self, recv, send):
+        return self._call("ntt128_fourstep_forward_c_nat", recv, send)
+
+    def forward_unpack(self, recv, nat):
+        return self._call("ntt128_fourstep_forward_unpack", recv, nat)
+
+    def inverse_pack(self, nat, send):
+        return self._call("ntt128_fourstep_inverse_pack", nat, send)
+
+    def inverse_a_nat(self, recv, send):
+        return self._call("ntt128_fourstep_inverse_a_nat", recv, send)
+
+    def inverse_c_nat(self, recv, send):
+        return self._call("ntt128_fourstep_inverse_c_nat", recv, send)
+
+    def inverse_unpack(self, recv, nat):
+        return self._call("ntt128_fourstep_inverse_unpack", recv, nat)
+
     def _call_peers(self, name, a, peer_ptrs):
         if len(peer_ptrs) != self.world:
             raise ValueError(f"{name}: need {self.world} peer pointers, got {len(peer_ptrs)}")
@@ -153,16 +181,26 @@ class FourStep:
     and pass A's pack kernel stores every block straight into its destination rank's
     receive buffer; two device-side barriers order the writes (before: every peer has
     finished reading its buffer; after: every block has landed).  No collective moves data.
+
+    layout="transposed" (default): forward takes the columns layout X_g[R1][n2] and returns
+    the rows layout Y_g[R2][n1] (one exchange per direction).  layout="natural" (SURVEY.md
+    §8(e)): rank g passes and receives the contiguous slice [g N/G, (g+1) N/G) of x / y as
+    [N/G][2]; one more all-to-all at each end (pack -> exchange -> pass A -> exchange ->
+    pass C -> exchange -> unpack; include/ntt128.h "Natural block layout").
     """
 
     def __init__(self, log2n: int, q: int, omega: int, rank: int = 0, world: int = 1, group=None,
-                 device: int | None = None, local=None, transport: str = "nccl"):
+                 device: int | None = None, local=None, transport: str = "nccl", layout: str = "transposed"):
         # `local` is injectable so the exchange schedule can be exercised by CPU tests (gloo)
-        self.local = local if local is not None else FourStepLocal(log2n, q, omega, rank, world, device)
-        self.group, self.world = group, world
         if transport not in ("nccl", "p2p"):
             raise ValueError(f"transport must be 'nccl' or 'p2p', not {transport!r}")
-        self.transport = transport
+        if layout not in ("transposed", "natural"):
+            raise ValueError(f"layout must be 'transposed' or 'natural', not {layout!r}")
+        if layout == "natural" and transport != "nccl":
+            raise ValueError("the natural block layout exchanges by all-to-all (transport='nccl')")
+        self.local = local if local is not None else FourStepLocal(log2n, q, omega, rank, world, device)
+        self.group, self.world = group, world
+        self.transport, self.layout = transport, layout
         self._recv = self._hdl = None
         if transport == "p2p":
             self._setup_p2p()
@@ -186,9 +224,25 @@ class FourStep:
         if self._hdl is not None:
             self._hdl.barrier(channel=0, timeout_ms=30000)   # device-side, stream-ordered; errors instead of hanging
 
+    def _natural(self, nat, out, pack, pass_a, pass_c, unpack, blocks):
+        """pack -> exchange -> pass A -> exchange -> pass C -> exchange -> unpack; blocks =
+        the [rows][cols] shape of one exchange block after pack, pass A and pass C"""
+        import torch
+        out = torch.empty_like(nat) if out is None else out
+        cur = nat
+        for step, shp in zip((pack, pass_a, pass_c), blocks):
+            send = torch.empty((self.world, *shp, 2), dtype=nat.dtype, device=nat.device)
+            step(cur, send)
+            cur = exchange(send, self.group, self.world)
+        unpack(cur, out)
+        return out
+
     def forward(self, cols, out=None):
         import torch
         L = self.local
+        if self.layout == "natural":   # cols: this rank's slice of x, [N/G][2]
+            return self._natural(cols, out, L.forward_pack, L.forward_a_nat, L.forward_c_nat, L.forward_unpack,
+                                 ((L.R2, L.R1), (L.R1, L.R2), (L.R2, L.R1)))
         out = torch.empty((L.R2, L.n1, 2), dtype=cols.dtype, device=cols.device) if out is None else out
         if self.transport == "p2p":
             self._barrier()
@@ -203,6 +257,9 @@ class FourStep:
     def inverse(self, rows, out=None):
         import torch
         L = self.local
+        if self.layout == "natural":   # rows: this rank's slice of y, [N/G][2]
+            return self._natural(rows, out, L.inverse_pack, L.inverse_a_nat, L.inverse_c_nat, L.inverse_unpack,
+                                 ((L.R1, L.R2), (L.R2, L.R1), (L.R1, L.R2)))
         out = torch.empty((L.R1, L.n2, 2), dtype=rows.dtype, device=rows.device) if out is None else out
         if self.transport == "p2p":
             self._barrier()

@@ -69,7 +69,10 @@ EXPORTED = ("ntt128_plan_create", "ntt128_forward", "ntt128_inverse", "ntt128_fo
             "ntt128_plan_destroy", "vec128_add", "vec128_sub", "vec128_mul", "vec128_axpy",
             "ntt128_status_string", "ntt128_launch_count", "ntt128_fourstep_create", "ntt128_fourstep_forward_a",
             "ntt128_fourstep_forward_c", "ntt128_fourstep_inverse_a", "ntt128_fourstep_inverse_c",
-            "ntt128_fourstep_forward_a_peers", "ntt128_fourstep_inverse_a_peers", "ntt128_fourstep_destroy",
+            "ntt128_fourstep_forward_a_peers", "ntt128_fourstep_inverse_a_peers", "ntt128_fourstep_forward_pack",
+            "ntt128_fourstep_forward_a_nat", "ntt128_fourstep_forward_c_nat", "ntt128_fourstep_forward_unpack",
+            "ntt128_fourstep_inverse_pack", "ntt128_fourstep_inverse_a_nat", "ntt128_fourstep_inverse_c_nat",
+            "ntt128_fourstep_inverse_unpack", "ntt128_fourstep_destroy",
             "ntt256_plan_create", "ntt256_forward", "ntt256_inverse", "ntt256_plan_destroy", "vec256_mul")
 
 

@@ -25,7 +25,7 @@ def declared_functions():
 
 def test_exports_every_declared_symbol(N):
     names = declared_functions()
-    assert len(names) == 27, names
+    assert len(names) == 35, names
     lib = ctypes.CDLL(N.LIB_PATH)
     for name in names:
         assert hasattr(lib, name), name
@@ -83,6 +83,7 @@ def test_fourstep_validation_host_only(N, params):
     assert f(C.byref(h), 13, 13, N._pairs([q]), N._pairs([w]), 0, 3, 0) == 1     # world not a power of two
     assert f(C.byref(h), 13, 13, N._pairs([q]), N._pairs([w]), 2, 2, 0) == 1     # rank >= world
     assert f(C.byref(h), 2, 2, N._pairs([q]), N._pairs([w]), 0, 8, 0) == 1      # world > n1
+    assert f(C.byref(h), 3, 9, N._pairs([q]), N._pairs([w]), 0, 8, 0) == 1      # blocks of width n1 / G = 1
     assert f(C.byref(h), 13, 13, N._pairs([q + 1]), N._pairs([w]), 0, 1, 0) == 2  # even modulus
     assert f(C.byref(h), 13, 13, N._pairs([q]), N._pairs([w * w % q]), 0, 1, 0) == 5  # order N/2
 

@@ -66,6 +66,39 @@ class OracleLocal:
         return cols
 
 
+    # natural block layout (include/ntt128.h "Natural block layout"): data movement around the
+    # same passes, written here with numpy transposes
+    def _tr(self, t, R, C):
+        """[R][C] (flat t) -> [C][R]"""
+        return np.ascontiguousarray(_n(t).reshape(R, C, 2).transpose(1, 0, 2))
+
+    def forward_pack(self, nat, send):
+        send.copy_(_t(self._blocks(_n(nat).reshape(self.R2, self.n1, 2), self.R2, self.n1)))
+
+    def forward_a_nat(self, recv, send):
+        self.forward_a(_t(self._tr(recv, self.n2, self.R1)), send)
+
+    def forward_c_nat(self, recv, send):
+        rows = self.forward_c(recv, torch.empty((self.R2, self.n1, 2), dtype=torch.int64))
+        send.copy_(_t(self._blocks(_n(rows), self.R2, self.n1)))
+
+    def forward_unpack(self, recv, nat):
+        nat.copy_(_t(self._tr(recv, self.n2, self.R1).reshape(-1, 2)))
+
+    def inverse_pack(self, nat, send):
+        send.copy_(_t(self._blocks(_n(nat).reshape(self.R1, self.n2, 2), self.R1, self.n2)))
+
+    def inverse_a_nat(self, recv, send):
+        self.inverse_a(_t(self._tr(recv, self.n1, self.R2)), send)
+
+    def inverse_c_nat(self, recv, send):
+        cols = self.inverse_c(recv, torch.empty((self.R1, self.n2, 2), dtype=torch.int64))
+        send.copy_(_t(self._blocks(_n(cols), self.R1, self.n2)))
+
+    def inverse_unpack(self, recv, nat):
+        nat.copy_(_t(self._tr(recv, self.n1, self.R2).reshape(-1, 2)))
+
+
 def _worker(rank, world, port, log2n, q, w, x, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -101,6 +134,41 @@ def test_fourstep_gloo_world2(params, log2n, world):
     assert np.array_equal(y, O.ntt(x, q, w))
     xr = from_columns([out[r][1] for r in range(world)], n1, n2)
     assert np.array_equal(xr, x)
+
+
+def _worker_natural(rank, world, port, log2n, q, w, x, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 1 << log2n
+    fs = FourStep(log2n, q, w, rank, world, local=OracleLocal(log2n, q, w, rank, world), layout="natural")
+    ys = fs.forward(_t(x[rank * n // world:(rank + 1) * n // world]))
+    xs = fs.inverse(ys)
+    out[rank] = (_n(ys).copy(), _n(xs).copy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("log2n,world", [(6, 2), (9, 2), (8, 4)])
+def test_fourstep_natural_layout_gloo(params, log2n, world):
+    """natural block layout: rank g's forward output is y[g N/G, (g+1) N/G) of the oracle's
+    N-point NTT, and the inverse returns each rank its own slice of x"""
+    e = params["extra"]["rand128_0"]
+    q = e["q"]
+    w = pow(e["psi"], 1 << (e["logn"] + 1 - log2n), q)
+    x = synth.uniform_residues(q, 1 << log2n, 91 + log2n)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_natural, args=(world, _free_port(), log2n, q, w, x, out), nprocs=world)
+    y = np.concatenate([out[r][0] for r in range(world)])
+    assert np.array_equal(y, O.ntt(x, q, w))
+    assert np.array_equal(np.concatenate([out[r][1] for r in range(world)]), x)
+
+
+def test_natural_layout_requires_all_to_all():
+    with pytest.raises(ValueError):
+        FourStep(6, 97, 1, local=object(), transport="p2p", layout="natural")
+    with pytest.raises(ValueError):
+        FourStep(6, 97, 1, local=object(), layout="rowmajor")
 
 
 def test_layout_maps_roundtrip():

@@ -123,3 +123,78 @@ def test_fourstep_virtual_ranks(FS, params, log2n, world):
     y, xr = virtual_run(FS, log2n, q, w, x, world)
     assert np.array_equal(y, O.ntt(x, q, w))
     assert np.array_equal(xr, x)
+
+
+def virtual_run_natural(FS, log2n, q, w, x, world):
+    """natural block layout (include/ntt128.h): virtual rank g holds x[g N/G, (g+1) N/G);
+    the three all-to-alls per direction are block copies between the ranks' buffers"""
+    import torch
+    n = 1 << log2n
+    locs = [FS.FourStepLocal(log2n, q, w, r, world) for r in range(world)]
+    R1, R2 = locs[0].R1, locs[0].R2
+
+    def run(cur, names, blocks):
+        for name, shp in zip(names[:3], blocks):
+            sends = []
+            for r, L in enumerate(locs):
+                s = torch.full((world, *shp, 2), -1, dtype=torch.int64, device="cuda")
+                getattr(L, name)(cur[r], s)
+                sends.append(s)
+            cur = [torch.stack([sends[g][h] for g in range(world)]).contiguous() for h in range(world)]
+        outs = []
+        for r, L in enumerate(locs):
+            o = torch.full((n // world, 2), -1, dtype=torch.int64, device="cuda")
+            getattr(L, names[3])(cur[r], o)
+            outs.append(o)
+        return outs
+
+    xs = [to_dev(x[r * n // world:(r + 1) * n // world]) for r in range(world)]
+    ys = run(xs, ("forward_pack", "forward_a_nat", "forward_c_nat", "forward_unpack"), ((R2, R1), (R1, R2), (R2, R1)))
+    y = np.concatenate([to_host(t) for t in ys])
+    xb = run(ys, ("inverse_pack", "inverse_a_nat", "inverse_c_nat", "inverse_unpack"), ((R1, R2), (R2, R1), (R1, R2)))
+    return y, np.concatenate([to_host(t) for t in xb])
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("log2n", [8, 13, 17, 22])
+def test_fourstep_natural_layout_virtual_ranks(FS, params, log2n, world):
+    """natural block layout: concatenated forward slices = the oracle's NTT, exact round trip
+    (FULL-class cfg5 prime; a lazy-class prime up to its 2^17 roots; 2^22 = 2^9 x 2^13 has
+    multi-pass passes A and C)"""
+    for key in (("cfg5", "b126") if log2n <= 17 else ("cfg5",)):
+        e = params["cfg5"] if key == "cfg5" else params["extra"]["b126"]
+        q = e["q"]
+        if key == "cfg5":
+            w = pow(e["omega"], 1 << (26 - log2n), q)
+        else:
+            w = pow(e["psi"], 1 << (e["logn"] + 1 - log2n), q)
+        x = synth.uniform_residues(q, 1 << log2n, 500 + log2n + world)
+        y, xr = virtual_run_natural(FS, log2n, q, w, x, world)
+        assert np.array_equal(y, O.ntt(x, q, w)), key
+        assert np.array_equal(xr, x), key
+
+
+def test_fourstep_natural_layout_class(FS, params):
+    """FourStep(layout="natural") at world 1: the slice is the whole vector"""
+    e = params["cfg5"]
+    q, log2n = e["q"], 16
+    w = pow(e["omega"], 1 << (26 - log2n), q)
+    x = synth.uniform_residues(q, 1 << log2n, 78)
+    fs = FS.FourStep(log2n, q, w, layout="natural")
+    y = fs.forward(to_dev(x))
+    assert np.array_equal(to_host(y), O.ntt(x, q, w))
+    assert np.array_equal(to_host(fs.inverse(y)), x)
+
+
+def test_fourstep_natural_layout_errors(FS, params):
+    import torch
+    from paper_2509_12494_b200 import ntt128 as N
+    e = params["cfg5"]
+    q = e["q"]
+    w = pow(e["omega"], 1 << 16, q)
+    L = FS.FourStepLocal(10, q, w, 0, 2)
+    a = torch.zeros((512, 2), dtype=torch.int64, device="cuda")
+    with pytest.raises(N.NTT128ArgError):
+        L.forward_pack(a, a)          # in-place pack is refused
+    with pytest.raises(N.NTT128ArgError):
+        L.inverse_unpack(a, a)

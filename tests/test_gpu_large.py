@@ -2,7 +2,8 @@
 criterion is bitwise-identical results; SURVEY.md §8(c) "Parity procedure"):
 
 * BASELINE cfg 5, N = 2^26: the FULL output of the three-pass plan, of the four-step at
-  G = 1 and of the four-step over 8 virtual ranks (both transports) against the oracle's
+  G = 1 and of the four-step over 8 virtual ranks (both transports, and the natural block
+  layout at G = 1 and 8) against the oracle's
   textbook radix-2 `ntt_large`, itself pinned at sampled outputs by direct O(N)
   evaluation of Eq. ntt, which shares no structure with any radix
   algorithm; exact round trips;
@@ -81,6 +82,19 @@ def test_cfg5_fourstep_virtual_g8_full(N, cfg5, peers):
     yv, xr = (virtual_run_peers if peers else virtual_run)(FS, 26, q, w, x, 8)
     assert np.array_equal(yv, y), f"four-step virtual G=8 (peers={peers}) != oracle"
     assert np.array_equal(xr, x), f"four-step virtual G=8 (peers={peers}) round trip"
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("world", [1, 8])
+def test_cfg5_fourstep_natural_layout_full(N, cfg5, world):
+    """natural block layout: rank g's slices of x in, of y out"""
+    import torch
+    from paper_2509_12494_b200 import fourstep as FS
+    from tests.test_gpu_fourstep import virtual_run_natural
+    q, w, x, y = cfg5
+    yv, xr = virtual_run_natural(FS, 26, q, w, x, world)
+    assert np.array_equal(yv, y), f"four-step natural layout, virtual G={world} != oracle"
+    assert np.array_equal(xr, x), f"four-step natural layout, virtual G={world} round trip"
     torch.cuda.empty_cache()
 
 
