@@ -20,6 +20,18 @@ ys = [torch.from_numpy(synth.uniform_residues(q, n, 20 + s).view(np.int64)).cuda
 zs = [torch.empty_like(v) for v in xs]
 hbm = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6500
 out = []
+# spot check of every op on set 0 against Python integers (experiment kernels must stay exact)
+rng = np.random.default_rng(5)
+idx = rng.integers(0, n, 2000)
+xi, yi = synth.to_ints(xs[0].cpu().numpy().view(np.uint64)[idx]), synth.to_ints(ys[0].cpu().numpy().view(np.uint64)[idx])
+for name, ref in (("add", lambda u, v: (u + v) % q), ("mul", lambda u, v: u * v % q), ("axpy", lambda u, v: (a * u + v) % q)):
+    if name == "axpy":
+        zt = ys[0].clone(); N.axpy(a, xs[0], zt, q)
+    else:
+        zt = (N.vadd if name == "add" else N.vmul)(xs[0], ys[0], q)
+    torch.cuda.synchronize()
+    got = synth.to_ints(zt.cpu().numpy().view(np.uint64)[idx])
+    assert got == [ref(u, v) for u, v in zip(xi, yi)], name + " mismatch"
 for name, fn in [("add", N.vadd), ("mul", N.vmul)] + [("axpy", None)]:
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
