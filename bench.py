@@ -465,7 +465,9 @@ def run_rows(args, P, pk, stream, rank, world):
     import synth
     rows = {"rows_scaling": {"cfg1": "replica per rank (max latency)", "cfg2": "strong (n split over ranks)",
                              "cfg3_polymul": "weak (64 per rank)", "cfg4": "strong (1 GiB total, batch split)",
-                             "cfg5_three_pass": "replica per rank", "cfg5_fourstep": "one transform over all ranks",
+                             "cfg5_three_pass": "replica per rank",
+                             "cfg5_fourstep": "one transform over all ranks (transposed layouts: nccl / p2p; "
+                                              "natural block layout: nccl, two more all-to-alls per direction)",
                              "f4": "weak (32 per rank)"},
             "rows_timing": "median of 3 repeats, each max over ranks of CUDA-event time"}
     # cfg1: single N = 1024 forward + inverse (latency) -- one replica per rank
