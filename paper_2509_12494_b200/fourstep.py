@@ -190,7 +190,8 @@ class FourStep:
     """
 
     def __init__(self, log2n: int, q: int, omega: int, rank: int = 0, world: int = 1, group=None,
-                 device: int | None = None, local=None, transport: str = "nccl", layout: str = "transposed"):
+                 device: int | None = None, local=None, transport: str = "nccl", layout: str = "transposed",
+                 symmetric: bool | None = None):
         # `local` is injectable so the exchange schedule can be exercised by CPU tests (gloo)
         if transport not in ("nccl", "p2p"):
             raise ValueError(f"transport must be 'nccl' or 'p2p', not {transport!r}")
@@ -202,6 +203,10 @@ class FourStep:
         self.group, self.world = group, world
         self.transport, self.layout = transport, layout
         self._recv = self._hdl = None
+        # p2p receive buffer: symmetric memory whenever world > 1; `symmetric=True` forces it at
+        # world 1 too (a one-rank process group), so a single GPU exercises the same allocation,
+        # rendezvous, peer pointers and device barriers
+        self._symmetric = (world > 1) if symmetric is None else bool(symmetric)
         if transport == "p2p":
             self._setup_p2p()
 
@@ -210,7 +215,9 @@ class FourStep:
         L = self.local
         dev = torch.device("cuda", L.device)
         elems = L.R1 * L.n2                            # = R2 * n1 = N / G: both directions fit
-        if self.world == 1:
+        if not self._symmetric:
+            if self.world != 1:
+                raise ValueError("transport='p2p' with world > 1 needs symmetric memory")
             self._recv = torch.empty((elems, 2), dtype=torch.int64, device=dev)
             self._peers = [self._recv.data_ptr()]
             return

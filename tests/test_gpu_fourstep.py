@@ -209,3 +209,35 @@ def test_fourstep_natural_layout_errors(FS, params):
         L.forward_pack(a, a)          # in-place pack is refused
     with pytest.raises(N.NTT128ArgError):
         L.inverse_unpack(a, a)
+
+
+def test_fourstep_p2p_symmetric_memory_one_rank(FS, params):
+    """the p2p transport's symmetric-memory path (allocation, rendezvous, peer pointers,
+    device barriers) on a one-rank NCCL process group: the code a multi-GPU run takes,
+    with no rank waiting on another"""
+    import socket
+    import torch
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group already exists in this process")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    store = dist.TCPStore("127.0.0.1", port, 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        e = params["cfg5"]
+        q, log2n = e["q"], 14
+        w = pow(e["omega"], 1 << (26 - log2n), q)
+        x = synth.uniform_residues(q, 1 << log2n, 79)
+        l1, l2 = FS.split(log2n)
+        fs = FS.FourStep(log2n, q, w, transport="p2p", symmetric=True)
+        assert fs._hdl is not None and len(fs._peers) == 1
+        rows = fs.forward(to_dev(FS.to_columns(x, 1 << l1, 1 << l2, 0, 1)))
+        assert np.array_equal(FS.from_rows([to_host(rows)], 1 << l1, 1 << l2), O.ntt(x, q, w))
+        cols = fs.inverse(rows)
+        assert np.array_equal(FS.from_columns([to_host(cols)], 1 << l1, 1 << l2), x)
+        del fs
+    finally:
+        dist.destroy_process_group()
