@@ -27,8 +27,9 @@
  * They are not checked unless NTT128_FLAG_CHECK_INPUT is set on the plan (or
  * passed to a vec128 call); unreduced input gives unspecified output.
  *
- * Aliasing.  In place (out == in, z == x or z == y) is allowed everywhere.
- * Partial overlap is undefined.
+ * Aliasing.  In place (out == in, z == x or z == y) is allowed everywhere except
+ * where a function says otherwise (the four-step pass C and natural-layout calls
+ * refuse it with NTT128_ERR_INVALID_ARG).  Partial overlap is undefined.
  *
  * Errors.  No exception crosses the ABI.  Every function returns a status;
  * on error nothing is enqueued and outputs are untouched.
