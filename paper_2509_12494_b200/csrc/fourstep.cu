@@ -14,9 +14,11 @@
 // NVLink: the exchange is the epilogue of the transform); pass C's FIRST pass gathers the
 // columns of the received [n1][R2] matrix directly (element stride R2) and multiplies the
 // four-step twiddle w^{j1 k2} in as it loads -- one Montgomery product per element from a
-// per-rank factor table [n1][R2] (plan time, laid out like the received matrix).  No separate twiddle, pack or transpose
-// kernel and no extra HBM round trip: a direction is the same 3 passes as the single-GPU
-// plan (n2 = 2^17 as 9 + 8, n1 = 2^9 as one pass at cfg 5).
+// per-rank factor table [n1][R2] (plan time, laid out like the received matrix).  In the
+// transposed layouts there is no separate twiddle, pack or transpose kernel and no extra HBM
+// round trip: a direction is the same 3 passes as the single-GPU plan (n2 = 2^17 as 9 + 8,
+// n1 = 2^9 as one pass at cfg 5).  The natural block layout (contiguous N/G slices, below)
+// adds one pack kernel before and one transpose kernel after its two extra exchanges.
 // The inverse swaps the roles: pass A = n1-point transforms with root w^{-n2} of the rows
 // into the blocks of the destination of j1; pass C = N^{-1} w^{-j1 k2} at the load of the
 // n2-point transforms with root w^{-n1} of the received [n2][R1] matrix's columns (forward
