@@ -568,6 +568,23 @@ def run_rows(args, P, pk, stream, rank, world):
     rows["f4_ntt256_roofline_frac"] = bf * 136 / (pk["tprod_s"] * 1e12)
     del p6, xx, yy, zz
     torch.cuda.empty_cache()
+    # 192-bit moduli (q < 2^192: the 6-word kernels, 72 + 6 = 78 word products per butterfly)
+    e = P["w256"]["b192"]
+    q = hexint(e["q"])
+    w = pow(hexint(e["omega"]), 1 << (e["logn"] - 16), q)
+    p7 = N.Plan256(16, q, w, batch=32)
+    xx = torch.from_numpy(synth.uniform_residues_w(q, 32 << 16, synth.stream_seed(10, 0, 17))
+                          .reshape(32, 1 << 16, 4).view(np.int64)).cuda()
+    yy, zz = torch.empty_like(xx), torch.empty_like(xx)
+    p7.forward(xx, out=yy); p7.inverse(yy, out=zz)
+    torch.cuda.synchronize()
+    assert torch.equal(zz, xx)
+    ms = timed_rank(lambda i: (p7.forward(xx, out=yy), p7.inverse(yy, out=zz)), 10, world)
+    bf = 2 * 32 * (1 << 15) * 16 / (ms * 1e-3)
+    rows["f4_ntt192_n2^16_x32_butterflies_per_s"] = bf * world
+    rows["f4_ntt192_roofline_frac"] = bf * 78 / (pk["tprod_s"] * 1e12)
+    del p7, xx, yy, zz
+    torch.cuda.empty_cache()
     return rows
 
 

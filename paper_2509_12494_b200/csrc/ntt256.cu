@@ -12,6 +12,9 @@
 // per thread), a 32-byte residue kept as two 16-byte planes in shared memory so every
 // 8-lane phase touches distinct banks (slot l + l/8, as in the 128-bit kernels).  All
 // values canonical (no lazy classes yet).
+// Word count W (template parameter): plans and vec256_mul whose moduli are all < 2^192 run
+// the 6-word arithmetic (Montgomery R = 2^192, 72 + 6 word products per product instead of
+// 128 + 8); storage stays 32 bytes per residue with the top limb zero.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -129,61 +132,92 @@ struct ModC256 {
 struct E256 {
     uint32_t w[8];
 };
-__device__ __forceinline__ E256 e_from(uint4 lo, uint4 hi) { return E256{{lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w}}; }
+// W = 6: words 6 and 7 are zero by construction (known to the compiler: no registers spent)
+template <int W>
+__device__ __forceinline__ E256 e_from(uint4 lo, uint4 hi) {
+    return E256{{lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, W == 8 ? hi.z : 0u, W == 8 ? hi.w : 0u}};
+}
 __device__ __forceinline__ uint4 e_lo(const E256& e) { return make_uint4(e.w[0], e.w[1], e.w[2], e.w[3]); }
 __device__ __forceinline__ uint4 e_hi(const E256& e) { return make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]); }
-__device__ __forceinline__ E256 e_ld(const uint4* p) { return e_from(p[0], p[1]); }   // 32-byte element at p
+template <int W>
+__device__ __forceinline__ E256 e_ld(const uint4* p) { return e_from<W>(p[0], p[1]); }   // 32-byte element at p
 __device__ __forceinline__ void e_st(uint4* p, const E256& e) { p[0] = e_lo(e); p[1] = e_hi(e); }
+template <int W>
 __device__ __forceinline__ E256 mmul(const E256& a, const E256& b, const ModC256& M) {
     E256 r;
-    mont_mul256(a.w, b.w, M.q, M.qinv0, r.w);
+    if (W == 8) {
+        mont_mul256(a.w, b.w, M.q, M.qinv0, r.w);
+    } else {
+        mont_mul192(a.w, b.w, M.q, M.qinv0, r.w);
+        r.w[6] = r.w[7] = 0;
+    }
     return r;
+}
+template <int W>
+__device__ __forceinline__ void addm(const E256& a, const E256& b, const ModC256& M, E256& r) {
+    if (W == 8) {
+        add_mod256(a.w, b.w, M.q, r.w);
+    } else {
+        add_mod192(a.w, b.w, M.q, r.w);
+        r.w[6] = r.w[7] = 0;
+    }
+}
+template <int W>
+__device__ __forceinline__ void subm(const E256& a, const E256& b, const ModC256& M, E256& r) {
+    if (W == 8) {
+        sub_mod256(a.w, b.w, M.q, r.w);
+    } else {
+        sub_mod192(a.w, b.w, M.q, r.w);
+        r.w[6] = r.w[7] = 0;
+    }
 }
 __device__ __forceinline__ uint32_t brev_n(uint32_t x, int bits) { return bits == 0 ? 0u : (__brev(x) >> (32 - bits)); }
 // u 2^-s mod q (1 <= s <= 31, u < q): one s-bit Montgomery digit, as shr_mod in arith128.cuh --
 // m = u_0 (-q^-1) mod 2^s, T = (u + m q) / 2^s < q + u / 2^s < 2q, one conditional subtraction
 // (T may reach bit 256: ninth word).  The inverse's last stage: u N^-1 = u 2^-n.
+template <int W>
 __device__ __forceinline__ E256 shr256(const E256& u, uint32_t s, const ModC256& M) {
     const uint32_t m = (u.w[0] * M.qinv0) & ((1u << s) - 1u);
-    uint32_t x[9];
+    uint32_t x[W + 1];
     uint64_t c = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
+    for (int i = 0; i < W; i++) {
         const uint64_t t = (uint64_t)m * M.q[i] + u.w[i] + c;   // < 2^64
         x[i] = (uint32_t)t;
         c = t >> 32;
     }
-    x[8] = (uint32_t)c;
-    uint32_t t[9];
+    x[W] = (uint32_t)c;
+    uint32_t t[W + 1];
 #pragma unroll
-    for (int i = 0; i < 8; i++) t[i] = __funnelshift_r(x[i], x[i + 1], s);
-    t[8] = x[8] >> s;
-    uint32_t d[8];
+    for (int i = 0; i < W; i++) t[i] = __funnelshift_r(x[i], x[i + 1], s);
+    t[W] = x[W] >> s;
+    uint32_t d[W];
     int64_t bw = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
+    for (int i = 0; i < W; i++) {
         const int64_t v = (int64_t)t[i] - (int64_t)M.q[i] + bw;
         d[i] = (uint32_t)v;
         bw = v >> 32;                                            // 0 or -1
     }
-    const bool ge = ((int64_t)t[8] + bw) >= 0;                   // T >= q
+    const bool ge = ((int64_t)t[W] + bw) >= 0;                   // T >= q
     E256 r;
 #pragma unroll
-    for (int i = 0; i < 8; i++) r.w[i] = ge ? d[i] : t[i];
+    for (int i = 0; i < 8; i++) r.w[i] = i < W ? (ge ? d[i] : t[i]) : 0u;
     return r;
 }
 
 // out[m][i] = scale_m base_m^i (Montgomery form), i < count: product over the set bits of i
+template <int W>
 __global__ void k_pow256(uint4* out, uint64_t stride, uint64_t count, const uint4* pow2, int K, const uint4* scale,
                          const ModC256* mods) {
     const int m = blockIdx.y;
     const ModC256 M = mods[m];
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
-        E256 r = e_ld(scale + 2 * m);
+        E256 r = e_ld<W>(scale + 2 * m);
         uint64_t e = i;
         int k = 0;
         while (e) {
-            if (e & 1) r = mmul(r, e_ld(pow2 + 2 * ((size_t)m * K + k)), M);
+            if (e & 1) r = mmul<W>(r, e_ld<W>(pow2 + 2 * ((size_t)m * K + k)), M);
             e >>= 1;
             k++;
         }
@@ -233,7 +267,7 @@ struct Shape256 {
     static constexpr int GP = G + G / 8 + 1;
 };
 
-template <int B, bool FIRST, bool SCALE_LAST>
+template <int B, bool FIRST, bool SCALE_LAST, int W>
 __global__ void __launch_bounds__(Shape256<B>::C * Shape256<B>::T)
 k_ntt256_pass(const __grid_constant__ Pass256Args a) {
     using S = Shape256<B>;
@@ -293,7 +327,7 @@ k_ntt256_pass(const __grid_constant__ Pass256Args a) {
     #pragma unroll
             for (int k = 0; k < E; k++) {
                 const int s = slot256(l0 | (k << w));
-                x[k] = e_from(glo[s], ghi[s]);
+                x[k] = e_from<W>(glo[s], ghi[s]);
             }
     #pragma unroll
             for (int bit = 0; bit < RB; bit++) {
@@ -308,13 +342,13 @@ k_ntt256_pass(const __grid_constant__ Pass256Args a) {
                     E256 v = x[k1], u = x[k0];
                     if (!trivial) {
                         const int ti = (1 << sl) - 1 + tlo + ((kk & ((1 << bit) - 1)) << w);
-                        v = mmul(v, e_from(twl[ti], twh[ti]), M);
-                        if (last) u = (NTT256_SHIFT_SCALE && n >= 1) ? shr256(u, n, M)
-                                                                   : mmul(u, E256{{M.ninv_m[0], M.ninv_m[1], M.ninv_m[2], M.ninv_m[3], M.ninv_m[4],
-                                                                                    M.ninv_m[5], M.ninv_m[6], M.ninv_m[7]}}, M);
+                        v = mmul<W>(v, e_from<W>(twl[ti], twh[ti]), M);
+                        if (last) u = (NTT256_SHIFT_SCALE && n >= 1) ? shr256<W>(u, n, M)
+                                                                   : mmul<W>(u, E256{{M.ninv_m[0], M.ninv_m[1], M.ninv_m[2], M.ninv_m[3], M.ninv_m[4],
+                                                                                      M.ninv_m[5], M.ninv_m[6], M.ninv_m[7]}}, M);
                     }
-                    add_mod256(u.w, v.w, M.q, x[k0].w);
-                    sub_mod256(u.w, v.w, M.q, x[k1].w);
+                    addm<W>(u, v, M, x[k0]);
+                    subm<W>(u, v, M, x[k1]);
                 }
             }
     #pragma unroll
@@ -351,27 +385,30 @@ k_ntt256_pass(const __grid_constant__ Pass256Args a) {
 }
 
 // z = x y mod q: two Montgomery products (x y R^-1, then * R^2)
+template <int W>
 __global__ void k_vmul256(uint4* z, const uint4* x, const uint4* y, uint64_t n, const ModC256 M) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const E256 t = mmul(e_ld(x + 2 * i), e_ld(y + 2 * i), M);
-        e_st(z + 2 * i, mmul(t, E256{{M.r2[0], M.r2[1], M.r2[2], M.r2[3], M.r2[4], M.r2[5], M.r2[6], M.r2[7]}}, M));
+        const E256 t = mmul<W>(e_ld<W>(x + 2 * i), e_ld<W>(y + 2 * i), M);
+        e_st(z + 2 * i, mmul<W>(t, E256{{M.r2[0], M.r2[1], M.r2[2], M.r2[3], M.r2[4], M.r2[5], M.r2[6], M.r2[7]}}, M));
     }
 }
 
 typedef void (*Pass256Fn)(const Pass256Args);
-template <bool FIRST, bool SL>
-Pass256Fn pass256_fn(int B) {
+template <bool FIRST, bool SL, int W>
+Pass256Fn pass256_fn_w(int B) {
     switch (B) {
-        case 1: return k_ntt256_pass<1, FIRST, SL>;
-        case 2: return k_ntt256_pass<2, FIRST, SL>;
-        case 3: return k_ntt256_pass<3, FIRST, SL>;
-        case 4: return k_ntt256_pass<4, FIRST, SL>;
-        case 5: return k_ntt256_pass<5, FIRST, SL>;
-        case 6: return k_ntt256_pass<6, FIRST, SL>;
-        case 7: return k_ntt256_pass<7, FIRST, SL>;
-        default: return k_ntt256_pass<8, FIRST, SL>;
+        case 1: return k_ntt256_pass<1, FIRST, SL, W>;
+        case 2: return k_ntt256_pass<2, FIRST, SL, W>;
+        case 3: return k_ntt256_pass<3, FIRST, SL, W>;
+        case 4: return k_ntt256_pass<4, FIRST, SL, W>;
+        case 5: return k_ntt256_pass<5, FIRST, SL, W>;
+        case 6: return k_ntt256_pass<6, FIRST, SL, W>;
+        case 7: return k_ntt256_pass<7, FIRST, SL, W>;
+        default: return k_ntt256_pass<8, FIRST, SL, W>;
     }
 }
+template <bool FIRST, bool SL>
+Pass256Fn pass256_fn(int B, int W) { return W == 6 ? pass256_fn_w<FIRST, SL, 6>(B) : pass256_fn_w<FIRST, SL, 8>(B); }
 
 std::vector<int> pass_bits256(int n) {
     std::vector<int> b;
@@ -380,17 +417,20 @@ std::vector<int> pass_bits256(int n) {
     return b;
 }
 
-ModC256 make_modc(const H256& q, uint64_t N) {
+// words of the Montgomery radix R = 2^(32 W): 6 when q < 2^192, else 8
+inline int words_for(const H256& q) { return q.w[3] == 0 ? 6 : 8; }   // 64-bit limbs: q < 2^192
+
+ModC256 make_modc(const H256& q, uint64_t N, int W) {
     ModC256 c;
     memset(&c, 0, sizeof(c));
     h_words(q, c.q);
     uint32_t inv = 1;
     for (int i = 0; i < 5; i++) inv *= 2 - c.q[0] * inv;
     c.qinv0 = 0u - inv;
-    H256 r = h_from(1);                     // R mod q = 2^256 mod q, R^2 mod q: repeated doubling
-    for (int i = 0; i < 256; i++) r = h_addmod(r, r, q);
+    H256 r = h_from(1);                     // R mod q = 2^(32 W) mod q, R^2 mod q: repeated doubling
+    for (int i = 0; i < 32 * W; i++) r = h_addmod(r, r, q);
     H256 r2 = r;
-    for (int i = 0; i < 256; i++) r2 = h_addmod(r2, r2, q);
+    for (int i = 0; i < 32 * W; i++) r2 = h_addmod(r2, r2, q);
     h_words(r, c.one_m);
     h_words(r2, c.r2);
     if (N > 1) {
@@ -404,6 +444,7 @@ ModC256 make_modc(const H256& q, uint64_t N) {
 
 struct ntt256_plan_s {
     uint32_t log2n, batch, nq;
+    int words;                          // 6 (every modulus < 2^192) or 8
     int device;
     uint64_t N;
     std::vector<int> bits;
@@ -427,12 +468,12 @@ static void plan256_free(ntt256_plan_s* p) {
 
 // table[m][i] = scale_m base_m^i, i < count (Montgomery form), on the device
 static cudaError_t gen256(uint4* out, uint64_t stride, uint64_t count, const std::vector<H256>& qs,
-                          const std::vector<H256>& base, const std::vector<H256>& scale, const ModC256* d_mods) {
+                          const std::vector<H256>& base, const std::vector<H256>& scale, const ModC256* d_mods, int W) {
     const int nq = (int)qs.size(), K = 32;
     std::vector<uint4> pow2((size_t)nq * K * 2), sc((size_t)nq * 2);
     for (int m = 0; m < nq; m++) {
         H256 r = h_from(1);
-        for (int i = 0; i < 256; i++) r = h_addmod(r, r, qs[m]);    // R mod q
+        for (int i = 0; i < 32 * W; i++) r = h_addmod(r, r, qs[m]);   // R mod q
         H256 b = base[m];                                              // base^(2^k), normal form
         for (int k = 0; k < K; k++) {
             const H256 bm = h_mulmod(b, r, qs[m]);                     // Montgomery form
@@ -453,7 +494,8 @@ static cudaError_t gen256(uint4* out, uint64_t stride, uint64_t count, const std
         unsigned gx = (unsigned)((count + 255) / 256);
         if (gx > 4096) gx = 4096;
         if (gx == 0) gx = 1;
-        k_pow256<<<dim3(gx, nq), 256>>>(out, stride, count, d_pow2, K, d_sc, d_mods);
+        if (W == 6) k_pow256<6><<<dim3(gx, nq), 256>>>(out, stride, count, d_pow2, K, d_sc, d_mods);
+        else k_pow256<8><<<dim3(gx, nq), 256>>>(out, stride, count, d_pow2, K, d_sc, d_mods);
         ntt128_count_launch(1);
         e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -499,9 +541,13 @@ extern "C" ntt128_status ntt256_plan_create(ntt256_plan_t* out, uint32_t log2n, 
     p->device = device;
     p->N = N;
     p->bits = pass_bits256((int)log2n);
+    p->words = 6;
+    for (auto& q : qs)
+        if (words_for(q) == 8) p->words = 8;
+    const int W = p->words;
     ntt128_status st = NTT128_OK;
     std::vector<ModC256> mc;
-    for (auto& q : qs) mc.push_back(make_modc(q, N));
+    for (auto& q : qs) mc.push_back(make_modc(q, N, W));
     p->mc0 = mc[0];
     if (cudaMalloc(&p->d_mods, n_moduli * sizeof(ModC256)) != cudaSuccess) st = NTT128_ERR_OOM;
     else if (cudaMemcpy(p->d_mods, mc.data(), n_moduli * sizeof(ModC256), cudaMemcpyHostToDevice) != cudaSuccess)
@@ -512,9 +558,9 @@ extern "C" ntt128_status ntt256_plan_create(ntt256_plan_t* out, uint32_t log2n, 
                             cudaMalloc(&ti, 32 * half * n_moduli) != cudaSuccess ||
                             cudaMalloc(&tl, 32 * half * n_moduli) != cudaSuccess))
         st = NTT128_ERR_OOM;
-    if (st == NTT128_OK && (gen256(tf, half, half, qs, omega, ones, p->d_mods) != cudaSuccess ||
-                            gen256(ti, half, half, qs, omega_inv, ones, p->d_mods) != cudaSuccess ||
-                            gen256(tl, half, half, qs, omega_inv, ninv, p->d_mods) != cudaSuccess))
+    if (st == NTT128_OK && (gen256(tf, half, half, qs, omega, ones, p->d_mods, W) != cudaSuccess ||
+                            gen256(ti, half, half, qs, omega_inv, ones, p->d_mods, W) != cudaSuccess ||
+                            gen256(tl, half, half, qs, omega_inv, ninv, p->d_mods, W) != cudaSuccess))
         st = NTT128_ERR_CUDA;
     int lo = 0;
     for (size_t i = 0; i < p->bits.size() && st == NTT128_OK; i++) {
@@ -557,8 +603,8 @@ static ntt128_status run256(ntt256_plan_s* p, const uint4* src, uint4* dst, cuda
     for (size_t i = 0; i < np; i++) {
         const int B = p->bits[i];
         const bool first = i == 0, sl = inverse && i + 1 == np;
-        Pass256Fn fn = first ? (sl ? pass256_fn<true, true>(B) : pass256_fn<true, false>(B))
-                             : (sl ? pass256_fn<false, true>(B) : pass256_fn<false, false>(B));
+        Pass256Fn fn = first ? (sl ? pass256_fn<true, true>(B, p->words) : pass256_fn<true, false>(B, p->words))
+                             : (sl ? pass256_fn<false, true>(B, p->words) : pass256_fn<false, false>(B, p->words));
         Pass256Args a;
         memset(&a, 0, sizeof(a));
         a.src = first ? src : dst;
@@ -623,10 +669,12 @@ extern "C" ntt128_status vec256_mul(uint64_t* d_z, const uint64_t* d_x, const ui
     if (((uintptr_t)d_z | (uintptr_t)d_x | (uintptr_t)d_y) & 15u) return NTT128_ERR_ALIGNMENT;
     uint64_t g0, g1;
     ntt128_stream_gen((cudaStream_t)s, &g0, &g1);
-    const ModC256 M = make_modc(q, 1);
+    const int W = words_for(q);
+    const ModC256 M = make_modc(q, 1, W);
     unsigned g = (unsigned)((n + 255) / 256);
     if (g > 148 * 8) g = 148 * 8;
-    k_vmul256<<<g, 256, 0, (cudaStream_t)s>>>((uint4*)d_z, (const uint4*)d_x, (const uint4*)d_y, n, M);
+    if (W == 6) k_vmul256<6><<<g, 256, 0, (cudaStream_t)s>>>((uint4*)d_z, (const uint4*)d_x, (const uint4*)d_y, n, M);
+    else k_vmul256<8><<<g, 256, 0, (cudaStream_t)s>>>((uint4*)d_z, (const uint4*)d_x, (const uint4*)d_y, n, M);
     ntt128_count_launch(1);
     return cudaGetLastError() == cudaSuccess ? NTT128_OK : NTT128_ERR_CUDA;
 }

@@ -1,7 +1,7 @@
 """GPU parity of the wider-modulus path (ntt256_*, vec256_mul) against
 the 256-bit oracle (oracle/oracle256.c), bit-exact: single-pass sizes, two- and three-pass
-schedules, 256/255/254/192-bit primes, several moduli per batch, structured inputs,
-in place, and the plan's argument checks."""
+schedules, 256/255/254/192-bit primes (moduli < 2^192 run the 6-word arithmetic), several
+moduli per batch, structured inputs, in place, and the plan's argument checks."""
 import numpy as np
 import pytest
 
@@ -50,11 +50,33 @@ def test_ntt256_sizes(N, params, logn):
         run(N, [e["q"]], [root(e, logn)], logn, x)
 
 
-def test_ntt256_three_pass(N, params):
-    e = params["w256"]["b255"]
-    logn = 18                                   # 6 + 6 + 6
+@pytest.mark.parametrize("key", ["b255", "b192"])
+def test_ntt256_three_pass(N, params, key):
+    """three passes (6 + 6 + 6); b192 (q < 2^192) runs the 6-word kernels"""
+    e = params["w256"][key]
+    logn = 18
     x = synth.uniform_residues_w(e["q"], 1 << logn, 2100).reshape(1, 1 << logn, 4)
     run(N, [e["q"]], [root(e, logn)], logn, x)
+
+
+def test_ntt192_structured_and_in_place(N, params):
+    """6-word plans: delta -> ones, all q-1, in place, and a 6-word / 8-word pair of plans on
+    the same data agreeing (the same transform through R = 2^192 and R = 2^256 arithmetic is
+    covered by the oracle on both sides)"""
+    import torch
+    e = params["w256"]["b192"]
+    q, logn = e["q"], 11
+    n = 1 << logn
+    x = np.stack([O4.to_array([1] + [0] * (n - 1)), O4.to_array([q - 1] * n),
+                  synth.uniform_residues_w(q, n, 2500)])
+    run(N, [q], [root(e, logn)], logn, x)
+    plan = N.Plan256(logn, q, root(e, logn), batch=3)
+    d = dev(x)
+    plan.forward(d, out=d)
+    assert O4.to_ints(host(d)[0]) == [1] * n
+    assert np.array_equal(host(d), O4.ntt(x, q, root(e, logn)))
+    plan.inverse(d, out=d)
+    assert torch.equal(d, dev(x))
 
 
 def test_ntt256_many_moduli_and_structured(N, params):

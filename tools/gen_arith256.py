@@ -1,14 +1,12 @@
-"""Generate paper_2509_12494_b200/csrc/arith256_gen.cuh: 8-word (256-bit) modular arithmetic
-for sm_100a as inline-PTX carry chains.  The Montgomery product is the
-even/odd alternating CIOS of arith128.cuh generalised to 8 words; its carry structure is
-checked word by word by tools/model/mont_eo_model_w.py (W = 8).
+"""Generate paper_2509_12494_b200/csrc/arith256_gen.cuh: 8-word (256-bit) and 6-word (192-bit)
+modular arithmetic for sm_100a as inline-PTX carry chains.  The Montgomery
+product is the even/odd alternating CIOS of arith128.cuh generalised to W words; its carry
+structure is checked word by word by tools/model/mont_eo_model_w.py (W = 8 and W = 6).
 
     python tools/gen_arith256.py        (rewrites the header; it is committed)
 """
 import os
 
-W = 8
-H = W // 2
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2509_12494_b200", "csrc",
                    "arith256_gen.cuh")
 
@@ -30,16 +28,18 @@ def asm_block(lines, outs, ins):
     return f"    asm({body.rstrip()}\n        : {o}\n        : {i});\n"
 
 
-def gen_mont():
+def gen_mont(W):
+    H = W // 2
+    NB = 32 * W
     s = []
-    s.append("// Montgomery product a b 2^-256 mod q, canonical result (a < 2^256, b < q, q odd < 2^256).\n"
+    s.append(f"// Montgomery product a b 2^-{NB} mod q, canonical result (a < 2^{NB}, b < q, q odd < 2^{NB}).\n"
              "// Even/odd alternating CIOS over 32-bit digits of b: 2^32 T_i = X + 2^32 Y, X holding the\n"
              "// products at even word positions, Y at odd ones (register-pair aligned); after a digit\n"
              "// X_0 = 0 and the shift is a change of roles (X' = Y + X_1, Y' = X / 2^64 + ...).  Per\n"
-             "// digit 16 IMAD.WIDE + 1 IMAD; 128 + 8 word products in all.\n")
-    s.append("__device__ __forceinline__ void mont_mul256(const uint32_t a[8], const uint32_t b[8], const uint32_t q[8],\n"
-             "                                            uint32_t qinv0, uint32_t r[8]) {\n")
-    s.append("    uint32_t x[9], y[9], n[9], m;\n")
+             f"// digit {2 * W} IMAD.WIDE + 1 IMAD; {2 * W * W} + {W} word products in all.\n")
+    s.append(f"__device__ __forceinline__ void mont_mul{NB}(const uint32_t a[{W}], const uint32_t b[{W}], const uint32_t q[{W}],\n"
+             f"                                            uint32_t qinv0, uint32_t r[{W}]) {{\n")
+    s.append(f"    uint32_t x[{W + 1}], y[{W + 1}], n[{W + 1}], m;\n")
     # digit 0
     lines, outs, ins = [], [], []
     for k in range(H):
@@ -56,14 +56,14 @@ def gen_mont():
             op_lo = "mad.lo.cc.u32" if k == 0 else "madc.lo.cc.u32"
             lines += [f"{op_lo} {{{acc}{2*k}}}, {{m}}, {{q{2*k+parity}}}, {{{acc}{2*k}}}",
                       f"madc.hi.cc.u32 {{{acc}{2*k+1}}}, {{m}}, {{q{2*k+parity}}}, {{{acc}{2*k+1}}}"]
-        lines.append(f"addc.u32 {{{acc}8}}, 0, 0" if fresh_top else f"addc.u32 {{{acc}8}}, {{{acc}8}}, 0")
-        outs = [("+r", f"{acc}[{i}]", f"{acc}{i}") for i in range(W)] + [("=r" if fresh_top else "+r", f"{acc}[8]", f"{acc}8")]
+        lines.append(f"addc.u32 {{{acc}{W}}}, 0, 0" if fresh_top else f"addc.u32 {{{acc}{W}}}, {{{acc}{W}}}, 0")
+        outs = [("+r", f"{acc}[{i}]", f"{acc}{i}") for i in range(W)] + [("=r" if fresh_top else "+r", f"{acc}[{W}]", f"{acc}{W}")]
         ins = [("r", "m", "m")] + [("r", f"q[{2*k+parity}]", f"q{2*k+parity}") for k in range(H)]
         return asm_block(lines, outs, ins)
 
     s.append(red_chain("x", 0, True))
     s.append(red_chain("y", 1, True))
-    s.append("#pragma unroll\n    for (int i = 1; i < 8; i++) {\n")
+    s.append(f"#pragma unroll\n    for (int i = 1; i < {W}; i++) {{\n")
     # block A: y (becomes X') in place, n = Y'
     lines = ["add.cc.u32 {y0}, {y0}, {x1}"]
     for k in range(H):
@@ -76,7 +76,7 @@ def gen_mont():
         op_lo = "mad.lo.cc.u32" if k == 0 else "madc.lo.cc.u32"
         lines += [f"{op_lo} {{y{2*k}}}, {{a{2*k}}}, {{bi}}, {{y{2*k}}}",
                   f"madc.hi.cc.u32 {{y{2*k+1}}}, {{a{2*k}}}, {{bi}}, {{y{2*k+1}}}"]
-    lines.append("addc.u32 {y8}, {y8}, 0")
+    lines.append(f"addc.u32 {{y{W}}}, {{y{W}}}, 0")
     outs = [("+r", f"y[{i}]", f"y{i}") for i in range(W + 1)] + [("=&r", f"n[{i}]", f"n{i}") for i in range(W)]
     ins = [("r", f"x[{i}]", f"x{i}") for i in range(1, W + 1)] + [("r", f"a[{i}]", f"a{i}") for i in range(W)] + \
           [("r", "b[i]", "bi")]
@@ -84,20 +84,21 @@ def gen_mont():
     s.append("        m = y[0] * qinv0;\n")
     s.append("    " + red_chain("y", 0, False).replace("\n    ", "\n        ").lstrip())
     s.append("    " + red_chain("n", 1, True).replace("\n    ", "\n        ").lstrip())
-    s.append("#pragma unroll\n        for (int k = 0; k < 9; k++) { x[k] = y[k]; y[k] = n[k]; }\n    }\n")
-    # final: T = Y + X / 2^32, then T - q if T >= q (T < 2q, 257 bits)
+    s.append(f"#pragma unroll\n        for (int k = 0; k < {W + 1}; k++) {{ x[k] = y[k]; y[k] = n[k]; }}\n    }}\n")
+    # final: T = Y + X / 2^32, then T - q if T >= q (T < 2q, NB + 1 bits)
     lines = ["add.cc.u32 t0, {y0}, {x1}"]
     for k in range(1, W):
         lines.append(f"addc.cc.u32 t{k}, {{y{k}}}, {{x{k+1}}}")
-    lines.append("addc.u32 t8, {y8}, 0")
+    lines.append(f"addc.u32 t{W}, {{y{W}}}, 0")
     lines.append("sub.cc.u32 d0, t0, {q0}")
     for k in range(1, W):
         lines.append(f"subc.cc.u32 d{k}, t{k}, {{q{k}}}")
-    lines += ["subc.u32 bw, t8, 0", "not.b32 nb, bw"]
+    lines += [f"subc.u32 bw, t{W}, 0", "not.b32 nb, bw"]
     for k in range(W):
         # bw == 0: T >= q -> d; bw == ~0: T < q -> t   (r = (t & bw) | (d & ~bw))
         lines += [f"and.b32 t{k}, t{k}, bw", f"and.b32 d{k}, d{k}, nb", f"or.b32 {{r{k}}}, t{k}, d{k}"]
-    lines = ["{", ".reg .u32 t0, t1, t2, t3, t4, t5, t6, t7, t8, d0, d1, d2, d3, d4, d5, d6, d7, bw, nb"] + lines + ["}"]
+    regs = ", ".join([f"t{k}" for k in range(W + 1)] + [f"d{k}" for k in range(W)] + ["bw", "nb"])
+    lines = ["{", f".reg .u32 {regs}"] + lines + ["}"]
     outs = [("=r", f"r[{i}]", f"r{i}") for i in range(W)]
     ins = [("r", f"y[{i}]", f"y{i}") for i in range(W + 1)] + [("r", f"x[{i}]", f"x{i}") for i in range(1, W + 1)] + \
           [("r", f"q[{i}]", f"q{i}") for i in range(W)]
@@ -106,13 +107,15 @@ def gen_mont():
     return "".join(s)
 
 
-def gen_addsub():
+def gen_addsub(W):
+    NB = 32 * W
     s = []
-    # add: 257-bit sum, subtract q, select
-    lines = ["{", ".reg .u32 s0, s1, s2, s3, s4, s5, s6, s7, s8, d0, d1, d2, d3, d4, d5, d6, d7, bw, nb",
+    # add: (NB+1)-bit sum, subtract q, select
+    regs = ", ".join([f"s{k}" for k in range(W + 1)] + [f"d{k}" for k in range(W)] + ["bw", "nb"])
+    lines = ["{", f".reg .u32 {regs}",
              "add.cc.u32 s0, {a0}, {b0}"] + [f"addc.cc.u32 s{k}, {{a{k}}}, {{b{k}}}" for k in range(1, W)] + \
-            ["addc.u32 s8, 0, 0", "sub.cc.u32 d0, s0, {q0}"] + [f"subc.cc.u32 d{k}, s{k}, {{q{k}}}" for k in range(1, W)] + \
-            ["subc.u32 bw, s8, 0", "not.b32 nb, bw"]
+            [f"addc.u32 s{W}, 0, 0", "sub.cc.u32 d0, s0, {q0}"] + [f"subc.cc.u32 d{k}, s{k}, {{q{k}}}" for k in range(1, W)] + \
+            [f"subc.u32 bw, s{W}, 0", "not.b32 nb, bw"]
     for k in range(W):
         lines += [f"and.b32 s{k}, s{k}, bw", f"and.b32 d{k}, d{k}, nb", f"or.b32 {{r{k}}}, s{k}, d{k}"]
     lines.append("}")
@@ -120,30 +123,33 @@ def gen_addsub():
     ins = [("r", f"a[{i}]", f"a{i}") for i in range(W)] + [("r", f"b[{i}]", f"b{i}") for i in range(W)] + \
           [("r", f"q[{i}]", f"q{i}") for i in range(W)]
     blk = asm_block(lines, outs, ins)
-    s.append("// r = a + b mod q (Eq. saddmod, PAPER.md:184-192, 257-bit sum); a, b < q\n")
-    s.append("__device__ __forceinline__ void add_mod256(const uint32_t a[8], const uint32_t b[8], const uint32_t q[8],\n"
-             "                                           uint32_t r[8]) {\n" + blk + "}\n\n")
+    s.append(f"// r = a + b mod q (Eq. saddmod, PAPER.md:184-192, {NB + 1}-bit sum); a, b < q\n")
+    s.append(f"__device__ __forceinline__ void add_mod{NB}(const uint32_t a[{W}], const uint32_t b[{W}], const uint32_t q[{W}],\n"
+             f"                                           uint32_t r[{W}]) {{\n" + blk + "}\n\n")
     # sub: borrow chain, + (q & mask)
-    lines = ["{", ".reg .u32 d0, d1, d2, d3, d4, d5, d6, d7, bw, m0, m1, m2, m3, m4, m5, m6, m7",
+    regs = ", ".join([f"d{k}" for k in range(W)] + ["bw"] + [f"m{k}" for k in range(W)])
+    lines = ["{", f".reg .u32 {regs}",
              "sub.cc.u32 d0, {a0}, {b0}"] + [f"subc.cc.u32 d{k}, {{a{k}}}, {{b{k}}}" for k in range(1, W)] + \
             ["subc.u32 bw, 0, 0"] + [f"and.b32 m{k}, {{q{k}}}, bw" for k in range(W)] + \
             ["add.cc.u32 {r0}, d0, m0"] + [f"addc.cc.u32 {{r{k}}}, d{k}, m{k}" for k in range(1, W - 1)] + \
             [f"addc.u32 {{r{W-1}}}, d{W-1}, m{W-1}", "}"]
     blk = asm_block(lines, outs, ins)
     s.append("// r = a - b mod q (Eq. ssubmod, PAPER.md:193-201)\n")
-    s.append("__device__ __forceinline__ void sub_mod256(const uint32_t a[8], const uint32_t b[8], const uint32_t q[8],\n"
-             "                                           uint32_t r[8]) {\n" + blk + "}\n\n")
+    s.append(f"__device__ __forceinline__ void sub_mod{NB}(const uint32_t a[{W}], const uint32_t b[{W}], const uint32_t q[{W}],\n"
+             f"                                           uint32_t r[{W}]) {{\n" + blk + "}\n\n")
     return "".join(s)
 
 
 def main():
+    w6 = ("// ---- 192-bit moduli (6 words, R = 2^192): the same generator at W = 6, used by plans whose\n"
+          "// moduli are all < 2^192 (residues still stored in 32-byte slots, top limb zero).\n\n")
     head = ("// arith256_gen.cuh -- GENERATED by tools/gen_arith256.py; do not edit by hand.\n"
             "// 256-bit (8 x 32-bit word) modular arithmetic for sm_100a (SURVEY.md §8(f) f4: wider\n"
             "// multi-word moduli, the paper's stated generalisation, PAPER.md:807-808).  Any odd\n"
             "// q < 2^256; residues canonical (< q) at every interface.\n"
             "#pragma once\n#include <cstdint>\n\nnamespace ntt256 {\n\n")
     with open(OUT, "w") as f:
-        f.write(head + gen_addsub() + gen_mont() + "}  // namespace ntt256\n")
+        f.write(head + gen_addsub(8) + gen_mont(8) + w6 + gen_addsub(6) + gen_mont(6) + "}  // namespace ntt256\n")
     print("wrote", OUT)
 
 
