@@ -251,7 +251,9 @@ void ntt128_fourstep_destroy(ntt128_fourstep_t fs);
  * conventions as the 128-bit plans above.  log2n in [1, 24]; flags must be 0.
  *   q_host, root_host: [n_moduli][4] uint64 (root of exact order N); n_moduli 1 or batch.
  * Plan creation validates primality (Miller-Rabin, 20 bases), N | q - 1 and the root's
- * order on the host (milliseconds per modulus).
+ * order on the host (milliseconds per modulus).  A plan whose moduli are all < 2^192 (and
+ * vec256_mul with such a q) computes with 6-word arithmetic; the layout is unchanged
+ * (the top limb of every residue is zero).
  * ------------------------------------------------------------------------- */
 typedef struct ntt256_plan_s *ntt256_plan_t;
 ntt128_status ntt256_plan_create(ntt256_plan_t *out, uint32_t log2n, uint32_t batch, const uint64_t *q_host,
