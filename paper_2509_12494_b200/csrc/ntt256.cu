@@ -267,8 +267,14 @@ struct Shape256 {
     static constexpr int GP = G + G / 8 + 1;
 };
 
+#ifndef NTT256_MINB6
+#define NTT256_MINB6 1        // resident CTAs per SM the 6-word pass kernels are register-budgeted for
+#endif
+#ifndef NTT256_MINB8
+#define NTT256_MINB8 1
+#endif
 template <int B, bool FIRST, bool SCALE_LAST, int W>
-__global__ void __launch_bounds__(Shape256<B>::C * Shape256<B>::T)
+__global__ void __launch_bounds__(Shape256<B>::C * Shape256<B>::T, W == 6 ? NTT256_MINB6 : NTT256_MINB8)
 k_ntt256_pass(const __grid_constant__ Pass256Args a) {
     using S = Shape256<B>;
     constexpr int G = S::G, RB = S::RB, E = S::E, T = S::T, C = S::C, GP = S::GP;

@@ -1,5 +1,5 @@
-"""Experiment: 256-bit NTT forward+inverse throughput (w256 b256 prime), N = 2^n, batch
-filling 2^21 residues (64 MiB)."""
+"""Experiment: 256-bit NTT forward+inverse throughput (w256 prime PRIME, default b256; b192 runs
+the 6-word kernels), N = 2^n, batch filling 2^21 residues (64 MiB)."""
 import json
 import sys
 
@@ -13,7 +13,10 @@ from paper_2509_12494_b200 import ntt128 as N  # noqa: E402
 import synth  # noqa: E402
 
 P = json.load(open("tests/golden/params.json"))
-e = P["w256"]["b256"]
+import os  # noqa: E402
+KEY = os.environ.get("PRIME", "b256")
+PROD = 78 if KEY == "b192" else 136
+e = P["w256"][KEY]
 q, L = int(e["q"], 16), e["logn"]
 for logn in [int(v) for v in sys.argv[1].split(",")]:
     w = pow(int(e["omega"], 16), 1 << (L - logn), q)
@@ -32,5 +35,5 @@ for logn in [int(v) for v in sys.argv[1].split(",")]:
     e1.record(); e1.synchronize()
     ms = e0.elapsed_time(e1) / 5
     bf = 2 * B * (1 << (logn - 1)) * logn
-    print("256-bit logn %2d batch %4d: %.3f ms  %.4e bfly/s  %.1f%% of the 136-product roofline" %
-          (logn, B, ms, bf / (ms * 1e-3), 100 * bf / (ms * 1e-3) * 136 / 9.3062e12))
+    print("%s logn %2d batch %4d: %.3f ms  %.4e bfly/s  %.1f%% of the %d-product roofline" %
+          (KEY, logn, B, ms, bf / (ms * 1e-3), 100 * bf / (ms * 1e-3) * PROD / 9.0992e12, PROD))
