@@ -7,7 +7,8 @@ trips, and the same transform through different launch shapes must agree bit for
 Shapes: the 8-CTA cluster kernel (N = 2^10, 1 polynomial), the one-CTA latency shape
 (40 polynomials), the batched single pass (400), two passes with pass-overlap counters
 (N = 2^14), the permutation-free negacyclic passes and polymul (N = 2^12), the BLAS ops
-(ragged n), and the 256-bit passes.
+(ragged n), the 256-bit and 192-bit (6-word) passes, and the four-step in the natural block
+layout (pack / transpose kernels) against the three-pass plan.
 """
 import json
 import os
@@ -87,6 +88,28 @@ def main():
     x4 = torch.from_numpy(synth.uniform_residues_w(q4, 2 << 10, 17).reshape(2, 1 << 10, 4).view(np.int64)).cuda()
     p4 = N.Plan256(10, q4, w4, batch=2)
     assert torch.equal(p4.inverse(p4.forward(x4)), x4), "256-bit round trip"
+    # 192-bit moduli (6-word kernels): round trip, and vec256_mul against Python integers
+    e6 = P["w256"]["b192"]
+    q6 = h(e6["q"])
+    w6 = pow(h(e6["omega"]), 1 << (e6["logn"] - 12), q6)
+    x6 = torch.from_numpy(synth.uniform_residues_w(q6, 2 << 12, 18).reshape(2, 1 << 12, 4).view(np.int64)).cuda()
+    p6 = N.Plan256(12, q6, w6, batch=2)
+    assert torch.equal(p6.inverse(p6.forward(x6)), x6), "192-bit round trip"
+    a6 = synth.uniform_residues_w(q6, 64, 19)
+    b6 = synth.uniform_residues_w(q6, 64, 20)
+    z6 = N.vmul256(torch.from_numpy(a6.view(np.int64)).cuda(), torch.from_numpy(b6.view(np.int64)).cuda(), q6)
+    ints = lambda arr: [sum(int(r[k]) << (64 * k) for k in range(4)) for r in arr]  # noqa: E731
+    assert ints(z6.cpu().numpy().view(np.uint64)) == [u * v % q6 for u, v in zip(ints(a6), ints(b6))], "vec256_mul (192-bit)"
+    # four-step in the natural block layout at one rank == the three-pass plan, bit for bit
+    from paper_2509_12494_b200 import fourstep as FS
+    e5 = P["cfg5"]
+    q5 = h(e5["q"])
+    w5 = pow(h(e5["omega"]), 1 << (26 - 14), q5)
+    x5 = dev(synth.uniform_residues(q5, 1 << 14, 21))
+    fs = FS.FourStep(14, q5, w5, layout="natural")
+    y5 = fs.forward(x5)
+    assert torch.equal(y5, N.Plan(14, q5, w5).forward(x5.reshape(1, -1, 2)).reshape(-1, 2)), "four-step vs plan"
+    assert torch.equal(fs.inverse(y5), x5), "four-step natural round trip"
     torch.cuda.synchronize()
     print("sanitize driver: all checks passed; library launches", N.launch_count())
 
