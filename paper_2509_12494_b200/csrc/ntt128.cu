@@ -966,6 +966,115 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
 #endif
 }
 
+// ----------------------------------------------------------------------------- first pass, TL groups per CTA
+// (DESIGN.md §6 "Two tiles per CTA").  A multi-pass first pass shares ONE twiddle set among
+// all its groups, so a CTA can own TL consecutive groups of one polynomial for the shared
+// memory of TL data tiles + one set: every tile's gather is issued up front (one cp.async
+// group per tile), tile k + 1's loads land while tile k computes, tile k's stores drain while
+// tile k + 1 computes, and the CTA signals the pass-overlap counter once for TL groups (one
+// release fence instead of TL).  Same arithmetic, addressing and layouts as k_ntt_pass's
+// FIRST path with C = 1; plain cyclic I/O only (no load-side factors, natural layout).
+#ifndef NTT_FIRST_TILES
+#define NTT_FIRST_TILES 2
+#endif
+#ifndef NTT_FIRST_TILES9
+#define NTT_FIRST_TILES9 1    // 9-stage first passes (radix-8 rounds)
+#endif
+template <int B, int RBMAX, int TL>
+__global__ void __launch_bounds__(PassShape<B, RBMAX>::T,
+                                  (PassOcc<B, RBMAX, false>::THREADS / PassShape<B, RBMAX>::T) > 0
+                                      ? PassOcc<B, RBMAX, false>::THREADS / PassShape<B, RBMAX>::T : 1)
+k_ntt_first_tl(const __grid_constant__ PassArgs a) {
+    constexpr int C = 1;
+    using S = PassShape<B, RBMAX, C, true>;
+    constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS;
+    constexpr int LT = B - RB;
+    constexpr int PER = G / T;                       // == E
+    constexpr bool WARPMAP = T <= 32 && (32 % T) == 0;
+    static_assert(B >= 8, "twiddles by bulk copy");
+    static_assert(TL >= 1 && (TL & (TL - 1)) == 0, "a CTA's groups stay in one polynomial: TL a power of two");
+    extern __shared__ __align__(128) uint4 sm[];
+    uint4* const dsm = sm;                           // [TL][GS] data tiles
+    uint4* const tsm = dsm + TL * GS;                // the pass's one twiddle set
+    __shared__ __align__(8) uint64_t tw_bar;
+
+    const uint32_t n = a.n, gbits = n - B;
+    const uint64_t N = 1ull << n;
+    const uint64_t gmask = (1ull << gbits) - 1;
+    uint64_t gg0 = (uint64_t)blockIdx.x * TL;        // TL divides the groups of a polynomial
+    if (a.nq > 1) gg0 = ((uint64_t)a.ord[gg0 >> gbits] << gbits) | (gg0 & gmask);
+    const int tid = threadIdx.x;
+    const uint64_t ggl = gg0 < a.total_groups ? gg0 : a.total_groups - 1;
+    const uint64_t poly = ggl >> gbits;
+    const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
+    if (tid == 0) {
+        mbar_init(&tw_bar, 1);
+        mbar_expect_tx(&tw_bar, (G - 1) * 16);
+        bulk_g2s(tsm, a.pt + m * a.pt_stride, (G - 1) * 16, &tw_bar);
+    }
+    if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.cnt_in) {
+        if (tid == 0) {
+            const uint32_t* cp = a.cnt_in + poly;
+            while ((int32_t)(ld_acquire_gpu(cp) - a.target) < 0) __nanosleep(128);
+        }
+        __syncthreads();
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // gathers: row r = t0 + i T of group g holds local index brev_B(r) (k_ntt_pass, C = 1)
+    constexpr int RT = 3 < LT ? 3 : LT;
+    const int t0 = (tid >> RT) | ((tid & ((1 << RT) - 1)) << (LT - RT));
+    const int lbase = (int)brev_bits((uint32_t)t0, B);
+    const uint64_t gstride = (uint64_t)T << gbits;
+#pragma unroll
+    for (int k = 0; k < TL; k++) {
+        const uint64_t gg = gg0 + k;
+        if (gg < a.total_groups) {
+            const uint4* srcp = a.src + poly * N + (((uint64_t)t0 << gbits) | (gg & gmask));
+            uint4* smc = dsm + k * GS;
+#pragma unroll
+            for (int i = 0; i < PER; i++)
+                cp_async16(smc + slot<B, true, RB>(lbase | (int)brev_bits((uint32_t)i, RB)), srcp + (size_t)i * gstride);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const QPar& M = a.qp[m];
+    uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+    const uint32_t qinv0 = M.qinv0;
+    const int mode = mode_of(q);
+    const U128 nf = U128{{0, 0, 0, 0}};
+#pragma unroll
+    for (int k = 0; k < TL; k++) {
+        // tile k's copies done (the later tiles' may still be in flight)
+        if (k == 0) asm volatile("cp.async.wait_group %0;" ::"n"(TL - 1) : "memory");
+        else if (k == 1) asm volatile("cp.async.wait_group %0;" ::"n"(TL > 2 ? TL - 2 : 0) : "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (k == 0) mbar_wait(&tw_bar, 0);
+        const uint64_t gg = gg0 + k;
+        uint4* gsm = dsm + k * GS;
+        if (mode == MODE_LAZY)
+            pass_rounds<B, C, true, false, RBMAX, MODE_LAZY, WARPMAP, true>(gsm, tsm, tid, 0, n, q, qinv0, nf, 0);
+        else if (mode == MODE_HALF)
+            pass_rounds<B, C, true, false, RBMAX, MODE_HALF, WARPMAP, true>(gsm, tsm, tid, 0, n, q, qinv0, nf, 0);
+        else
+            pass_rounds<B, C, true, false, RBMAX, MODE_FULL, WARPMAP, true>(gsm, tsm, tid, 0, n, q, qinv0, nf, 0);
+        if (WARPMAP) __syncthreads();
+        if (gg < a.total_groups) {   // the group is one contiguous row of the working order
+            uint4 outv[PER];
+#pragma unroll
+            for (int i = 0; i < PER; i++) outv[i] = gsm[slot<B, true, RB>(tid + i * T)];
+            uint4* dstp = a.dst + poly * N + ((uint64_t)brev_bits((uint32_t)(gg & gmask), gbits) << B);
+#pragma unroll
+            for (int i = 0; i < PER; i++) dstp[tid + i * T] = outv[i];
+        }
+    }
+    if (a.cnt_out) {
+        __syncthreads();
+        if (tid == 0) red_release_gpu_add(a.cnt_out + poly, 1u);
+    }
+}
+
 // ----------------------------------------------------------------------------- permutation-free negacyclic passes
 // SURVEY §8(f) f1 (DESIGN.md §6 "Bit-reversed negacyclic path").  Forward: Cooley-Tukey
 // butterflies with psi-merged twiddles, natural-order input, stages from the top index
@@ -1317,6 +1426,7 @@ struct PassCfg {
     bool tma = false;     // k_ntt_pass<..., TMA>: the launch must carry the data tile's tensor map
     bool first = false;
     bool single = false;  // one-pass kernel (several moduli per CTA: the device table, not QPar)
+    int tiles = 1;        // groups per CTA beyond C, handled one after another (k_ntt_first_tl)
 };
 
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE = false, int RBMAX = 3, bool PM = false, bool TMA = false>
@@ -1332,6 +1442,21 @@ static PassCfg make_cfg() {
     c.single = SINGLE;
     const size_t ntw = (size_t)((FIRST && !SINGLE) ? 1 : C) * S::TS;
     c.smem = ((size_t)C * S::GS + ntw + (TMA ? 2 : 0)) * sizeof(uint4);   // TMA: + the pad slot, + two mbarriers
+    return c;
+}
+
+// multi-pass first pass over TL groups per CTA (k_ntt_first_tl): plain cyclic I/O, C = 1
+template <int B, int RB, int TL>
+static PassCfg first_tl_cfg_t() {
+    using S = PassShape<B, RB, 1, true>;
+    PassCfg c;
+    c.fn = k_ntt_first_tl<B, RB, TL>;
+    c.B = B;
+    c.C = 1;
+    c.threads = S::T;
+    c.first = true;
+    c.tiles = TL;
+    c.smem = ((size_t)TL * S::GS + S::TS) * sizeof(uint4);
     return c;
 }
 
@@ -1955,9 +2080,10 @@ static ntt128_status check_range(const ntt128_plan_s* p, const uint4* src, cudaS
 // NTT128_NO_PDL (no pass overlap), NTT128_PDL_NOCNT (whole-grid programmatic dependencies
 // only), NTT128_NO_NC (polymul through the natural-order path), NTT128_NO_CLUSTER.
 struct Switches {
-    bool no_pdl = false, pdl_nocnt = false, no_nc = false, no_cluster = false;
+    bool no_pdl = false, pdl_nocnt = false, no_nc = false, no_cluster = false, no_tiles = false;
     Switches() {
 #if NTT128_EXPERIMENTS
+        no_tiles = getenv("NTT128_NO_TILES") != nullptr;
         no_pdl = getenv("NTT128_NO_PDL") != nullptr;
         pdl_nocnt = getenv("NTT128_PDL_NOCNT") != nullptr;
         no_nc = getenv("NTT128_NO_NC") != nullptr;
@@ -2032,7 +2158,8 @@ static ntt128_status launch_pass_q(const ntt128_plan_s* p, const PassCfg& c, con
         if (chunked) a.total_groups = (uint64_t)nb << (n - B);
         const PassCfg* cc = &c;
         if (c.tma && !tma_encode(a, c.first, n, B, lo, chunked ? nb : batch)) cc = &alt;   // per-thread cp.async tiles
-        const uint64_t ctas = (a.total_groups + cc->C - 1) / cc->C;
+        const uint64_t per_cta = (uint64_t)cc->C * cc->tiles;
+        const uint64_t ctas = (a.total_groups + per_cta - 1) / per_cta;
         if (launch_pass(*cc, a, ctas, stream, pdl) != cudaSuccess) return NTT128_ERR_CUDA;
         ntt128_count_launch(1);
     }
@@ -2321,6 +2448,17 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
         PassCfg c = pass_cfg(npass, i, B, scale_last, lo, n);
         if (npass == 1 && use_latency_shape(B, p->batch))
             c = scale_last ? single_lat_cfg_t<true>(B) : single_lat_cfg_t<false>(B);
+        // plain cyclic first pass of 8 stages, one group per CTA: TL groups per CTA
+        {
+            const int tl = B == 8 ? NTT_FIRST_TILES : (B == 9 ? NTT_FIRST_TILES9 : 1);
+            if (tl > 1 && i == 0 && npass > 1 && c.first && !c.single && !c.tma && c.C == 1 && !o.io && !o.pmul &&
+                p->kind == 0 && ((1ull << (n - B)) % tl) == 0 && !switches().no_tiles) {
+                c = B == 8 ? first_tl_cfg_t<8, NTT_RB8, (NTT_FIRST_TILES > 1 ? NTT_FIRST_TILES : 2)>()
+                           : first_tl_cfg_t<9, NTT_RB9, (NTT_FIRST_TILES9 > 1 ? NTT_FIRST_TILES9 : 2)>();
+                if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
+                    return NTT128_ERR_CUDA;
+            }
+        }
         bool pm = false;
         if (i == 0 && o.io && npass == 1 && B == 9 && o.io->in_ps == 1 && strided_pm_first(B, p->batch)) {
             // four-step 2^9-point pass C: one polynomial-major pass of the padded multi-pass
@@ -2384,7 +2522,7 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
             if (a.fin || a.pmul || a.in_ps != p->N || a.in_es != 1) c = alt;   // TMA passes read natural tiles only
         }
         // CTAs that signal each polynomial's counter (a PM CTA signals all of its C polynomials)
-        const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (pm ? 1u : (uint64_t)c.C));
+        const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (pm ? 1u : (uint64_t)c.C * c.tiles));
         if (overlap) set_overlap(p, ctr, a, i, npass, prev_ctas_per_poly);
         if (i == 0 && wait_prev) chain_first(p, ctr, a);
         if (chain && last) chain_last(p, ctr, a, npass, ctas_per_poly, o, bufs);
