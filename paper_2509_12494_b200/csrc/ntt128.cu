@@ -1075,6 +1075,112 @@ k_ntt_first_tl(const __grid_constant__ PassArgs a) {
     }
 }
 
+// ----------------------------------------------------------------------------- later pass, TL polynomials per CTA
+// One-modulus plans (nq == 1): the twiddle set of a later-pass group depends only on its L
+// (and the modulus), so group g of TL consecutive polynomials shares one set -- the same
+// two-tile scheme as k_ntt_first_tl for the later passes of plain cyclic one-modulus plans
+// (BASELINE cfg 4 and 5 shapes).  The CTA signals each of its polynomials' counters once.
+#ifndef NTT_LATER_TILES
+#define NTT_LATER_TILES 2
+#endif
+template <int B, bool SCALE_LAST, int RBMAX, int TL>
+__global__ void __launch_bounds__(PassShape<B, RBMAX>::T,
+                                  (PassOcc<B, RBMAX, false>::THREADS / PassShape<B, RBMAX>::T) > 0
+                                      ? PassOcc<B, RBMAX, false>::THREADS / PassShape<B, RBMAX>::T : 1)
+k_ntt_later_tl(const __grid_constant__ PassArgs a) {
+    constexpr int C = 1;
+    using S = PassShape<B, RBMAX, C, true>;
+    constexpr int G = S::G, RB = S::RB, T = S::T, GS = S::GS;
+    constexpr int LT = B - RB;
+    constexpr int PER = G / T;
+    constexpr bool WARPMAP = T <= 32 && (32 % T) == 0;
+    static_assert(B >= 8, "twiddles by bulk copy");
+    extern __shared__ __align__(128) uint4 sm[];
+    uint4* const dsm = sm;                           // [TL][GS] data tiles
+    uint4* const tsm = dsm + TL * GS;                // the group's twiddle set (shared by the TL polynomials)
+    __shared__ __align__(8) uint64_t tw_bar;
+
+    const uint32_t n = a.n, lo = a.lo, gbits = n - B;
+    const uint64_t N = 1ull << n;
+    const uint64_t gpp = 1ull << gbits;              // groups per polynomial
+    const uint64_t g = blockIdx.x & (gpp - 1);
+    const uint64_t p0 = (uint64_t)(blockIdx.x >> gbits) * TL;   // TL divides the batch
+    const int tid = threadIdx.x;
+    const uint64_t H = g >> lo, L = g & ((1ull << lo) - 1);
+    if (tid == 0) {
+        mbar_init(&tw_bar, 1);
+        mbar_expect_tx(&tw_bar, (G - 1) * 16);
+        bulk_g2s(tsm, a.pt + L * (G - 1), (G - 1) * 16, &tw_bar);
+    }
+    if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.cnt_in) {
+        if (tid < TL) {
+            const uint32_t* cp = a.cnt_in + p0 + tid;
+            while ((int32_t)(ld_acquire_gpu(cp) - a.target) < 0) __nanosleep(128);
+        }
+        __syncthreads();
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // rows t + i T of group (H, L): elements H 2^(lo+B) + (t + i T) 2^lo + L
+    const uint64_t gbase = (H << (lo + B)) | ((uint64_t)tid << lo) | L;
+    const uint64_t gstride = (uint64_t)T << lo;
+#pragma unroll
+    for (int k = 0; k < TL; k++) {
+        const uint4* srcp = a.src + (p0 + k) * N + gbase;
+        uint4* smc = dsm + k * GS;
+#pragma unroll
+        for (int i = 0; i < PER; i++) cp_async16(smc + slot<B, true, RB>(tid + (i << LT)), srcp + (size_t)i * gstride);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const QPar& M = a.qp[0];
+    uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+    const uint32_t qinv0 = M.qinv0;
+    U128 nf = U128{{0, 0, 0, 0}};
+    if (SCALE_LAST) {
+        const uint32_t* src = a.ninv_r ? M.ninv_rm : M.ninv_m;
+        nf = U128{{src[0], src[1], src[2], src[3]}};
+    }
+    const uint32_t sh = (NTT_SHIFT_SCALE && SCALE_LAST && !a.ninv_r && n >= 2) ? n : 0u;
+    const int mode = mode_of(q);
+    const bool last_pass = lo + B == n;
+#pragma unroll
+    for (int k = 0; k < TL; k++) {
+        if (k == 0) asm volatile("cp.async.wait_group %0;" ::"n"(TL - 1) : "memory");
+        else if (k == 1) asm volatile("cp.async.wait_group %0;" ::"n"(TL > 2 ? TL - 2 : 0) : "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (k == 0) mbar_wait(&tw_bar, 0);
+        uint4* gsm = dsm + k * GS;
+        if (mode == MODE_LAZY)
+            pass_rounds<B, C, false, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP, true>(gsm, tsm, tid, lo, n, q, qinv0, nf, sh);
+        else if (mode == MODE_HALF)
+            pass_rounds<B, C, false, SCALE_LAST, RBMAX, MODE_HALF, WARPMAP, true>(gsm, tsm, tid, lo, n, q, qinv0, nf, sh);
+        else
+            pass_rounds<B, C, false, SCALE_LAST, RBMAX, MODE_FULL, WARPMAP, true>(gsm, tsm, tid, lo, n, q, qinv0, nf, sh);
+        if (WARPMAP) __syncthreads();
+        uint4 outv[PER];
+#pragma unroll
+        for (int i = 0; i < PER; i++) outv[i] = gsm[slot<B, true, RB>(tid + (i << LT))];
+        if (last_pass && mode != MODE_FULL) {   // lazy classes leave the transform canonical
+            if (mode == MODE_LAZY) {
+                const uint32_t q2[4] = {q[0] << 1, (q[1] << 1) | (q[0] >> 31), (q[2] << 1) | (q[1] >> 31),
+                                        (q[3] << 1) | (q[2] >> 31)};
+#pragma unroll
+                for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q2));
+            }
+#pragma unroll
+            for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q));
+        }
+        uint4* dstp = a.dst + (p0 + k) * N + gbase;
+#pragma unroll
+        for (int i = 0; i < PER; i++) dstp[(size_t)i * gstride] = outv[i];
+    }
+    if (a.cnt_out) {
+        __syncthreads();
+        if (tid < TL) red_release_gpu_add(a.cnt_out + p0 + tid, 1u);
+    }
+}
+
 // ----------------------------------------------------------------------------- permutation-free negacyclic passes
 // SURVEY §8(f) f1 (DESIGN.md §6 "Bit-reversed negacyclic path").  Forward: Cooley-Tukey
 // butterflies with psi-merged twiddles, natural-order input, stages from the top index
@@ -1426,7 +1532,8 @@ struct PassCfg {
     bool tma = false;     // k_ntt_pass<..., TMA>: the launch must carry the data tile's tensor map
     bool first = false;
     bool single = false;  // one-pass kernel (several moduli per CTA: the device table, not QPar)
-    int tiles = 1;        // groups per CTA beyond C, handled one after another (k_ntt_first_tl)
+    int tiles = 1;        // groups per CTA beyond C, handled one after another (k_ntt_first_tl / k_ntt_later_tl)
+    bool tiles_across = false;   // the tiles are one group of `tiles` polynomials (k_ntt_later_tl)
 };
 
 template <int B, int C, bool FIRST, bool SCALE_LAST, bool SINGLE = false, int RBMAX = 3, bool PM = false, bool TMA = false>
@@ -1456,6 +1563,21 @@ static PassCfg first_tl_cfg_t() {
     c.threads = S::T;
     c.first = true;
     c.tiles = TL;
+    c.smem = ((size_t)TL * S::GS + S::TS) * sizeof(uint4);
+    return c;
+}
+
+// later pass over group g of TL polynomials per CTA (k_ntt_later_tl): one-modulus plain cyclic plans
+template <int B, bool SL, int RB, int TL>
+static PassCfg later_tl_cfg_t() {
+    using S = PassShape<B, RB, 1, true>;
+    PassCfg c;
+    c.fn = k_ntt_later_tl<B, SL, RB, TL>;
+    c.B = B;
+    c.C = 1;
+    c.threads = S::T;
+    c.tiles = TL;
+    c.tiles_across = true;
     c.smem = ((size_t)TL * S::GS + S::TS) * sizeof(uint4);
     return c;
 }
@@ -2458,6 +2580,15 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
                 if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
                     return NTT128_ERR_CUDA;
             }
+            // one-modulus plans: a later 8-stage pass takes group g of NTT_LATER_TILES polynomials per CTA
+            if (NTT_LATER_TILES > 1 && i > 0 && !c.single && c.C == 1 && B == 8 && p->nq == 1 && !o.io && !o.pmul &&
+                p->kind == 0 && p->batch % NTT_LATER_TILES == 0 && !switches().no_tiles) {
+                const bool sl = scale_last && i + 1 == npass;
+                c = sl ? later_tl_cfg_t<8, true, NTT_RB8, (NTT_LATER_TILES > 1 ? NTT_LATER_TILES : 2)>()
+                       : later_tl_cfg_t<8, false, NTT_RB8, (NTT_LATER_TILES > 1 ? NTT_LATER_TILES : 2)>();
+                if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
+                    return NTT128_ERR_CUDA;
+            }
         }
         bool pm = false;
         if (i == 0 && o.io && npass == 1 && B == 9 && o.io->in_ps == 1 && strided_pm_first(B, p->batch)) {
@@ -2522,7 +2653,8 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
             if (a.fin || a.pmul || a.in_ps != p->N || a.in_es != 1) c = alt;   // TMA passes read natural tiles only
         }
         // CTAs that signal each polynomial's counter (a PM CTA signals all of its C polynomials)
-        const uint32_t ctas_per_poly = (uint32_t)(((uint64_t)1 << (n - B)) / (pm ? 1u : (uint64_t)c.C * c.tiles));
+        const uint32_t ctas_per_poly =
+            (uint32_t)(((uint64_t)1 << (n - B)) / (pm ? 1u : (uint64_t)c.C * (c.tiles_across ? 1 : c.tiles)));
         if (overlap) set_overlap(p, ctr, a, i, npass, prev_ctas_per_poly);
         if (i == 0 && wait_prev) chain_first(p, ctr, a);
         if (chain && last) chain_last(p, ctr, a, npass, ctas_per_poly, o, bufs);
