@@ -322,7 +322,7 @@ def run_gpu(args):
     fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     inv_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
 
-    # dominant kernel: the NTT pass kernel (k_ntt_pass); one launch = one pass over the batch.
+    # dominant kernels: the NTT pass kernels (k_ntt_first_tl, k_ntt_pass); one launch = one pass over the batch.
     # Its average launch duration over the timed region = local step time / launches per step
     # (the step is nothing but these launches, overlapped back to back).
     npasses = plan.info()["num_passes"]
@@ -338,7 +338,8 @@ def run_gpu(args):
             traffic_src = "capture, not measured in this run: " + tj.get("source", TRAFFIC_PATH)
         except Exception:
             traffic = None
-    roofline = {"bound": "alu", "kernel": "k_ntt_pass", "achieved": round(achieved, 4), "peak": round(pk["tprod_s"], 4),
+    roofline = {"bound": "alu", "kernel": "NTT pass kernels (k_ntt_first_tl first passes, k_ntt_pass later passes)",
+                "achieved": round(achieved, 4), "peak": round(pk["tprod_s"], 4),
                 "unit": "Tprod/s", "frac": round(achieved / pk["tprod_s"], 4), "traffic": traffic,
                 "traffic_src": traffic_src, "peak_src": pk["tprod_src"],
                 "step_frac": round(value / world * P_BUTTERFLY / 1e12 / pk["tprod_s"], 4)}

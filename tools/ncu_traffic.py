@@ -1,4 +1,4 @@
-"""Write profiles/ncu_traffic.json: DRAM bytes (read + write) per k_ntt_pass launch from an
+"""Write profiles/ncu_traffic.json: DRAM bytes (read + write) per NTT pass launch from an
 `ncu --set full` capture of `bench.py` (the roofline object's "traffic")."""
 import csv
 import json
@@ -14,7 +14,7 @@ def main(rep, out, tag):
     rows = []
     for row in r[2:]:
         name = row[hdr.index("Kernel Name")]
-        if "k_ntt_pass" not in name:
+        if "k_ntt_pass" not in name and "k_ntt_first_tl" not in name and "k_ntt_later_tl" not in name:
             continue
         rd = float(row[hdr.index("dram__bytes_read.sum")])
         wr = float(row[hdr.index("dram__bytes_write.sum")])
