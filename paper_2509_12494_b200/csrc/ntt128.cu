@@ -978,7 +978,10 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
 #define NTT_FIRST_TILES 2
 #endif
 #ifndef NTT_FIRST_TILES9
-#define NTT_FIRST_TILES9 1    // 9-stage first passes (radix-8 rounds)
+#define NTT_FIRST_TILES9 2    // 9-stage first passes: two tiles with radix-4 rounds (128 threads, 64
+#endif                        // registers, 8 CTAs per SM) +0.7..0.8 % at 2^15 / 2^17; with the radix-8
+#ifndef NTT_FIRST9_RB         // rounds (80 registers) shared memory caps residency: -2.6 % (first_tiles_ab)
+#define NTT_FIRST9_RB 2
 #endif
 template <int B, int RBMAX, int TL>
 __global__ void __launch_bounds__(PassShape<B, RBMAX>::T,
@@ -2576,7 +2579,7 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
             if (tl > 1 && i == 0 && npass > 1 && c.first && !c.single && !c.tma && c.C == 1 && !o.io && !o.pmul &&
                 p->kind == 0 && ((1ull << (n - B)) % tl) == 0 && !switches().no_tiles) {
                 c = B == 8 ? first_tl_cfg_t<8, NTT_RB8, (NTT_FIRST_TILES > 1 ? NTT_FIRST_TILES : 2)>()
-                           : first_tl_cfg_t<9, NTT_RB9, (NTT_FIRST_TILES9 > 1 ? NTT_FIRST_TILES9 : 2)>();
+                           : first_tl_cfg_t<9, NTT_FIRST9_RB, (NTT_FIRST_TILES9 > 1 ? NTT_FIRST_TILES9 : 2)>();
                 if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
                     return NTT128_ERR_CUDA;
             }
