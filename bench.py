@@ -551,41 +551,28 @@ def run_rows(args, P, pk, stream, rank, world):
         del p5, xx, yy, zz
         torch.cuda.empty_cache()
         rows.update(run_cfg5_fourstep(args, P, rank, world))
-    # 256-bit moduli, N = 2^16 x 32 forward + inverse per rank (largest prime
-    # < 2^256 with q = 1 mod 2^21); roofline P = 136 word products per butterfly
-    e = P["w256"]["b256"]
-    q = hexint(e["q"])
-    w = pow(hexint(e["omega"]), 1 << (e["logn"] - 16), q)
-    p6 = N.Plan256(16, q, w, batch=32)
-    xx = torch.from_numpy(synth.uniform_residues_w(q, 32 << 16, synth.stream_seed(10, 0, 16))
-                          .reshape(32, 1 << 16, 4).view(np.int64)).cuda()
-    yy, zz = torch.empty_like(xx), torch.empty_like(xx)
-    p6.forward(xx, out=yy); p6.inverse(yy, out=zz)
-    torch.cuda.synchronize()
-    assert torch.equal(zz, xx)
-    ms = timed_rank(lambda i: (p6.forward(xx, out=yy), p6.inverse(yy, out=zz)), 10, world)
-    bf = 2 * 32 * (1 << 15) * 16 / (ms * 1e-3)
-    rows["f4_ntt256_n2^16_x32_butterflies_per_s"] = bf * world
-    rows["f4_ntt256_roofline_frac"] = bf * 136 / (pk["tprod_s"] * 1e12)
-    del p6, xx, yy, zz
-    torch.cuda.empty_cache()
-    # 192-bit moduli (q < 2^192: the 6-word kernels, 72 + 6 = 78 word products per butterfly)
-    e = P["w256"]["b192"]
-    q = hexint(e["q"])
-    w = pow(hexint(e["omega"]), 1 << (e["logn"] - 16), q)
-    p7 = N.Plan256(16, q, w, batch=32)
-    xx = torch.from_numpy(synth.uniform_residues_w(q, 32 << 16, synth.stream_seed(10, 0, 17))
-                          .reshape(32, 1 << 16, 4).view(np.int64)).cuda()
-    yy, zz = torch.empty_like(xx), torch.empty_like(xx)
-    p7.forward(xx, out=yy); p7.inverse(yy, out=zz)
-    torch.cuda.synchronize()
-    assert torch.equal(zz, xx)
-    ms = timed_rank(lambda i: (p7.forward(xx, out=yy), p7.inverse(yy, out=zz)), 10, world)
-    bf = 2 * 32 * (1 << 15) * 16 / (ms * 1e-3)
-    rows["f4_ntt192_n2^16_x32_butterflies_per_s"] = bf * world
-    rows["f4_ntt192_roofline_frac"] = bf * 78 / (pk["tprod_s"] * 1e12)
-    del p7, xx, yy, zz
-    torch.cuda.empty_cache()
+    # wider moduli, N = 2^16 x 32 forward + inverse per rank: the largest prime
+    # < 2^b with q = 1 mod 2^21 for b = 256 (8 words, canonical), 254 (8 words, lazy class q < R/4),
+    # 192 (6 words, canonical), 190 (6 words, lazy); roofline P = 136 (8 words: 128 + 8) or 78
+    # (6 words: 72 + 6) word products per butterfly.  Row names keep the round-2 keys for b256 / b192.
+    for key, name, P_w, sk in (("b256", "ntt256", 136, 16), ("b254", "ntt254_lazy", 136, 18),
+                               ("b192", "ntt192", 78, 17), ("b190", "ntt190_lazy", 78, 19)):
+        e = P["w256"][key]
+        q = hexint(e["q"])
+        w = pow(hexint(e["omega"]), 1 << (e["logn"] - 16), q)
+        p6 = N.Plan256(16, q, w, batch=32)
+        xx = torch.from_numpy(synth.uniform_residues_w(q, 32 << 16, synth.stream_seed(10, 0, sk))
+                              .reshape(32, 1 << 16, 4).view(np.int64)).cuda()
+        yy, zz = torch.empty_like(xx), torch.empty_like(xx)
+        p6.forward(xx, out=yy); p6.inverse(yy, out=zz)
+        torch.cuda.synchronize()
+        assert torch.equal(zz, xx)
+        ms = timed_rank(lambda i: (p6.forward(xx, out=yy), p6.inverse(yy, out=zz)), 10, world)
+        bf = 2 * 32 * (1 << 15) * 16 / (ms * 1e-3)
+        rows[f"f4_{name}_n2^16_x32_butterflies_per_s"] = bf * world
+        rows[f"f4_{name}_roofline_frac"] = bf * P_w / (pk["tprod_s"] * 1e12)
+        del p6, xx, yy, zz
+        torch.cuda.empty_cache()
     return rows
 
 

@@ -10,8 +10,9 @@
 // (Montgomery form), stage-0 butterflies without a multiply, N^-1 folded into the
 // inverse's last stage.  One group per CTA, radix-4 register rounds (4 elements x 8 words
 // per thread), a 32-byte residue kept as two 16-byte planes in shared memory so every
-// 8-lane phase touches distinct banks (slot l + l/8, as in the 128-bit kernels).  All
-// values canonical (no lazy classes yet).
+// 8-lane phase touches distinct banks (slot l + l/8, as in the 128-bit kernels).  Values
+// canonical, except in plans whose moduli are all < R/4 (the lazy class, template LZ: [0, 4q)
+// between stages, Harvey butterflies, canonicalised in the last pass's store).
 // Word count W (template parameter): plans and vec256_mul whose moduli are all < 2^192 run
 // the 6-word arithmetic (Montgomery R = 2^192, 72 + 6 word products per product instead of
 // 128 + 8); storage stays 32 bytes per residue with the top limb zero.
@@ -82,6 +83,16 @@ inline H256 h_powmod(const H256& a, const H256& e, const H256& q) {
     }
     return r;
 }
+inline H256 h_add_nc(const H256& a, const H256& b) {   // a + b < 2^256
+    H256 r;
+    unsigned __int128 c = 0;
+    for (int i = 0; i < 4; i++) {
+        const unsigned __int128 t = (unsigned __int128)a.w[i] + b.w[i] + (uint64_t)c;
+        r.w[i] = (uint64_t)t;
+        c = t >> 64;
+    }
+    return r;
+}
 inline H256 h_shr1(const H256& a) {
     H256 r;
     for (int i = 0; i < 3; i++) r.w[i] = (a.w[i] >> 1) | (a.w[i + 1] << 63);
@@ -127,6 +138,7 @@ struct ModC256 {
     uint32_t one_m[8];    // R mod q
     uint32_t r2[8];       // R^2 mod q
     uint32_t ninv_m[8];   // N^-1 R mod q
+    uint32_t q2[8];       // 2q (lazy class only: q < R / 4)
 };
 
 struct E256 {
@@ -170,6 +182,49 @@ __device__ __forceinline__ void subm(const E256& a, const E256& b, const ModC256
         sub_mod192(a.w, b.w, M.q, r.w);
         r.w[6] = r.w[7] = 0;
     }
+}
+// Lazy class (every modulus < R / 4 = 2^(32 W - 2)): values in [0, 4q) between stages and
+// Harvey butterflies, as the 128-bit LAZY class; bounds checked by
+// tools/model/mont_eo_model_w.py (check_lazy).
+template <int W>
+__device__ __forceinline__ E256 mmul_lazy(const E256& a, const E256& b, const ModC256& M) {
+    E256 r;
+    if (W == 8) {
+        mont_mul256_lazy(a.w, b.w, M.q, M.qinv0, r.w);
+    } else {
+        mont_mul192_lazy(a.w, b.w, M.q, M.qinv0, r.w);
+        r.w[6] = r.w[7] = 0;
+    }
+    return r;
+}
+template <int W>
+__device__ __forceinline__ void add_nr(const E256& a, const E256& b, E256& r) {
+    if (W == 8) {
+        add_nored256(a.w, b.w, r.w);
+    } else {
+        add_nored192(a.w, b.w, r.w);
+        r.w[6] = r.w[7] = 0;
+    }
+}
+template <int W>
+__device__ __forceinline__ void sub_add_nr(const E256& a, const E256& b, const uint32_t c[8], E256& r) {
+    if (W == 8) {
+        sub_add_nored256(a.w, b.w, c, r.w);
+    } else {
+        sub_add_nored192(a.w, b.w, c, r.w);
+        r.w[6] = r.w[7] = 0;
+    }
+}
+template <int W>
+__device__ __forceinline__ E256 red_c(const E256& a, const uint32_t c[8]) {
+    E256 r;
+    if (W == 8) {
+        reduce_c256(a.w, c, r.w);
+    } else {
+        reduce_c192(a.w, c, r.w);
+        r.w[6] = r.w[7] = 0;
+    }
+    return r;
 }
 __device__ __forceinline__ uint32_t brev_n(uint32_t x, int bits) { return bits == 0 ? 0u : (__brev(x) >> (32 - bits)); }
 // u 2^-s mod q (1 <= s <= 31, u < q): one s-bit Montgomery digit, as shr_mod in arith128.cuh --
@@ -273,7 +328,7 @@ struct Shape256 {
 #ifndef NTT256_MINB8
 #define NTT256_MINB8 1
 #endif
-template <int B, bool FIRST, bool SCALE_LAST, int W>
+template <int B, bool FIRST, bool SCALE_LAST, int W, bool LZ>
 __global__ void __launch_bounds__(Shape256<B>::C * Shape256<B>::T, W == 6 ? NTT256_MINB6 : NTT256_MINB8)
 k_ntt256_pass(const __grid_constant__ Pass256Args a) {
     using S = Shape256<B>;
@@ -346,6 +401,20 @@ k_ntt256_pass(const __grid_constant__ Pass256Args a) {
                     const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
                     const int k1 = k0 | (1 << bit);
                     E256 v = x[k1], u = x[k0];
+                    if (LZ) {                // Harvey: u' in [0, 2q), t in [0, 2q); u' + t, u' - t + 2q
+                        E256 t = v, us = u;  // stage 0 of a first pass: canonical inputs, twiddle 1
+                        if (!trivial) {
+                            const int ti = (1 << sl) - 1 + tlo + ((kk & ((1 << bit) - 1)) << w);
+                            t = mmul_lazy<W>(v, e_from<W>(twl[ti], twh[ti]), M);
+                            if (last) us = (NTT256_SHIFT_SCALE && n >= 1) ? shr256<W>(u, n, M)
+                                                                        : mmul<W>(u, E256{{M.ninv_m[0], M.ninv_m[1], M.ninv_m[2], M.ninv_m[3], M.ninv_m[4],
+                                                                                           M.ninv_m[5], M.ninv_m[6], M.ninv_m[7]}}, M);
+                            else us = red_c<W>(u, M.q2);
+                        }
+                        add_nr<W>(us, t, x[k0]);
+                        sub_add_nr<W>(us, t, M.q2, x[k1]);
+                        continue;
+                    }
                     if (!trivial) {
                         const int ti = (1 << sl) - 1 + tlo + ((kk & ((1 << bit) - 1)) << w);
                         v = mmul<W>(v, e_from<W>(twl[ti], twh[ti]), M);
@@ -368,6 +437,17 @@ k_ntt256_pass(const __grid_constant__ Pass256Args a) {
     };
     if (a.nq == 1) rounds(a.mc0);
     else rounds(a.mods[m]);
+    if (LZ && lo + B == n) {   // the transform's last pass: [0, 4q) -> canonical [0, q) before the store
+        const ModC256& M = a.nq == 1 ? a.mc0 : a.mods[m];
+#pragma unroll
+        for (int i = 0; i < E; i++) {
+            const int s = slot256(t + i * T);
+            const E256 v = red_c<W>(red_c<W>(e_from<W>(glo[s], ghi[s]), M.q2), M.q);
+            glo[s] = e_lo(v);
+            ghi[s] = e_hi(v);
+        }
+        __syncthreads();
+    }
     if (!live) return;
     // store: the first pass writes the group as contiguous rows (natural order within it)
     if (FIRST) {
@@ -400,21 +480,24 @@ __global__ void k_vmul256(uint4* z, const uint4* x, const uint4* y, uint64_t n, 
 }
 
 typedef void (*Pass256Fn)(const Pass256Args);
-template <bool FIRST, bool SL, int W>
+template <bool FIRST, bool SL, int W, bool LZ>
 Pass256Fn pass256_fn_w(int B) {
     switch (B) {
-        case 1: return k_ntt256_pass<1, FIRST, SL, W>;
-        case 2: return k_ntt256_pass<2, FIRST, SL, W>;
-        case 3: return k_ntt256_pass<3, FIRST, SL, W>;
-        case 4: return k_ntt256_pass<4, FIRST, SL, W>;
-        case 5: return k_ntt256_pass<5, FIRST, SL, W>;
-        case 6: return k_ntt256_pass<6, FIRST, SL, W>;
-        case 7: return k_ntt256_pass<7, FIRST, SL, W>;
-        default: return k_ntt256_pass<8, FIRST, SL, W>;
+        case 1: return k_ntt256_pass<1, FIRST, SL, W, LZ>;
+        case 2: return k_ntt256_pass<2, FIRST, SL, W, LZ>;
+        case 3: return k_ntt256_pass<3, FIRST, SL, W, LZ>;
+        case 4: return k_ntt256_pass<4, FIRST, SL, W, LZ>;
+        case 5: return k_ntt256_pass<5, FIRST, SL, W, LZ>;
+        case 6: return k_ntt256_pass<6, FIRST, SL, W, LZ>;
+        case 7: return k_ntt256_pass<7, FIRST, SL, W, LZ>;
+        default: return k_ntt256_pass<8, FIRST, SL, W, LZ>;
     }
 }
 template <bool FIRST, bool SL>
-Pass256Fn pass256_fn(int B, int W) { return W == 6 ? pass256_fn_w<FIRST, SL, 6>(B) : pass256_fn_w<FIRST, SL, 8>(B); }
+Pass256Fn pass256_fn(int B, int W, bool lz) {
+    if (W == 6) return lz ? pass256_fn_w<FIRST, SL, 6, true>(B) : pass256_fn_w<FIRST, SL, 6, false>(B);
+    return lz ? pass256_fn_w<FIRST, SL, 8, true>(B) : pass256_fn_w<FIRST, SL, 8, false>(B);
+}
 
 std::vector<int> pass_bits256(int n) {
     std::vector<int> b;
@@ -425,6 +508,11 @@ std::vector<int> pass_bits256(int n) {
 
 // words of the Montgomery radix R = 2^(32 W): 6 when q < 2^192, else 8
 inline int words_for(const H256& q) { return q.w[3] == 0 ? 6 : 8; }   // 64-bit limbs: q < 2^192
+// lazy class of a W-word plan: q < R / 4 = 2^(32 W - 2) (4q fits the W words)
+#ifndef NTT256_LAZY
+#define NTT256_LAZY 1         // 0: every plan canonical (A/B experiment build)
+#endif
+inline bool lazy_ok(const H256& q, int W) { return NTT256_LAZY && (q.w[W / 2 - 1] >> 62) == 0; }
 
 ModC256 make_modc(const H256& q, uint64_t N, int W) {
     ModC256 c;
@@ -439,6 +527,7 @@ ModC256 make_modc(const H256& q, uint64_t N, int W) {
     for (int i = 0; i < 32 * W; i++) r2 = h_addmod(r2, r2, q);
     h_words(r, c.one_m);
     h_words(r2, c.r2);
+    if (!(q.w[3] >> 63)) h_words(h_add_nc(q, q), c.q2);   // 2q < 2^256
     if (N > 1) {
         const H256 ninv = h_powmod(h_from(N), h_sub(q, h_from(2)), q);
         h_words(h_mulmod(ninv, r, q), c.ninv_m);
@@ -451,6 +540,7 @@ ModC256 make_modc(const H256& q, uint64_t N, int W) {
 struct ntt256_plan_s {
     uint32_t log2n, batch, nq;
     int words;                          // 6 (every modulus < 2^192) or 8
+    bool lazy;                          // every modulus < 2^(32 words - 2): lazy class (values in [0, 4q))
     int device;
     uint64_t N;
     std::vector<int> bits;
@@ -551,6 +641,9 @@ extern "C" ntt128_status ntt256_plan_create(ntt256_plan_t* out, uint32_t log2n, 
     for (auto& q : qs)
         if (words_for(q) == 8) p->words = 8;
     const int W = p->words;
+    p->lazy = true;
+    for (auto& q : qs)
+        if (!lazy_ok(q, W)) p->lazy = false;
     ntt128_status st = NTT128_OK;
     std::vector<ModC256> mc;
     for (auto& q : qs) mc.push_back(make_modc(q, N, W));
@@ -609,8 +702,9 @@ static ntt128_status run256(ntt256_plan_s* p, const uint4* src, uint4* dst, cuda
     for (size_t i = 0; i < np; i++) {
         const int B = p->bits[i];
         const bool first = i == 0, sl = inverse && i + 1 == np;
-        Pass256Fn fn = first ? (sl ? pass256_fn<true, true>(B, p->words) : pass256_fn<true, false>(B, p->words))
-                             : (sl ? pass256_fn<false, true>(B, p->words) : pass256_fn<false, false>(B, p->words));
+        const bool lz = p->lazy;
+        Pass256Fn fn = first ? (sl ? pass256_fn<true, true>(B, p->words, lz) : pass256_fn<true, false>(B, p->words, lz))
+                             : (sl ? pass256_fn<false, true>(B, p->words, lz) : pass256_fn<false, false>(B, p->words, lz));
         Pass256Args a;
         memset(&a, 0, sizeof(a));
         a.src = first ? src : dst;

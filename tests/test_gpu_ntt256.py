@@ -1,7 +1,9 @@
 """GPU parity of the wider-modulus path (ntt256_*, vec256_mul) against
 the 256-bit oracle (oracle/oracle256.c), bit-exact: single-pass sizes, two- and three-pass
-schedules, 256/255/254/192-bit primes (moduli < 2^192 run the 6-word arithmetic), several
-moduli per batch, structured inputs, in place, and the plan's argument checks."""
+schedules, 256/255/254/192/190-bit primes (moduli < 2^192 run the 6-word arithmetic; plans whose
+moduli are all < R/4 -- b254 on 8 words, b190 on 6 -- run the lazy class, values in [0, 4q)
+between stages), several moduli per batch, structured inputs, in place, and the plan's
+argument checks."""
 import numpy as np
 import pytest
 
@@ -44,27 +46,28 @@ def run(N, qs, ws, logn, x):
 
 @pytest.mark.parametrize("logn", [1, 2, 3, 5, 8, 9, 11, 13, 16])
 def test_ntt256_sizes(N, params, logn):
-    for key in ("b256", "b192"):
+    for key in ("b256", "b192", "b254", "b190"):
         e = params["w256"][key]
         x = synth.uniform_residues_w(e["q"], 2 << logn, 2000 + logn).reshape(2, 1 << logn, 4)
         run(N, [e["q"]], [root(e, logn)], logn, x)
 
 
-@pytest.mark.parametrize("key", ["b255", "b192"])
+@pytest.mark.parametrize("key", ["b255", "b192", "b254", "b190"])
 def test_ntt256_three_pass(N, params, key):
-    """three passes (6 + 6 + 6); b192 (q < 2^192) runs the 6-word kernels"""
+    """three passes (6 + 6 + 6); b192 (q < 2^192) runs the 6-word kernels, b254 / b190 the
+    lazy class (two passes on [0, 4q) values before the canonicalising last pass)"""
     e = params["w256"][key]
     logn = 18
     x = synth.uniform_residues_w(e["q"], 1 << logn, 2100).reshape(1, 1 << logn, 4)
     run(N, [e["q"]], [root(e, logn)], logn, x)
 
 
-def test_ntt192_structured_and_in_place(N, params):
-    """6-word plans: delta -> ones, all q-1, in place, and a 6-word / 8-word pair of plans on
-    the same data agreeing (the same transform through R = 2^192 and R = 2^256 arithmetic is
-    covered by the oracle on both sides)"""
+@pytest.mark.parametrize("key", ["b192", "b190", "b254"])
+def test_ntt192_structured_and_in_place(N, params, key):
+    """6-word plans (b192 canonical, b190 lazy) and the 8-word lazy class (b254): delta ->
+    ones, all q-1 (the largest values every stage can see), in place"""
     import torch
-    e = params["w256"]["b192"]
+    e = params["w256"][key]
     q, logn = e["q"], 11
     n = 1 << logn
     x = np.stack([O4.to_array([1] + [0] * (n - 1)), O4.to_array([q - 1] * n),
@@ -92,6 +95,19 @@ def test_ntt256_many_moduli_and_structured(N, params):
     plan = N.Plan256(logn, qs, ws, batch=4)
     y = host(plan.forward(dev(x)))
     assert O4.to_ints(y[1]) == [1] * n                       # delta -> ones
+
+
+@pytest.mark.parametrize("logn", [9, 12, 17])
+def test_ntt256_lazy_many_moduli(N, params, logn):
+    """a lazy 8-word plan with several moduli (b254, b192, b190 < 2^254: moduli from the device
+    table, not the kernel parameter), 1-3 passes, all-(q-1) and uniform rows"""
+    keys = ["b254", "b192", "b190"]
+    qs = [params["w256"][k]["q"] for k in keys]
+    ws = [root(params["w256"][k], logn) for k in keys]
+    n = 1 << logn
+    x = np.stack([O4.to_array([qs[0] - 1] * n), synth.uniform_residues_w(qs[1], n, 2600 + logn),
+                  synth.uniform_residues_w(qs[2], n, 2700 + logn)])
+    run(N, qs, ws, logn, x)
 
 
 def test_ntt256_in_place(N, params):

@@ -15,7 +15,7 @@ import synth  # noqa: E402
 P = json.load(open("tests/golden/params.json"))
 import os  # noqa: E402
 KEY = os.environ.get("PRIME", "b256")
-PROD = 78 if KEY == "b192" else 136
+PROD = 78 if KEY in ("b192", "b190") else 136
 e = P["w256"][KEY]
 q, L = int(e["q"], 16), e["logn"]
 for logn in [int(v) for v in sys.argv[1].split(",")]:

@@ -28,16 +28,21 @@ def asm_block(lines, outs, ins):
     return f"    asm({body.rstrip()}\n        : {o}\n        : {i});\n"
 
 
-def gen_mont(W):
+def gen_mont(W, lazy=False):
     H = W // 2
     NB = 32 * W
+    sfx = "_lazy" if lazy else ""
     s = []
-    s.append(f"// Montgomery product a b 2^-{NB} mod q, canonical result (a < 2^{NB}, b < q, q odd < 2^{NB}).\n"
+    if lazy:
+        s.append(f"// Lazy Montgomery product (q < 2^{NB - 2}): T = a b 2^-{NB} + {{0, q}} in [0, 2q), no final subtraction.\n"
+                 f"// T = (a b + m q) / R < q (a / R) + q < 2q for any a < R; 2q < 2^{NB - 1}, so T's word {W} is zero\n"
+                 f"// (tools/model/mont_eo_model_w.py checks both on a < 4q).  Same digit loop as mont_mul{NB}.\n")
+    s.append(("" if lazy else f"// Montgomery product a b 2^-{NB} mod q, canonical result (a < 2^{NB}, b < q, q odd < 2^{NB}).\n") +
              "// Even/odd alternating CIOS over 32-bit digits of b: 2^32 T_i = X + 2^32 Y, X holding the\n"
              "// products at even word positions, Y at odd ones (register-pair aligned); after a digit\n"
              "// X_0 = 0 and the shift is a change of roles (X' = Y + X_1, Y' = X / 2^64 + ...).  Per\n"
              f"// digit {2 * W} IMAD.WIDE + 1 IMAD; {2 * W * W} + {W} word products in all.\n")
-    s.append(f"__device__ __forceinline__ void mont_mul{NB}(const uint32_t a[{W}], const uint32_t b[{W}], const uint32_t q[{W}],\n"
+    s.append(f"__device__ __forceinline__ void mont_mul{NB}{sfx}(const uint32_t a[{W}], const uint32_t b[{W}], const uint32_t q[{W}],\n"
              f"                                            uint32_t qinv0, uint32_t r[{W}]) {{\n")
     s.append(f"    uint32_t x[{W + 1}], y[{W + 1}], n[{W + 1}], m;\n")
     # digit 0
@@ -85,6 +90,16 @@ def gen_mont(W):
     s.append("    " + red_chain("y", 0, False).replace("\n    ", "\n        ").lstrip())
     s.append("    " + red_chain("n", 1, True).replace("\n    ", "\n        ").lstrip())
     s.append(f"#pragma unroll\n        for (int k = 0; k < {W + 1}; k++) {{ x[k] = y[k]; y[k] = n[k]; }}\n    }}\n")
+    if lazy:   # final: T = Y + X / 2^32 in W words (T < 2q < 2^(NB-1): no carry out)
+        lines = ["add.cc.u32 {r0}, {y0}, {x1}"]
+        for k in range(1, W - 1):
+            lines.append(f"addc.cc.u32 {{r{k}}}, {{y{k}}}, {{x{k+1}}}")
+        lines.append(f"addc.u32 {{r{W-1}}}, {{y{W-1}}}, {{x{W}}}")
+        outs = [("=r", f"r[{i}]", f"r{i}") for i in range(W)]
+        ins = [("r", f"y[{i}]", f"y{i}") for i in range(W)] + [("r", f"x[{i}]", f"x{i}") for i in range(1, W + 1)]
+        s.append(asm_block(lines, outs, ins))
+        s.append("}\n\n")
+        return "".join(s)
     # final: T = Y + X / 2^32, then T - q if T >= q (T < 2q, NB + 1 bits)
     lines = ["add.cc.u32 t0, {y0}, {x1}"]
     for k in range(1, W):
@@ -140,16 +155,55 @@ def gen_addsub(W):
     return "".join(s)
 
 
+def gen_lazy(W):
+    """Harvey-butterfly helpers for the lazy class (q < 2^(NB-2), values in [0, 4q))"""
+    NB = 32 * W
+    s = []
+    outs = [("=r", f"r[{i}]", f"r{i}") for i in range(W)]
+    # r = a + b, no reduction (caller: a + b < 2^NB)
+    lines = ["add.cc.u32 {r0}, {a0}, {b0}"] + [f"addc.cc.u32 {{r{k}}}, {{a{k}}}, {{b{k}}}" for k in range(1, W - 1)] + \
+            [f"addc.u32 {{r{W-1}}}, {{a{W-1}}}, {{b{W-1}}}"]
+    ins = [("r", f"a[{i}]", f"a{i}") for i in range(W)] + [("r", f"b[{i}]", f"b{i}") for i in range(W)]
+    s.append(f"// r = a + b without reduction (lazy class: a < 2q, b < 2q, r < 4q < 2^{NB})\n")
+    s.append(f"__device__ __forceinline__ void add_nored{NB}(const uint32_t a[{W}], const uint32_t b[{W}], uint32_t r[{W}]) {{\n"
+             + asm_block(lines, outs, ins) + "}\n\n")
+    # r = a + c - b  (c = 2q; a < 2q, b < 2q: r in (0, 4q))
+    regs = ", ".join(f"s{k}" for k in range(W))
+    lines = ["{", f".reg .u32 {regs}", "add.cc.u32 s0, {a0}, {c0}"] + \
+            [f"addc.cc.u32 s{k}, {{a{k}}}, {{c{k}}}" for k in range(1, W - 1)] + [f"addc.u32 s{W-1}, {{a{W-1}}}, {{c{W-1}}}"] + \
+            ["sub.cc.u32 {r0}, s0, {b0}"] + [f"subc.cc.u32 {{r{k}}}, s{k}, {{b{k}}}" for k in range(1, W - 1)] + \
+            [f"subc.u32 {{r{W-1}}}, s{W-1}, {{b{W-1}}}", "}"]
+    ins = [("r", f"a[{i}]", f"a{i}") for i in range(W)] + [("r", f"b[{i}]", f"b{i}") for i in range(W)] + \
+          [("r", f"c[{i}]", f"c{i}") for i in range(W)]
+    s.append(f"// r = a - b + c without reduction (lazy class, c = 2q: a, b < 2q, r in (0, 4q))\n")
+    s.append(f"__device__ __forceinline__ void sub_add_nored{NB}(const uint32_t a[{W}], const uint32_t b[{W}], const uint32_t c[{W}],\n"
+             f"                                                 uint32_t r[{W}]) {{\n" + asm_block(lines, outs, ins) + "}\n\n")
+    # r = a mod c for a < 2c (c = 2q or q): d = a - c; r = d + (c & borrow)
+    regs = ", ".join([f"d{k}" for k in range(W)] + ["bw"] + [f"m{k}" for k in range(W)])
+    lines = ["{", f".reg .u32 {regs}", "sub.cc.u32 d0, {a0}, {c0}"] + \
+            [f"subc.cc.u32 d{k}, {{a{k}}}, {{c{k}}}" for k in range(1, W)] + ["subc.u32 bw, 0, 0"] + \
+            [f"and.b32 m{k}, {{c{k}}}, bw" for k in range(W)] + ["add.cc.u32 {r0}, d0, m0"] + \
+            [f"addc.cc.u32 {{r{k}}}, d{k}, m{k}" for k in range(1, W - 1)] + [f"addc.u32 {{r{W-1}}}, d{W-1}, m{W-1}", "}"]
+    ins = [("r", f"a[{i}]", f"a{i}") for i in range(W)] + [("r", f"c[{i}]", f"c{i}") for i in range(W)]
+    s.append(f"// r = a mod c for a < 2c (one conditional subtraction: c = 2q takes [0, 4q) to [0, 2q), c = q [0, 2q) to [0, q))\n")
+    s.append(f"__device__ __forceinline__ void reduce_c{NB}(const uint32_t a[{W}], const uint32_t c[{W}], uint32_t r[{W}]) {{\n"
+             + asm_block(lines, outs, ins) + "}\n\n")
+    return "".join(s)
+
+
 def main():
     w6 = ("// ---- 192-bit moduli (6 words, R = 2^192): the same generator at W = 6, used by plans whose\n"
           "// moduli are all < 2^192 (residues still stored in 32-byte slots, top limb zero).\n\n")
     head = ("// arith256_gen.cuh -- GENERATED by tools/gen_arith256.py; do not edit by hand.\n"
             "// 256-bit (8 x 32-bit word) modular arithmetic for sm_100a (SURVEY.md §8(f) f4: wider\n"
             "// multi-word moduli, the paper's stated generalisation, PAPER.md:807-808).  Any odd\n"
-            "// q < 2^256; residues canonical (< q) at every interface.\n"
+            "// q < 2^256; residues canonical (< q) at every interface.  Lazy class (q < 2^254 / 2^190):\n"
+            "// values in [0, 4q) between stages, Harvey butterflies (add_nored, sub_add_nored, reduce_c,\n"
+            "// mont_mul*_lazy), as the 128-bit LAZY class of arith128.cuh.\n"
             "#pragma once\n#include <cstdint>\n\nnamespace ntt256 {\n\n")
     with open(OUT, "w") as f:
-        f.write(head + gen_addsub(8) + gen_mont(8) + w6 + gen_addsub(6) + gen_mont(6) + "}  // namespace ntt256\n")
+        f.write(head + gen_addsub(8) + gen_mont(8) + gen_lazy(8) + gen_mont(8, True) + w6 +
+                gen_addsub(6) + gen_mont(6) + gen_lazy(6) + gen_mont(6, True) + "}  // namespace ntt256\n")
     print("wrote", OUT)
 
 

@@ -119,6 +119,34 @@ def check(W, q, a, b):
     assert (t * R - a * b) % q == 0, "not a b R^-1"
 
 
+def check_lazy(W, q, rng, n):
+    """Lazy class (q < R/4, values in [0, 4q) between stages; ntt256.cu, arith256_gen.cuh):
+    mont_mul*_lazy on a < 4q drops T's word W, so T[W] must be 0 and T < 2q; the Harvey
+    butterfly u' = u mod 2q (reduce_c with c = 2q), t = lazy(v, w), (u' + t, u' - t + 2q) must
+    stay in [0, 4q) < 2^NB (add_nored / sub_add_nored drop their carries) and be congruent
+    to (u + v w, u - v w) mod q (Montgomery twiddles: w = w_true R mod q)."""
+    R = 1 << (32 * W)
+    assert 4 * q < R
+    qinv0 = (-pow(q, -1, 1 << 32)) & M32
+    edge = [0, 1, q - 1, q, 2 * q - 1, 2 * q, 3 * q, 4 * q - 1]
+    pairs = [(a, b) for a in edge for b in (0, 1, q - 1)] + \
+            [(rng.randrange(4 * q), rng.randrange(q)) for _ in range(n)]
+    for a, b in pairs:
+        T = mont_eo(words(a, W), words(b, W), words(q, W), qinv0, W)
+        assert T[W] == 0, "lazy: word W not zero"
+        t = val(T)
+        assert t < 2 * q and (t * R - a * b) % q == 0
+    for _ in range(n):
+        u, v, w = rng.randrange(4 * q), rng.randrange(4 * q), rng.randrange(q)
+        up = u - 2 * q if u >= 2 * q else u                       # reduce_c(u, 2q)
+        t = val(mont_eo(words(v, W), words(w, W), words(q, W), qinv0, W))
+        x0, x1 = up + t, up + 2 * q - t
+        assert 0 <= x0 < 4 * q and 0 < x1 < 4 * q and x0 < R and x1 < R
+        wt = w * pow(R, -1, q) % q
+        assert (x0 - (u + v * wt)) % q == 0 and (x1 - (u - v * wt)) % q == 0
+    return len(pairs) + n
+
+
 def main():
     W = int(sys.argv[1]) if len(sys.argv) > 1 else 8
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
@@ -140,7 +168,11 @@ def main():
                 a = (1 << bits) - 1 - rng.randrange(1 << 40)
             check(W, q, a, rng.randrange(q))
             cnt += 1
-    print(f"W={W}: {cnt} products, all carries accounted for, T < 2q, T = a b R^-1 mod q")
+    lz = 0
+    for q in [(1 << (bits - 2)) - 57 | 1, rng.randrange(1 << (bits - 3), 1 << (bits - 2)) | 1, (1 << (bits - 64)) + 1, 65537]:
+        lz += check_lazy(W, q, rng, max(1, n // 8))
+    print(f"W={W}: {cnt} products, all carries accounted for, T < 2q, T = a b R^-1 mod q; "
+          f"lazy class (q < R/4): {lz} products / butterflies, word W zero, results in [0, 4q)")
 
 
 if __name__ == "__main__":
