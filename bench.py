@@ -49,6 +49,9 @@ INT_PEAK_PATH = os.path.join(ROOT, "profiles", "int_peak.json")
 # (SURVEY.md §8(d)): 36 per butterfly / constant mulmod, 42 per general mulmod.
 P_BUTTERFLY = 36
 P_GENERAL = 42
+# word products the kernels actually issue per butterfly, by the plan's arithmetic class
+# (DESIGN.md §5): Montgomery CIOS 32 IMAD.WIDE + 4 IMAD; pseudo-Mersenne 16 + 4 + 1 IMAD.WIDE
+P_EMITTED = {"montgomery": 36, "pseudo_mersenne": 21}
 SMS = 148
 IMAD_WIDE_PER_CLK_SM = 32          # fallback only: IMAD.WIDE.U32 at half the IMAD rate
 FALLBACK_HBM_GBS = 6650.0
@@ -343,6 +346,14 @@ def run_gpu(args):
                 "unit": "Tprod/s", "frac": round(achieved / pk["tprod_s"], 4), "traffic": traffic,
                 "traffic_src": traffic_src, "peak_src": pk["tprod_src"],
                 "step_frac": round(value / world * P_BUTTERFLY / 1e12 / pk["tprod_s"], 4)}
+    # `achieved` counts SURVEY §8(d)'s ALGORITHMIC products (P = 36 per butterfly, fixed from the
+    # schoolbook + Shoup/Montgomery decomposition whatever the SASS does).  A plan in the
+    # pseudo-Mersenne class (every cfg3 prime is 2^b - c with a small c) emits 21 per butterfly,
+    # so the pipe itself is busier than `frac` x 21/36 says and `frac` may pass 1: both are stated.
+    arith = plan.arith_class()
+    roofline["arith_class"] = arith
+    roofline["products_emitted_per_butterfly"] = P_EMITTED[arith]
+    roofline["frac_emitted"] = round(achieved * P_EMITTED[arith] / P_BUTTERFLY / pk["tprod_s"], 4)
 
     # ---------------- end to end through the public API with host buffers
     e2e = run_e2e(plan, sets[0], args, stream, bfly_per_step, world)
@@ -532,6 +543,7 @@ def run_rows(args, P, pk, stream, rank, world):
         bf = 2 * Bn * (nn // 2) * logn / (ms * 1e-3)
         rows[f"cfg4_logn{logn}_butterflies_per_s"] = bf
         rows[f"cfg4_logn{logn}_int_frac"] = round(bf / world * P_BUTTERFLY / 1e12 / pk["tprod_s"], 4)   # per GPU
+        rows[f"cfg4_logn{logn}_arith_class"] = ps.arith_class()
         del ps, xx, yy, zz
         torch.cuda.empty_cache()
     # cfg5: N = 2^26 single transform through one plan (three passes), a replica per rank

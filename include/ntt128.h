@@ -134,6 +134,17 @@ ntt128_status ntt128_inverse_bitrev(const ntt128_plan_t plan, const uint64_t *d_
 ntt128_status ntt128_plan_info(const ntt128_plan_t plan, uint32_t *log2n, uint32_t *batch, uint32_t *n_moduli,
                                uint32_t *flags, uint32_t *num_passes);
 
+/* Arithmetic class of the plan's plain forward / inverse calls (host-side query):
+ * *cls = NTT128_CLASS_MONTGOMERY (0): Montgomery products (36 word products per butterfly),
+ * lazy per modulus size; NTT128_CLASS_PSEUDO_MERSENNE (1): every modulus is 2^b - c with
+ * c 2^(128-b) < 2^32 (the largest NTT-friendly primes below a power of two)
+ * and the plan is cyclic with >= 2 passes -- products fold 2^128 = c 2^(128-b) (mod q 2^(128-b)),
+ * 21 word products per butterfly.  Results are the same canonical residues
+ * either way ("bitwise-identical"); the class only changes the cost. */
+#define NTT128_CLASS_MONTGOMERY 0u
+#define NTT128_CLASS_PSEUDO_MERSENNE 1u
+ntt128_status ntt128_plan_arith_class(const ntt128_plan_t plan, uint32_t *cls);
+
 void ntt128_plan_destroy(ntt128_plan_t plan);
 
 /* ---------------------------------------------------------------------------

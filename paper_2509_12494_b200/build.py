@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SOURCES = ["ntt128.cu", "vec128.cu", "fourstep.cu", "ntt256.cu"]
-HEADERS = ["arith128.cuh", "barrett128.cuh", "arith256_gen.cuh", "host128.h", os.path.join("..", "..", "include", "ntt128.h")]
+HEADERS = ["arith128.cuh", "psm128.cuh", "barrett128.cuh", "arith256_gen.cuh", "host128.h", os.path.join("..", "..", "include", "ntt128.h")]
 LIB = os.path.join(PKG, "libntt128.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

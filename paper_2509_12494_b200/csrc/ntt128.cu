@@ -37,6 +37,7 @@
 
 #include "../../include/ntt128.h"
 #include "arith128.cuh"
+#include "psm128.cuh"
 #include "host128.h"
 #include "ntt128_internal.h"
 
@@ -276,6 +277,16 @@ __global__ void k_gather_pass_tw(uint4* out, uint64_t out_stride, const uint4* T
 // global stage b = lo + sl: psi^e (forward) or psi^-e (inverse), e = brev_n(2^(n-1-b) + i),
 // from psi_pow[m][j] = psi^j R mod q (j < N; psi^-e = -psi^(N-e) since psi^N = -1); the
 // inverse's b = n - 1 entries are multiplied by `scale` (Montgomery form) when given.
+// Plain-residue copy of a Montgomery-form table (pseudo-Mersenne class): out = in R^-1 mod q.
+__global__ void k_table_to_plain(uint4* out, const uint4* in, uint64_t stride, const ModC* mods) {
+    const ModC& M = mods[blockIdx.y];
+    const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+    const U128 one = U128{{1u, 0u, 0u, 0u}};
+    const uint64_t base = (uint64_t)blockIdx.y * stride;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < stride; i += (uint64_t)gridDim.x * blockDim.x)
+        out[base + i] = u128_to(mont_mul(u128_from(in[base + i]), one, q, M.qinv0));
+}
+
 __global__ void k_gather_nc_tw(uint4* out, uint64_t out_stride, const uint4* psi_pow, uint32_t n, uint32_t lo,
                                uint32_t b, int inv, const uint4* scale, const ModC* mods) {
     const int m = blockIdx.y;
@@ -357,6 +368,7 @@ struct PassArgs {
     uint64_t in_ps, in_es;
     uint64_t f_ps, f_es;     // fpoly: factor of (p, idx) at fin[p f_ps + idx f_es]
     uint32_t fpoly, r_lb;
+    uint32_t psm, psm_pad;   // 1: pseudo-Mersenne class (MODE_PSM): pt holds plain twiddles (plain cyclic multi-pass only)
     uint64_t r_ps;
     uint4* rdst[NTT128_FS_MAX_RANKS];
 };
@@ -422,7 +434,11 @@ __device__ __forceinline__ int slot(int l) {
 //   MODE_LAZY (q < 2^126): values in [0, 4q), Harvey butterflies, lazy Montgomery.
 // Single-pass CTAs (one CTA may hold several moduli) and the last pass's store keep the
 // interface canonical.
-enum { MODE_FULL = 0, MODE_HALF = 1, MODE_LAZY = 2 };
+enum { MODE_FULL = 0, MODE_HALF = 1, MODE_LAZY = 2, MODE_PSM = 3 };
+// MODE_PSM (psm128.cuh): pseudo-Mersenne moduli q = 2^b - c in plain cyclic multi-pass
+// transforms whose launch sets PassArgs::psm -- plain (non-Montgomery) twiddles, values are
+// any 128-bit representative between stages, 21 word products per butterfly; q2[0] carries
+// C = 2^128 - q 2^(128-b).  The inverse's u N^-1 is always the short digit (sh != 0).
 #ifndef NTT_FORCE_FULL
 #define NTT_FORCE_FULL 0      // 1: canonical arithmetic for every modulus (experiment)
 #endif
@@ -433,6 +449,9 @@ __device__ __forceinline__ int mode_of(const uint32_t q[4]) {
 
 // One radix-2 CT butterfly (u, v) -> (u + w v, u - w v) in the given mode.  In the last
 // stage of a scaled inverse u is multiplied by nf = N^-1 (Montgomery form) too.
+#ifndef NTT_PSM
+#define NTT_PSM 1             // 0: no pseudo-Mersenne class (A/B build)
+#endif
 #ifndef NTT_SHIFT_SCALE
 #define NTT_SHIFT_SCALE 1     // 0: N^-1 always by the Montgomery product (A/B experiment)
 #endif
@@ -441,7 +460,12 @@ __device__ __forceinline__ int mode_of(const uint32_t q[4]) {
 template <int MODE, bool SCALE_U>
 __device__ __forceinline__ void bfly(U128& u, U128& v, const U128& w, const uint32_t q[4], const uint32_t q2[4],
                                      uint32_t qinv0, const U128& nf, uint32_t sh = 0) {
-    if (MODE == MODE_FULL) {
+    if (MODE == MODE_PSM) {
+        const U128 us = SCALE_U ? shr_mod(u, sh, q, qinv0) : u;   // any u < 2^128 -> < max(q, 2^127)
+        const U128 t = psm_mul(v, w, q2[0]);
+        u = psm_add(us, t, q2[0]);
+        v = psm_sub(us, t, q2[0]);
+    } else if (MODE == MODE_FULL) {
         const U128 us = SCALE_U ? (sh ? shr_mod(u, sh, q, qinv0) : mont_mul(u, nf, q, qinv0)) : u;
         const U128 t = mont_mul(v, w, q, qinv0);
         u = add_mod(us, t, q);
@@ -460,8 +484,12 @@ __device__ __forceinline__ void bfly(U128& u, U128& v, const U128& w, const uint
 }
 // Stage with twiddle 1 (first stage of a first pass): inputs canonical (< q).
 template <int MODE>
-__device__ __forceinline__ void bfly1(U128& u, U128& v, const uint32_t q[4]) {
-    if (MODE == MODE_FULL) {
+__device__ __forceinline__ void bfly1(U128& u, U128& v, const uint32_t q[4], const uint32_t q2[4]) {
+    if (MODE == MODE_PSM) {
+        const U128 a = psm_add(u, v, q2[0]);
+        v = psm_sub(u, v, q2[0]);
+        u = a;
+    } else if (MODE == MODE_FULL) {
         const U128 a = add_mod(u, v, q);
         v = sub_mod(u, v, q);
         u = a;
@@ -474,7 +502,11 @@ __device__ __forceinline__ void bfly1(U128& u, U128& v, const uint32_t q[4]) {
 // Butterfly with twiddle 1 on values in the mode's lazy range (a later stage's j = 0 block).
 template <int MODE>
 __device__ __forceinline__ void bfly_tw1(U128& u, U128& v, const uint32_t q[4], const uint32_t q2[4]) {
-    if (MODE == MODE_FULL) {
+    if (MODE == MODE_PSM) {
+        const U128 a = psm_add(u, v, q2[0]);
+        v = psm_sub(u, v, q2[0]);
+        u = a;
+    } else if (MODE == MODE_FULL) {
         const U128 a = add_mod(u, v, q);
         v = sub_mod(u, v, q);
         u = a;
@@ -521,7 +553,7 @@ __device__ __forceinline__ void round_body(const int rd, uint4* gsm, const uint4
 #pragma unroll
             for (int kk = 0; kk < E / 2; kk++) {
                 const int k0 = ((kk >> bit) << (bit + 1)) | (kk & ((1 << bit) - 1));
-                bfly1<MODE>(x[k0], x[k0 | (1 << bit)], q);
+                bfly1<MODE>(x[k0], x[k0 | (1 << bit)], q, q2);
             }
             continue;
         }
@@ -548,7 +580,9 @@ template <int B, int C, bool FIRST, bool SCALE_LAST, int RBMAX, int MODE, bool W
 __device__ __forceinline__ void pass_rounds(uint4* gsm, const uint4* tws, const int t, const uint32_t lo, const uint32_t n,
                                             const uint32_t q[4], const uint32_t qinv0, const U128 nf, const uint32_t sh) {
     uint32_t q2[4] = {0, 0, 0, 0};
-    if (MODE != MODE_FULL) {
+    if (MODE == MODE_PSM) {
+        q2[0] = psm_C(q, psm_shift(q));
+    } else if (MODE != MODE_FULL) {
         q2[0] = q[0] << 1;
         q2[1] = (q[1] << 1) | (q[0] >> 31);
         q2[2] = (q[2] << 1) | (q[1] >> 31);
@@ -830,13 +864,15 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
         uint4* gsm = dsm + c * GS;
         const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
-        const int mode = SINGLE ? MODE_FULL : mode_of(q);   // uniform per CTA: its groups share the polynomial
+        const int mode = SINGLE ? MODE_FULL : (a.psm ? MODE_PSM : mode_of(q));   // uniform per CTA: its groups share the polynomial
         const uint32_t sh = (NTT_SHIFT_SCALE && SCALE_LAST && !a.ninv_r && n >= 2) ? n : 0u;   // plain inverse: N^-1 by shifting
 #if NTT_COMPUTE_REPEAT != 1
 #pragma unroll 1
         for (int rep = 0; rep < NTT_COMPUTE_REPEAT; rep++)
 #endif
-        if (mode == MODE_LAZY)
+        if (!SINGLE && mode == MODE_PSM)
+            pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_PSM, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
+        else if (mode == MODE_LAZY)
             pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
         else if (mode == MODE_HALF)
             pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_HALF, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
@@ -914,16 +950,22 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
                 // lazy classes leave the last pass in [0, 4q) / [0, 2q): canonicalize
                 const QPar& M = a.qp[a.nq == 1 ? 0 : (uint32_t)(gg0 >> gbits)];
                 const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
-                const int mode = mode_of(q);
-                if (mode == MODE_LAZY) {
-                    const uint32_t q2[4] = {q[0] << 1, (q[1] << 1) | (q[0] >> 31), (q[2] << 1) | (q[1] >> 31),
-                                            (q[3] << 1) | (q[2] >> 31)};
+                const int mode = a.psm ? MODE_PSM : mode_of(q);
+                if (mode == MODE_PSM) {
+                    const uint32_t s = psm_shift(q), Cq = psm_C(q, s);
 #pragma unroll
-                    for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q2));
-                }
-                if (mode != MODE_FULL) {
+                    for (int i = 0; i < PER; i++) outv[i] = u128_to(psm_canon(u128_from(outv[i]), q, s, Cq));
+                } else {
+                    if (mode == MODE_LAZY) {
+                        const uint32_t q2[4] = {q[0] << 1, (q[1] << 1) | (q[0] >> 31), (q[2] << 1) | (q[1] >> 31),
+                                                (q[3] << 1) | (q[2] >> 31)};
 #pragma unroll
-                    for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q));
+                        for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q2));
+                    }
+                    if (mode != MODE_FULL) {
+#pragma unroll
+                        for (int i = 0; i < PER; i++) outv[i] = u128_to(reduce_2q(u128_from(outv[i]), q));
+                    }
                 }
             }
             if (live) {
@@ -1044,7 +1086,7 @@ k_ntt_first_tl(const __grid_constant__ PassArgs a) {
     const QPar& M = a.qp[m];
     uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
     const uint32_t qinv0 = M.qinv0;
-    const int mode = mode_of(q);
+    const int mode = a.psm ? MODE_PSM : mode_of(q);
     const U128 nf = U128{{0, 0, 0, 0}};
 #pragma unroll
     for (int k = 0; k < TL; k++) {
@@ -1056,7 +1098,9 @@ k_ntt_first_tl(const __grid_constant__ PassArgs a) {
         if (k == 0) mbar_wait(&tw_bar, 0);
         const uint64_t gg = gg0 + k;
         uint4* gsm = dsm + k * GS;
-        if (mode == MODE_LAZY)
+        if (mode == MODE_PSM)
+            pass_rounds<B, C, true, false, RBMAX, MODE_PSM, WARPMAP, true>(gsm, tsm, tid, 0, n, q, qinv0, nf, 0);
+        else if (mode == MODE_LAZY)
             pass_rounds<B, C, true, false, RBMAX, MODE_LAZY, WARPMAP, true>(gsm, tsm, tid, 0, n, q, qinv0, nf, 0);
         else if (mode == MODE_HALF)
             pass_rounds<B, C, true, false, RBMAX, MODE_HALF, WARPMAP, true>(gsm, tsm, tid, 0, n, q, qinv0, nf, 0);
@@ -1144,7 +1188,7 @@ k_ntt_later_tl(const __grid_constant__ PassArgs a) {
         nf = U128{{src[0], src[1], src[2], src[3]}};
     }
     const uint32_t sh = (NTT_SHIFT_SCALE && SCALE_LAST && !a.ninv_r && n >= 2) ? n : 0u;
-    const int mode = mode_of(q);
+    const int mode = a.psm ? MODE_PSM : mode_of(q);
     const bool last_pass = lo + B == n;
 #pragma unroll
     for (int k = 0; k < TL; k++) {
@@ -1154,7 +1198,9 @@ k_ntt_later_tl(const __grid_constant__ PassArgs a) {
         __syncthreads();
         if (k == 0) mbar_wait(&tw_bar, 0);
         uint4* gsm = dsm + k * GS;
-        if (mode == MODE_LAZY)
+        if (mode == MODE_PSM)
+            pass_rounds<B, C, false, SCALE_LAST, RBMAX, MODE_PSM, WARPMAP, true>(gsm, tsm, tid, lo, n, q, qinv0, nf, sh);
+        else if (mode == MODE_LAZY)
             pass_rounds<B, C, false, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP, true>(gsm, tsm, tid, lo, n, q, qinv0, nf, sh);
         else if (mode == MODE_HALF)
             pass_rounds<B, C, false, SCALE_LAST, RBMAX, MODE_HALF, WARPMAP, true>(gsm, tsm, tid, lo, n, q, qinv0, nf, sh);
@@ -1164,7 +1210,11 @@ k_ntt_later_tl(const __grid_constant__ PassArgs a) {
         uint4 outv[PER];
 #pragma unroll
         for (int i = 0; i < PER; i++) outv[i] = gsm[slot<B, true, RB>(tid + (i << LT))];
-        if (last_pass && mode != MODE_FULL) {   // lazy classes leave the transform canonical
+        if (last_pass && mode == MODE_PSM) {
+            const uint32_t s = psm_shift(q), Cq = psm_C(q, s);
+#pragma unroll
+            for (int i = 0; i < PER; i++) outv[i] = u128_to(psm_canon(u128_from(outv[i]), q, s, Cq));
+        } else if (last_pass && mode != MODE_FULL) {   // lazy classes leave the transform canonical
             if (mode == MODE_LAZY) {
                 const uint32_t q2[4] = {q[0] << 1, (q[1] << 1) | (q[0] >> 31), (q[2] << 1) | (q[1] >> 31),
                                         (q[3] << 1) | (q[2] >> 31)};
@@ -1476,7 +1526,7 @@ __global__ void __launch_bounds__(1 << (LB - CLU_LOG - 1)) k_ntt_cluster(const P
         const uint32_t br = brev_bits(r, CLU_LOG);
         U128 u = u128_from(__ldcg(src + ((brev_bits(2 * t, LM) << CLU_LOG) | br)));
         U128 v = u128_from(__ldcg(src + ((brev_bits(2 * t + 1, LM) << CLU_LOG) | br)));
-        bfly1<MODE_FULL>(u, v, q);
+        bfly1<MODE_FULL>(u, v, q, q2);
         loc[2 * t] = u128_to(u);
         loc[2 * t + 1] = u128_to(v);
         __syncthreads();
@@ -1778,6 +1828,11 @@ struct ntt128_plan_s {
     uint4* d_f_untwist_r = nullptr;           // [nq][N]    N^-1 psi^-j R          (negacyclic polymul)
     std::vector<u128> q_host;
     std::vector<uint4*> d_pt_fwd, d_pt_inv, d_pt_inv_r;  // per pass, [nq][pt_stride]
+    // pseudo-Mersenne class (psm128.cuh): every modulus is 2^b - c with c 2^(128-b) < 2^32 and the
+    // plan is cyclic with >= 2 passes -- plain-residue copies of d_pt_fwd / d_pt_inv for the
+    // plain forward / inverse calls (polymul, four-step I/O and negacyclic calls keep Montgomery)
+    bool psm = false;
+    std::vector<uint4*> d_pt_fwd_psm, d_pt_inv_psm;
     // permutation-free negacyclic path (n >= 10): pass widths bottom-up, per-pass tables
     // [nq][2^(n - lo - B)][2^B - 1] (psi, psi^-1; the top inverse pass N^-1 / N^-1 R scaled)
     std::vector<int> nc_bits;
@@ -1841,6 +1896,8 @@ static void plan_free(ntt128_plan_s* p) {
         cudaFree(p->d_nc_fwd[i]);
         cudaFree(p->d_nc_inv[i]);
     }
+    for (uint4* t : p->d_pt_fwd_psm) cudaFree(t);
+    for (uint4* t : p->d_pt_inv_psm) cudaFree(t);
     for (size_t i = 0; i < p->d_pt_fwd.size(); i++) {
         if (p->d_pt_inv_r[i] != p->d_pt_inv[i]) cudaFree(p->d_pt_inv_r[i]);
         cudaFree(p->d_pt_fwd[i]);
@@ -1931,6 +1988,14 @@ static cudaError_t gen_table(uint4* out, uint64_t stride, uint64_t count, const 
     cudaFree(d_pow2);
     cudaFree(d_sc);
     return e;
+}
+
+// q = 2^b - c with c 2^(128-b) < 2^32 (psm128.cuh): words 1..3 of q 2^(128-b) are all ones.
+static bool psm_eligible(u128 q) {
+    int s = 0;
+    while (((q << s) >> 127) == 0) s++;
+    const u128 Q = q << s;
+    return (Q >> 32) == (((u128)1 << 96) - 1);
 }
 
 extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, uint32_t batch, const uint64_t* q_host,
@@ -2107,6 +2172,25 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
             if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = NTT128_ERR_CUDA;
             lo += b;
         }
+        // pseudo-Mersenne class: plain-residue copies of the forward / inverse pass tables
+        p->psm = NTT_PSM && NTT_SHIFT_SCALE && !NTT_FORCE_FULL && !kind && np >= 2;
+        for (uint32_t m = 0; m < n_moduli && p->psm; m++) p->psm = psm_eligible(qs[m]);
+        for (size_t i = 0; i < np && st == NTT128_OK && p->psm; i++) {
+            const uint64_t stride = p->pt_stride[i];
+            const size_t bytes = (size_t)stride * n_moduli * sizeof(uint4);
+            uint4 *f = nullptr, *v = nullptr;
+            if (cudaMalloc(&f, bytes) != cudaSuccess || cudaMalloc(&v, bytes) != cudaSuccess) st = NTT128_ERR_OOM;
+            p->d_pt_fwd_psm.push_back(f);
+            p->d_pt_inv_psm.push_back(v);
+            if (st != NTT128_OK) break;
+            unsigned gx = (unsigned)((stride + 255) / 256);
+            if (gx > 4096) gx = 4096;
+            const dim3 grid(gx, n_moduli);
+            k_table_to_plain<<<grid, 256>>>(f, p->d_pt_fwd[i], stride, p->d_mods);
+            k_table_to_plain<<<grid, 256>>>(v, p->d_pt_inv[i], stride, p->d_mods);
+            ntt128_count_launch(2);
+            if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = NTT128_ERR_CUDA;
+        }
         // permutation-free negacyclic tables (ntt128_forward_bitrev / inverse_bitrev, polymul)
         if (st == NTT128_OK && kind) {
             p->nc_bits = nc_pass_bits((int)log2n);
@@ -2183,6 +2267,12 @@ extern "C" ntt128_status ntt128_plan_info(const ntt128_plan_t p, uint32_t* log2n
     if (n_moduli) *n_moduli = p->nq;
     if (flags) *flags = p->flags;
     if (num_passes) *num_passes = (uint32_t)p->bits.size();
+    return NTT128_OK;
+}
+
+extern "C" ntt128_status ntt128_plan_arith_class(const ntt128_plan_t p, uint32_t* cls) {
+    if (!p || !cls) return NTT128_ERR_INVALID_ARG;
+    *cls = p->psm ? NTT128_CLASS_PSEUDO_MERSENNE : NTT128_CLASS_MONTGOMERY;
     return NTT128_OK;
 }
 
@@ -2624,6 +2714,10 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
         a.lo = (uint32_t)lo;
         a.nq = p->nq;
         a.pt = !o.inverse ? p->d_pt_fwd[i] : (o.polymul ? p->d_pt_inv_r[i] : p->d_pt_inv[i]);
+        if (p->psm && !o.io && !o.pmul && !o.polymul) {   // plain cyclic call: pseudo-Mersenne class
+            a.psm = 1;
+            a.pt = !o.inverse ? p->d_pt_fwd_psm[i] : p->d_pt_inv_psm[i];
+        }
         const bool first = i == 0, last = i + 1 == npass;
         if (first && o.pmul) a.pmul = o.pmul;
         if (scale_last && last) a.ninv_r = o.polymul ? 1 : 0;

@@ -38,6 +38,8 @@ _L.ntt128_polymul.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _L.ntt128_polymul.restype = ctypes.c_int
 _L.ntt128_plan_info.argtypes = [_vp] + [ctypes.POINTER(ctypes.c_uint32)] * 5
 _L.ntt128_plan_info.restype = ctypes.c_int
+_L.ntt128_plan_arith_class.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32)]
+_L.ntt128_plan_arith_class.restype = ctypes.c_int
 _L.ntt128_plan_destroy.argtypes = [_vp]
 _L.ntt128_plan_destroy.restype = None
 for _name in ("vec128_add", "vec128_sub", "vec128_mul"):
@@ -65,7 +67,7 @@ OK = 0
 _ARG_ERRORS = {1, 2, 3, 4, 5, 6, 7}
 
 EXPORTED = ("ntt128_plan_create", "ntt128_forward", "ntt128_inverse", "ntt128_forward_bitrev",
-            "ntt128_inverse_bitrev", "ntt128_polymul", "ntt128_plan_info",
+            "ntt128_inverse_bitrev", "ntt128_polymul", "ntt128_plan_info", "ntt128_plan_arith_class",
             "ntt128_plan_destroy", "vec128_add", "vec128_sub", "vec128_mul", "vec128_axpy",
             "ntt128_status_string", "ntt128_launch_count", "ntt128_fourstep_create", "ntt128_fourstep_forward_a",
             "ntt128_fourstep_forward_c", "ntt128_fourstep_inverse_a", "ntt128_fourstep_inverse_c",
@@ -158,6 +160,12 @@ class Plan:
         v = [ctypes.c_uint32() for _ in range(5)]
         _check(_L.ntt128_plan_info(self._h, *[ctypes.byref(x) for x in v]), "ntt128_plan_info")
         return dict(zip(("log2n", "batch", "n_moduli", "flags", "num_passes"), [x.value for x in v]))
+
+    def arith_class(self) -> str:
+        """'pseudo_mersenne' or 'montgomery' (ntt128_plan_arith_class)"""
+        c = ctypes.c_uint32()
+        _check(_L.ntt128_plan_arith_class(self._h, ctypes.byref(c)), "ntt128_plan_arith_class")
+        return "pseudo_mersenne" if c.value == 1 else "montgomery"
 
     def _shape_ok(self, t: torch.Tensor, name: str) -> None:
         if t.numel() != 2 * self.n * self.batch:

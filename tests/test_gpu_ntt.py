@@ -103,6 +103,26 @@ def test_structured_inputs(N, params):
         assert np.array_equal(to_host(plan.inverse(to_dev(y))), x)
 
 
+@pytest.mark.parametrize("key", ["b124", "b125", "b126", "b127", "cfg5"])
+def test_pseudo_mersenne_class_structured(N, params, key):
+    """multi-pass plain cyclic plans whose moduli are all 2^b - c with c 2^(128-b) < 2^32 run the
+    pseudo-Mersenne class (csrc/psm128.cuh): structured inputs (q - 1 everywhere, alternating
+    0 / q - 1, a geometric sequence) plus uniform ones, every bit length 124..128 and the
+    largest fold constant of the parameter set (cfg5's C = 2013265919), vs the oracle"""
+    e = params["cfg5"] if key == "cfg5" else params["extra"][key]
+    q = e["q"]
+    for logn in (13, 17):
+        w, n = sub_root(e, logn), 1 << logn
+        S = structured(q, n)
+        x = np.stack([synth.from_ints(v) for v in S.values()] +
+                     [synth.uniform_residues(q, n, 900 + logn).reshape(n, 2)])
+        B = x.shape[0]
+        plan = N.Plan(logn, q, w, batch=B)
+        y = to_host(plan.forward(to_dev(x)))
+        assert np.array_equal(y, O.ntt(x, [q] * B, [w] * B))
+        assert np.array_equal(to_host(plan.inverse(to_dev(y))), x)
+
+
 def test_cfg1_full(N, params):
     """BASELINE cfg 1: N = 1024, one polynomial, forward + inverse, natural order"""
     e = params["cfg1"]
