@@ -864,13 +864,13 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
         uint4* gsm = dsm + c * GS;
         const uint4* tws = tsm + (NTW == 1 ? 0 : c) * TS;
 
-        const int mode = SINGLE ? MODE_FULL : (a.psm ? MODE_PSM : mode_of(q));   // uniform per CTA: its groups share the polynomial
+        const int mode = a.psm ? MODE_PSM : (SINGLE ? MODE_FULL : mode_of(q));   // uniform per CTA: its groups share the polynomial
         const uint32_t sh = (NTT_SHIFT_SCALE && SCALE_LAST && !a.ninv_r && n >= 2) ? n : 0u;   // plain inverse: N^-1 by shifting
 #if NTT_COMPUTE_REPEAT != 1
 #pragma unroll 1
         for (int rep = 0; rep < NTT_COMPUTE_REPEAT; rep++)
 #endif
-        if (!SINGLE && mode == MODE_PSM)
+        if (mode == MODE_PSM)
             pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_PSM, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
         else if (mode == MODE_LAZY)
             pass_rounds<B, C, FIRST, SCALE_LAST, RBMAX, MODE_LAZY, WARPMAP, PADL>(gsm, tws, t, lo, n, q, qinv0, nf, sh);
@@ -918,18 +918,29 @@ k_ntt_pass(const __grid_constant__ PassArgs a) {
                 const uint64_t poly = gg >> gbits, g = gg & gmask;
                 const uint64_t idx = ((uint64_t)brev_bits((uint32_t)g, gbits) << B) | (uint64_t)l;
                 uint4 v = outv[i];
+                if (SINGLE && a.psm && !a.fout) {   // pseudo-Mersenne class: any representative -> canonical
+                    const ModC& M = a.mods[a.nq == 1 ? 0 : (uint32_t)poly];
+                    const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
+                    const uint32_t s = psm_shift(q);
+                    v = u128_to(psm_canon(u128_from(v), q, s, psm_C(q, s)));
+                }
                 if (!SINGLE && gbits == 0 && !a.fout) {
                     // the whole transform was this pass (four-step sub-transforms of 2^9 run the
                     // padded multi-pass kernel as their single pass): lazy classes -> canonical
                     const QPar& M = a.qp[a.nq == 1 ? 0 : (uint32_t)poly];
                     const uint32_t q[4] = {M.q[0], M.q[1], M.q[2], M.q[3]};
-                    const int mode = mode_of(q);
-                    if (mode == MODE_LAZY) {
-                        const uint32_t q2[4] = {q[0] << 1, (q[1] << 1) | (q[0] >> 31), (q[2] << 1) | (q[1] >> 31),
-                                                (q[3] << 1) | (q[2] >> 31)};
-                        v = u128_to(reduce_2q(u128_from(v), q2));
+                    const int mode = a.psm ? MODE_PSM : mode_of(q);
+                    if (mode == MODE_PSM) {
+                        const uint32_t s = psm_shift(q);
+                        v = u128_to(psm_canon(u128_from(v), q, s, psm_C(q, s)));
+                    } else {
+                        if (mode == MODE_LAZY) {
+                            const uint32_t q2[4] = {q[0] << 1, (q[1] << 1) | (q[0] >> 31), (q[2] << 1) | (q[1] >> 31),
+                                                    (q[3] << 1) | (q[2] >> 31)};
+                            v = u128_to(reduce_2q(u128_from(v), q2));
+                        }
+                        if (mode != MODE_FULL) v = u128_to(reduce_2q(u128_from(v), q));
                     }
-                    if (mode != MODE_FULL) v = u128_to(reduce_2q(u128_from(v), q));
                 }
                 if (a.fout) {
                     const uint32_t m = a.nq == 1 ? 0 : (uint32_t)poly;
@@ -2173,7 +2184,7 @@ extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, 
             lo += b;
         }
         // pseudo-Mersenne class: plain-residue copies of the forward / inverse pass tables
-        p->psm = NTT_PSM && NTT_SHIFT_SCALE && !NTT_FORCE_FULL && !kind && np >= 2;
+        p->psm = NTT_PSM && NTT_SHIFT_SCALE && !NTT_FORCE_FULL && !kind && log2n >= 2;
         for (uint32_t m = 0; m < n_moduli && p->psm; m++) p->psm = psm_eligible(qs[m]);
         for (size_t i = 0; i < np && st == NTT128_OK && p->psm; i++) {
             const uint64_t stride = p->pt_stride[i];
@@ -2714,7 +2725,7 @@ static ntt128_status run_transform(ntt128_plan_s* p, const uint4* src, uint4* ds
         a.lo = (uint32_t)lo;
         a.nq = p->nq;
         a.pt = !o.inverse ? p->d_pt_fwd[i] : (o.polymul ? p->d_pt_inv_r[i] : p->d_pt_inv[i]);
-        if (p->psm && !o.io && !o.pmul && !o.polymul) {   // plain cyclic call: pseudo-Mersenne class
+        if (p->psm && !o.pmul && !o.polymul) {   // cyclic call without a point-wise operand: pseudo-Mersenne class
             a.psm = 1;
             a.pt = !o.inverse ? p->d_pt_fwd_psm[i] : p->d_pt_inv_psm[i];
         }
