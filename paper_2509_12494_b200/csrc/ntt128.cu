@@ -462,9 +462,9 @@ __device__ __forceinline__ void bfly(U128& u, U128& v, const U128& w, const uint
                                      uint32_t qinv0, const U128& nf, uint32_t sh = 0) {
     if (MODE == MODE_PSM) {
         const U128 us = SCALE_U ? shr_mod(u, sh, q, qinv0) : u;   // any u < 2^128 -> < max(q, 2^127)
-        const U128 t = psm_mul(v, w, q2[0]);
-        u = psm_add(us, t, q2[0]);
-        v = psm_sub(us, t, q2[0]);
+        const U128 t = psm_mul(v, w, q2[0]);      // < Q: one fold in the add and the subtract
+        u = psm_add1(us, t, q2[0]);
+        v = psm_sub1(us, t, q2[0]);
     } else if (MODE == MODE_FULL) {
         const U128 us = SCALE_U ? (sh ? shr_mod(u, sh, q, qinv0) : mont_mul(u, nf, q, qinv0)) : u;
         const U128 t = mont_mul(v, w, q, qinv0);
@@ -2006,7 +2006,7 @@ static bool psm_eligible(u128 q) {
     int s = 0;
     while (((q << s) >> 127) == 0) s++;
     const u128 Q = q << s;
-    return (Q >> 32) == (((u128)1 << 96) - 1);
+    return (Q >> 32) == (((u128)1 << 96) - 1) && (uint32_t)Q != 1u;   // C = 2^32 - 1 excluded (psm_mul's l4 + 1)
 }
 
 extern "C" ntt128_status ntt128_plan_create(ntt128_plan_t* out, uint32_t log2n, uint32_t batch, const uint64_t* q_host,

@@ -5,12 +5,16 @@
 // primes") have this shape.  With s = 128 - b and
 // Q = q 2^s = 2^128 - C, C = c 2^s < 2^32, arithmetic modulo Q is arithmetic modulo q
 // (q | Q), and 2^128 = C (mod Q): a 256-bit product H 2^128 + L folds to H C + L
-// (4 word products), its fifth word folds once more (1 product), and a last carry adds C.
-// A butterfly's product costs 16 + 4 + 1 = 21 word products instead of Montgomery's 36
-// (DESIGN.md §5 "Pseudo-Mersenne class"); twiddles are stored as plain residues.
+// (4 word products), and its fifth word folds once more with the quotient estimate l4 + 1
+// (1 product) straight to the residue modulo Q.  A butterfly's product costs 16 + 4 + 1 = 21
+// word products instead of Montgomery's 36 (DESIGN.md §5 "Pseudo-Mersenne class"); twiddles
+// are stored as plain residues.
 //
 // Representation between stages: ANY 128-bit value congruent to the residue modulo q
 // (not canonical, not even < Q); psm_canon maps it to [0, q) in the last pass's store.
+// psm_mul returns t < Q, so the butterfly's u + t and u - t fold their carry / borrow once
+// (psm_add1 / psm_sub1); the twiddle-1 butterflies add and subtract two arbitrary
+// representatives and fold twice (psm_add / psm_sub).  C = 2^32 - 1 is excluded by the host.
 // The word-level algorithm (every carry, every bound) is modelled and checked against
 // Python integers in tools/model/psm_model.py (CPU test tests/test_psm_model.py).
 #pragma once
@@ -80,8 +84,48 @@ __device__ __forceinline__ U128 psm_sub(const U128& a, const U128& b, uint32_t C
     return U128{{d0, d1, d2, d3}};
 }
 
-// a * b (mod Q) for a, b < 2^128.  The 4 x 4 schoolbook product is accumulated in two
-// register-pair-aligned halves (every 64-bit partial product lands on an aligned pair, so
+// a + t and a - t (mod Q) for any a < 2^128 and t < Q = 2^128 - C (psm_mul's results): one fold
+// suffices.  a + t - 2^128 + C <= (2^128 - 1) + (Q - 1) - 2^128 + C = 2^128 - 2: no second carry;
+// a - t + 2^128 - C >= 2^128 - (Q - 1) - C = 1: no second borrow.
+__device__ __forceinline__ U128 psm_add1(const U128& a, const U128& t, uint32_t C) {
+    uint32_t s0, s1, s2, s3, k;
+    asm("add.cc.u32  %0, %5, %9;\n\t"
+        "addc.cc.u32 %1, %6, %10;\n\t"
+        "addc.cc.u32 %2, %7, %11;\n\t"
+        "addc.cc.u32 %3, %8, %12;\n\t"
+        "addc.u32    %4, 0, 0;"
+        : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3), "=r"(k)
+        : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(t.w[0]), "r"(t.w[1]), "r"(t.w[2]), "r"(t.w[3]));
+    const uint32_t f = k ? C : 0u;
+    asm("add.cc.u32  %0, %0, %4;\n\t"
+        "addc.cc.u32 %1, %1, 0;\n\t"
+        "addc.cc.u32 %2, %2, 0;\n\t"
+        "addc.u32    %3, %3, 0;"
+        : "+r"(s0), "+r"(s1), "+r"(s2), "+r"(s3)
+        : "r"(f));
+    return U128{{s0, s1, s2, s3}};
+}
+__device__ __forceinline__ U128 psm_sub1(const U128& a, const U128& t, uint32_t C) {
+    uint32_t d0, d1, d2, d3, bw;
+    asm("sub.cc.u32  %0, %5, %9;\n\t"
+        "subc.cc.u32 %1, %6, %10;\n\t"
+        "subc.cc.u32 %2, %7, %11;\n\t"
+        "subc.cc.u32 %3, %8, %12;\n\t"
+        "subc.u32    %4, 0, 0;"
+        : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(d3), "=r"(bw)
+        : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(t.w[0]), "r"(t.w[1]), "r"(t.w[2]), "r"(t.w[3]));
+    const uint32_t f = bw ? C : 0u;
+    asm("sub.cc.u32  %0, %0, %4;\n\t"
+        "subc.cc.u32 %1, %1, 0;\n\t"
+        "subc.cc.u32 %2, %2, 0;\n\t"
+        "subc.u32    %3, %3, 0;"
+        : "+r"(d0), "+r"(d1), "+r"(d2), "+r"(d3)
+        : "r"(f));
+    return U128{{d0, d1, d2, d3}};
+}
+
+// a * b (mod Q) for a < 2^128, b < q (a twiddle): the result is < Q.  The 4 x 4 schoolbook
+// product is accumulated in two register-pair-aligned halves (every 64-bit partial product lands on an aligned pair, so
 // each is one IMAD.WIDE with carry in / out): E collects a_i b_j with i + j even (words
 // 0..7), O those with i + j odd (words 1..8 of the product, o[0] at word 1; the top word o7
 // only ever holds carries).  P = E + 2^32 O, then the folds described in the header.
@@ -157,21 +201,26 @@ __device__ __forceinline__ U128 psm_mul(const U128& a, const U128& b, uint32_t C
         "madc.hi.u32    %4, %8, %9, %4;"
         : "+r"(e0), "+r"(e1), "+r"(e2), "+r"(e3), "=&r"(l4)
         : "r"(e4), "r"(e5), "r"(e6), "r"(e7), "r"(C));
-    // second fold: l4 C < 2^64 onto words 0..1; the sum is < 2^128 + 2^64, carry k
+    // second fold with the quotient estimate l4 + 1: y = L' + l4 C < 2^128 + 2^64 is the value modulo
+    // Q up to one subtraction of Q = 2^128 - C, and y >= Q exactly when z = y + C = L' + (l4 + 1) C
+    // carries out of 128 bits.  Carry: z - 2^128 = y - Q is the result; no carry: undo the + C.
+    // Either way the result is < Q, which lets the butterfly's add / sub fold only once.
+    // (l4 <= C: H <= q - 1 because b < q, so H C + L < 2^128 (C + 1); the host excludes C = 2^32 - 1.)
     uint32_t k;
+    const uint32_t m = l4 + 1u;
     asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
         "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
         "addc.cc.u32    %2, %2, 0;\n\t"
         "addc.cc.u32    %3, %3, 0;\n\t"
         "addc.u32       %4, 0, 0;"
         : "+r"(e0), "+r"(e1), "+r"(e2), "+r"(e3), "=r"(k)
-        : "r"(l4), "r"(C));
-    // k == 1: the low 128 bits are < 2^64 (words 2..3 zero); + C may reach word 2, no further
-    const uint32_t f = (0u - k) & C;
-    asm("add.cc.u32  %0, %0, %3;\n\t"
-        "addc.cc.u32 %1, %1, 0;\n\t"
-        "addc.u32    %2, %2, 0;"
-        : "+r"(e0), "+r"(e1), "+r"(e2)
+        : "r"(m), "r"(C));
+    const uint32_t f = k ? 0u : C;   // no carry: subtract the C again (cannot borrow: y >= 0)
+    asm("sub.cc.u32  %0, %0, %4;\n\t"
+        "subc.cc.u32 %1, %1, 0;\n\t"
+        "subc.cc.u32 %2, %2, 0;\n\t"
+        "subc.u32    %3, %3, 0;"
+        : "+r"(e0), "+r"(e1), "+r"(e2), "+r"(e3)
         : "r"(f));
     return U128{{e0, e1, e2, e3}};
 }

@@ -24,7 +24,7 @@ QS = [
     (1 << 128) - 55295, (1 << 128) - 8257535, (1 << 128) - 2013265919,     # Appendix A, 128-bit
     0x7fffffffffffffffffffffffff860001, 0x3ffffffffffffffffffffffffffc0001,  # cfg3 q_1, q_2
     0x1ffffffffffffffffffffffffffc0001, 0xfffffffffffffffffffffffffa60001,   # cfg3 q_3, q_4
-    (1 << 128) - (1 << 32) + 1,                                            # C = 2^32 - 1 (largest)
+    (1 << 128) - (1 << 32) + 2 + 1,                                        # C = 2^32 - 3 (arithmetic only)
     (1 << 128) - 1,                                                        # C = 1 (smallest; not prime: arithmetic only)
     (1 << 124) - (1 << 28) + 1,                                            # s = 4, c 2^s = 2^32 - 16
 ]
@@ -51,3 +51,5 @@ def test_class_membership():
         m.params(0x804671da650e225b9b75f6b15a9a0001)   # SURVEY Appendix A's random prime: not in the class
     with pytest.raises(AssertionError):
         m.params((1 << 128) - (1 << 32) - 1)           # C = 2^32 + 1
+    with pytest.raises(AssertionError):
+        m.params((1 << 128) - (1 << 32) + 1)           # C = 2^32 - 1: excluded (l4 + 1 must fit a word)

@@ -51,6 +51,7 @@ def params(q):
     assert Q >> 32 == (1 << 96) - 1, "not in the class"
     C = (-((q & M32) << s)) & M32
     assert R - Q == C and C >= 1
+    assert C != M32, "C = 2^32 - 1 is excluded (psm_mul's l4 + 1)"
     return s, C
 
 
@@ -133,17 +134,43 @@ def psm_mul(a, b, C):
     e[3] = f.mad_lo(h[3], C, e[3], True)
     l4 = f.mad_hi(h[3], C, l4, True, cout=False)
     assert val(e[:4]) + (l4 << 128) == (a * b) % R + ((a * b) >> 128) * C
-    e[0] = f.mad_lo(l4, C, e[0])
-    e[1] = f.mad_hi(l4, C, e[1], True)
+    m = l4 + 1
+    assert m <= M32 and l4 <= C
+    e[0] = f.mad_lo(m, C, e[0])
+    e[1] = f.mad_hi(m, C, e[1], True)
     e[2] = f.add(e[2], 0, True)
     e[3] = f.add(e[3], 0, True)
     k = f.c
-    if k:
-        assert e[2] == 0 and e[3] == 0
-    e[0] = f.add(e[0], C if k else 0)
-    e[1] = f.add(e[1], 0, True)
-    e[2] = f.add(e[2], 0, True, cout=False)
+    e[0] = f.sub(e[0], 0 if k else C)
+    e[1] = f.sub(e[1], 0, True)
+    e[2] = f.sub(e[2], 0, True)
+    e[3] = f.sub(e[3], 0, True, bout=False)
     return val(e[:4])
+
+
+def psm_add1(a, t, C):
+    """t < Q: a single fold"""
+    A, B = words(a), words(t)
+    f = Flag()
+    s = [f.add(A[0], B[0])] + [f.add(A[i], B[i], True) for i in (1, 2, 3)]
+    k = f.c
+    s[0] = f.add(s[0], C if k else 0)
+    s[1] = f.add(s[1], 0, True)
+    s[2] = f.add(s[2], 0, True)
+    s[3] = f.add(s[3], 0, True, cout=False)
+    return val(s)
+
+
+def psm_sub1(a, t, C):
+    A, B = words(a), words(t)
+    f = Flag()
+    d = [f.sub(A[0], B[0])] + [f.sub(A[i], B[i], True) for i in (1, 2, 3)]
+    bw = f.c
+    d[0] = f.sub(d[0], C if bw else 0)
+    d[1] = f.sub(d[1], 0, True)
+    d[2] = f.sub(d[2], 0, True)
+    d[3] = f.sub(d[3], 0, True, bout=False)
+    return val(d)
 
 
 def psm_canon(v, q, s, C):
@@ -160,13 +187,22 @@ def psm_canon(v, q, s, C):
 
 
 def check(q, a, b):
-    """a, b: any 128-bit values"""
+    """a, b: any 128-bit values; the product takes b mod q (a twiddle is canonical), and the
+    butterfly (a + a w, a - a w forms: u = b, v = a, w = b mod q) takes the single-fold add / sub"""
     s, C = params(q)
     Q = q << s
-    for fn, ref in ((psm_add, a + b), (psm_sub, a - b), (psm_mul, a * b)):
+    for fn, ref in ((psm_add, a + b), (psm_sub, a - b)):
         r = fn(a, b, C)
         assert 0 <= r < R and (r - ref) % Q == 0, (fn.__name__, hex(q), hex(a), hex(b))
         assert psm_canon(r, q, s, C) == ref % q, ("canon", fn.__name__, hex(q), hex(a), hex(b))
+    for w in {b % q, q - 1, 1, 0}:
+        t = psm_mul(a, w, C)
+        assert 0 <= t < Q and (t - a * w) % Q == 0, ("mul", hex(q), hex(a), hex(w))
+        assert psm_canon(t, q, s, C) == (a * w) % q
+        for u in (a, b, R - 1, 0):
+            for fn, ref in ((psm_add1, u + t), (psm_sub1, u - t)):
+                r = fn(u, t, C)
+                assert 0 <= r < R and (r - ref) % Q == 0, (fn.__name__, hex(q), hex(u), hex(t))
 
 
 def edge_values(q):
