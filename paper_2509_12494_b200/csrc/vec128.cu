@@ -15,6 +15,7 @@
 #include "../../include/ntt128.h"
 #include "arith128.cuh"
 #include "barrett128.cuh"
+#include "psm128.cuh"
 #include "host128.h"
 #include "ntt128_internal.h"
 
@@ -35,11 +36,18 @@ struct VecConst {
     uint32_t a_m[4];  // axpy scalar, Montgomery form
     uint32_t r2[4];   // R^2 mod q
     BarrettC bc;      // q and mu' = floor(2^256 / q) - 2^128 (OP_MULB: q > 2^127)
+    uint32_t psm_s, psm_C;   // OP_MULP: s = 128 - bitlen(q), C = 2^128 - q 2^s (psm128.cuh)
 };
 
 // OP_MUL: two Montgomery products (any odd q); OP_MULB: one Barrett product (q > 2^127,
 // 43 word products instead of 72: barrett128.cuh).
-enum Op { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_AXPY = 3, OP_MULB = 4 };
+// OP_MULP: q = 2^b - c with c 2^(128-b) < 2^32 (pseudo-Mersenne, psm128.cuh): the 256-bit product
+// folds 2^128 = C modulo q 2^(128-b), 21 word products, then one canonicalisation.
+enum Op { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_AXPY = 3, OP_MULB = 4, OP_MULP = 5 };
+
+__device__ __forceinline__ U128 mul_p(const U128& a, const U128& b, const uint32_t q[4], uint32_t s, uint32_t C) {
+    return psm_canon(psm_mul(a, b, C), q, s, C);   // b < q (an input residue): the product is < Q
+}
 
 __device__ __forceinline__ U128 mul_b(const U128& a, const U128& b, const BarrettC& bc) {
     U128 r;
@@ -51,6 +59,9 @@ __device__ __forceinline__ U128 mul_b(const U128& a, const U128& b, const Barret
 // many small CTAs over several waves beat one wave of 4-residue threads -- a CTA that finishes
 // is replaced by one whose loads then overlap its neighbours' products.  mul keeps 2 residues
 // per thread (its 43-product Barrett needs the in-flight loads), add / sub / axpy take 1.
+#ifndef NTT_VEC_PSM
+#define NTT_VEC_PSM 1         // 0: vec128_mul never takes the pseudo-Mersenne product (A/B build)
+#endif
 #ifndef NTT_VEC_UNROLL_MUL
 #define NTT_VEC_UNROLL_MUL 2
 #endif
@@ -61,7 +72,7 @@ __device__ __forceinline__ U128 mul_b(const U128& a, const U128& b, const Barret
 #define NTT_VEC_CTAS_PER_SM 16
 #endif
 template <int OPK>
-constexpr int vec_unroll() { return (OPK == OP_MUL || OPK == OP_MULB) ? NTT_VEC_UNROLL_MUL : NTT_VEC_UNROLL; }
+constexpr int vec_unroll() { return (OPK == OP_MUL || OPK == OP_MULB || OPK == OP_MULP) ? NTT_VEC_UNROLL_MUL : NTT_VEC_UNROLL; }
 #ifndef NTT_VEC_THREADS
 #define NTT_VEC_THREADS 256
 #endif
@@ -90,6 +101,7 @@ __global__ void __launch_bounds__(THREADS) k_vec(uint4* z, const uint4* __restri
             else if (OPK == OP_SUB) r = sub_mod(a, b, c.q);
             else if (OPK == OP_MUL) r = mont_mul(mont_mul(a, b, c.q, c.qinv0), U128{{c.r2[0], c.r2[1], c.r2[2], c.r2[3]}}, c.q, c.qinv0);
             else if (OPK == OP_MULB) r = mul_b(a, b, c.bc);
+            else if (OPK == OP_MULP) r = mul_p(a, b, c.q, c.psm_s, c.psm_C);
             else r = add_mod(mont_mul(a, U128{{c.a_m[0], c.a_m[1], c.a_m[2], c.a_m[3]}}, c.q, c.qinv0), b, c.q);
             z[i + u * stride] = u128_to(r);
         }
@@ -100,6 +112,7 @@ __global__ void __launch_bounds__(THREADS) k_vec(uint4* z, const uint4* __restri
         else if (OPK == OP_SUB) r = sub_mod(a, b, c.q);
         else if (OPK == OP_MUL) r = mont_mul(mont_mul(a, b, c.q, c.qinv0), U128{{c.r2[0], c.r2[1], c.r2[2], c.r2[3]}}, c.q, c.qinv0);
         else if (OPK == OP_MULB) r = mul_b(a, b, c.bc);
+        else if (OPK == OP_MULP) r = mul_p(a, b, c.q, c.psm_s, c.psm_C);
         else r = add_mod(mont_mul(a, U128{{c.a_m[0], c.a_m[1], c.a_m[2], c.a_m[3]}}, c.q, c.qinv0), b, c.q);
         z[i] = u128_to(r);
     }
@@ -145,6 +158,7 @@ __device__ __forceinline__ U128 vec_op1(const U128& a, const U128& b, const VecC
     if (OPK == OP_SUB) return sub_mod(a, b, c.q);
     if (OPK == OP_MUL) return mont_mul(mont_mul(a, b, c.q, c.qinv0), U128{{c.r2[0], c.r2[1], c.r2[2], c.r2[3]}}, c.q, c.qinv0);
     if (OPK == OP_MULB) return mul_b(a, b, c.bc);
+    if (OPK == OP_MULP) return mul_p(a, b, c.q, c.psm_s, c.psm_C);
     return add_mod(mont_mul(a, U128{{c.a_m[0], c.a_m[1], c.a_m[2], c.a_m[3]}}, c.q, c.qinv0), b, c.q);
 }
 
@@ -291,6 +305,8 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
     ntt128_stream_gen(stream, &g0, &g1);   // NTT128_FLAG_CHAIN: other library work on the stream
     ntt128h::Mont M(q);
     VecConst c;
+    c.psm_s = 0;
+    c.psm_C = 0;
     words(q, c.q);
     c.qinv0 = (uint32_t)M.qp;
     words(M.r2, c.r2);
@@ -305,7 +321,17 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
 #else
     constexpr bool no_barrett = false;
 #endif
-    const bool barrett = (q >> 127) != 0 && !no_barrett;
+    // pseudo-Mersenne moduli (words 1..3 of q 2^s all ones, C != 2^32 - 1) take the folding product
+    bool psm = false;
+    if (NTT_VEC_PSM && op == OP_MUL) {
+        int s = 0;
+        while (((q << s) >> 127) == 0) s++;
+        const u128 Q = q << s;
+        psm = (Q >> 32) == (((u128)1 << 96) - 1) && (uint32_t)Q != 1u;
+        c.psm_s = (uint32_t)s;
+        c.psm_C = 0u - (uint32_t)Q;
+    }
+    const bool barrett = (q >> 127) != 0 && !no_barrett && !psm;
     if (barrett) {
         // mu = floor((2^256 - 1) / q) (= floor(2^256 / q), q odd) by restoring division
         u128 rem = 0, quo_lo = 0;
@@ -324,8 +350,7 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
     const uint4* x = (const uint4*)d_x;
     const uint4* y = (const uint4*)d_y;
     uint4* z = (uint4*)d_z;
-    const int opk_ = (op == OP_MUL && (q >> 127) != 0) ? OP_MULB : op;
-    const int grid = grid_for(n, (opk_ == OP_MUL || opk_ == OP_MULB) ? NTT_VEC_UNROLL_MUL : NTT_VEC_UNROLL);
+    const int grid = grid_for(n, op == OP_MUL ? NTT_VEC_UNROLL_MUL : NTT_VEC_UNROLL);
     if (flags & NTT128_FLAG_CHECK_INPUT) {
         int* d_err = nullptr;
         int h = 0;
@@ -346,7 +371,7 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
     constexpr int pipe_mask = NTT_VEC_PIPE_MASK;
 #endif
     const int opk = (op == OP_MUL && barrett) ? OP_MULB : op;
-    if ((pipe_mask >> opk) & 1) {
+    if (!psm && ((pipe_mask >> opk) & 1)) {
         cudaLaunchConfig_t pc;
         memset(&pc, 0, sizeof(pc));
         pc.stream = stream;
@@ -381,8 +406,9 @@ ntt128_status vec_op(int op, uint64_t* d_z, const uint64_t* d_x, const uint64_t*
         case OP_ADD: e = cudaLaunchKernelEx(&cfg, k_vec<OP_ADD, vec_unroll<OP_ADD>()>, z, x, y, (uint64_t)n, c); break;
         case OP_SUB: e = cudaLaunchKernelEx(&cfg, k_vec<OP_SUB, vec_unroll<OP_SUB>()>, z, x, y, (uint64_t)n, c); break;
         case OP_MUL:
-            e = barrett ? cudaLaunchKernelEx(&cfg, k_vec<OP_MULB, vec_unroll<OP_MULB>()>, z, x, y, (uint64_t)n, c)
-                        : cudaLaunchKernelEx(&cfg, k_vec<OP_MUL, vec_unroll<OP_MUL>()>, z, x, y, (uint64_t)n, c);
+            e = psm ? cudaLaunchKernelEx(&cfg, k_vec<OP_MULP, vec_unroll<OP_MULP>()>, z, x, y, (uint64_t)n, c)
+                : barrett ? cudaLaunchKernelEx(&cfg, k_vec<OP_MULB, vec_unroll<OP_MULB>()>, z, x, y, (uint64_t)n, c)
+                          : cudaLaunchKernelEx(&cfg, k_vec<OP_MUL, vec_unroll<OP_MUL>()>, z, x, y, (uint64_t)n, c);
             break;
         default: e = cudaLaunchKernelEx(&cfg, k_vec<OP_AXPY, vec_unroll<OP_AXPY>()>, z, x, y, (uint64_t)n, c); break;
     }

@@ -123,6 +123,24 @@ def test_pseudo_mersenne_class_structured(N, params, key):
         assert np.array_equal(to_host(plan.inverse(to_dev(y))), x)
 
 
+def test_arith_class_query(N, params):
+    """ntt128_plan_arith_class: pseudo-Mersenne only when EVERY modulus of a cyclic plan is
+    2^b - c with c 2^(128-b) < 2^32; one general prime puts the whole plan in the generic class
+    (both plans give the oracle's result either way)"""
+    a, b = params["cfg4"]["16"], params["extra"]["rand128_0"]
+    logn, n = 13, 1 << 13
+    wa, wb = sub_root(a, logn), sub_root(b, logn)
+    assert N.Plan(logn, a["q"], wa, batch=2).arith_class() == "pseudo_mersenne"
+    assert N.Plan(logn, b["q"], wb, batch=2).arith_class() == "montgomery"
+    qs, ws = [a["q"], b["q"]], [wa, wb]
+    plan = N.Plan(logn, qs, ws, batch=2)
+    assert plan.arith_class() == "montgomery"
+    x = np.stack([synth.uniform_residues(q, n, 950 + i).reshape(n, 2) for i, q in enumerate(qs)])
+    y = to_host(plan.forward(to_dev(x)))
+    assert np.array_equal(y, O.ntt(x, qs, ws))
+    assert np.array_equal(to_host(plan.inverse(to_dev(y))), x)
+
+
 def test_cfg1_full(N, params):
     """BASELINE cfg 1: N = 1024, one polynomial, forward + inverse, natural order"""
     e = params["cfg1"]
